@@ -1,0 +1,228 @@
+/*
+ * mobile.h -- C ABI of the B200-native MoBiLE MoE layer (libmobile.so).
+ *
+ * The reference (`moesim`, /root/reference/pkg/src/moesim) is pure Python with
+ * no FFI layer: its MoE block is inlined in `toymoe.forward`
+ * (toymoe.py:188-207) and the decision/plan/cache logic lives in policy.py and
+ * memory.py.  Each entry point below replaces one of those reference
+ * operations; the citation next to it names the reference code it stands in
+ * for.  The Python package `paper_2510_12357_b200` binds these with ctypes
+ * (see INTEGRATION.md for the binding a maintainer would add to `moesim`).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Device buffers are caller-owned; kernels
+ *    never allocate.  `stream` is a cudaStream_t passed as void*.
+ *  - Every function returns a status code (MOBILE_OK == 0); no exceptions
+ *    cross the ABI.  The Python layer maps codes back to the reference's
+ *    exception types and message substrings (ValueError "exceeds",
+ *    "finite", "empty", ...; CapacityDeadlock).
+ *  - Matrices are row-major.  Weights use the "out-major" layout
+ *    (rows = output features, contiguous over the input dimension), i.e. the
+ *    transpose of the reference's `h @ W` matrices.
+ *  - Determinism: no float atomics; every reduction has a fixed order.
+ */
+#ifndef MOBILE_H_
+#define MOBILE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define MOBILE_OK 0
+#define MOBILE_ERR_INVALID 1      /* bad argument / shape ("shape", "empty") */
+#define MOBILE_ERR_K_EXCEEDS 2    /* k > E  (toymoe.py:83-84 "exceeds")      */
+#define MOBILE_ERR_NONFINITE 3    /* non-finite logits (toymoe.py:85-86)     */
+#define MOBILE_ERR_CUDA 4         /* CUDA runtime error                      */
+#define MOBILE_ERR_DEADLOCK 5     /* CapacityDeadlock (memory.py:137-144)    */
+#define MOBILE_ERR_DEFERRED 6     /* speculative request deferred (None)     */
+#define MOBILE_ERR_UNSUPPORTED 7  /* shape/dtype outside the kernel's range  */
+#define MOBILE_ERR_NOT_FOUND 8    /* key not resident (KeyError)             */
+
+/* ---- dtypes / enums ---------------------------------------------------- */
+#define MOBILE_F32 0
+#define MOBILE_BF16 1
+#define MOBILE_F64 2
+
+#define MOBILE_ACT_RELU 0   /* toymoe.py:203  relu(h W_in) W_out        */
+#define MOBILE_ACT_SWIGLU 1 /* extension:     (silu(h W1) * h W3) W2    */
+
+#define MOBILE_GATE_SELECTED_SOFTMAX 0 /* toymoe.py:201 softmax(logits[sel]) */
+#define MOBILE_GATE_SOFTMAX_ALL 1      /* HF norm_topk_prob=False (extension) */
+
+#define MOBILE_STATUS_HIT 0       /* memory.py:20 */
+#define MOBILE_STATUS_IN_FLIGHT 1 /* memory.py:21 */
+#define MOBILE_STATUS_ISSUED 2    /* memory.py:22 */
+
+int mobile_version(void);
+const char* mobile_last_error(void);
+int mobile_num_sms(void);
+
+/* ---- router ------------------------------------------------------------
+ * Replaces toymoe.py:188-201 (h2 = LN(x); logits = h2 @ router; per-position
+ * top_k with the stable lower-index tie rule; final-position replay of
+ * recorded logits; gate softmax over the selected logits) for T tokens.
+ *   x        (T, d) f32 residual stream (LN is applied in-kernel)
+ *   h2_out   (T, d) f32 normalised activations (consumed by the experts)
+ *   w_router (E + n_extra, d) out-major router weight, w_dtype; rows E.. are
+ *            extra GEMV rows (e.g. Qwen's sigmoid shared-expert gate) whose
+ *            logits go to extra_out (T, n_extra) and never enter top-k
+ *   k_tok    (T,) int32 per-token width (little = k_little, big = k_big)
+ *   replay   (T, E) f32 recorded logits, used where replay_mask[t] != 0
+ *   logits_out (T, E) f32 own router logits (h_s rows)
+ *   idx_out  (T, k_max) int32 selection (descending), -1 beyond k_tok[t]
+ *   gates_out (T, k_max) f32 gate weights in selection order, 0 beyond k_tok
+ *   flags    (1,) int32 device word; bit 0 set if any logit was non-finite,
+ *            bit 1 if any k_tok[t] > E.  Caller zeroes it.
+ */
+int mobile_router_topk(const float* x, float* h2_out, const void* w_router, int w_dtype,
+                       int T, int d, int E, int n_extra, int k_max, const int* k_tok,
+                       const float* replay, const uint8_t* replay_mask, int reuse_gates,
+                       int gate_norm, float* logits_out, float* extra_out, int* idx_out,
+                       float* gates_out, int* flags, void* stream);
+
+/* Row-wise top-k (toymoe.py:80-88) over R rows of E logits (f32 or f64):
+ * used by top_k(), build_mobile_plan (policy.py:98-103) and
+ * selections_from_logits (engine.py:76-81). -0.0 ties +0.0; subnormals are
+ * ordered (no FTZ). */
+int mobile_topk_rows(const void* rows, int dtype, int R, int E, int k, int* idx_out, int* flags,
+                     void* stream);
+
+/* ---- head + confidence -------------------------------------------------
+ * Replaces toymoe.py:209-210 + 273 and policy.py:69-79 for T rows:
+ *   logits = LN(x[t]) @ head * logit_scale; conf[t] = max softmax(logits);
+ *   argmax[t] = first maximiser; fallback[t] = conf[t] <= gamma (strict >
+ *   accepts).  logits_out (T, V) may be NULL.  workspace >= head_ws_bytes.
+ */
+size_t mobile_head_ws_bytes(int T, int V);
+int mobile_head_confidence(const float* x, const void* w_head, int w_dtype, int T, int d, int V,
+                           float logit_scale, float gamma, float* logits_out, float* conf_out,
+                           int* argmax_out, uint8_t* fallback_out, void* workspace, void* stream);
+
+/* probs = softmax(logits) row-wise (toymoe.py:91-94), T rows of V; f32/f64
+ * in, f32/f64 out (f64 accumulation when either side is f64). */
+int mobile_softmax_rows(const void* logits, int in_dtype, void* probs, int out_dtype, int T, int V,
+                        void* stream);
+
+/* should_fallback on a caller-provided probability row (policy.py:69-79):
+ * out[0] = sum (f64), out[1] = max (f64); fallback = max <= gamma. */
+int mobile_probs_check(const void* probs, int dtype, int V, double* out, void* stream);
+
+/* ---- permute ------------------------------------------------------------
+ * Deterministic stable counting sort of (token, slot) pairs by expert
+ * (replaces the implicit token-major loop toymoe.py:193-204).
+ *   idx (T, k_max), k_tok (T,)
+ *   offsets (E+1): pairs of expert e are sorted_pairs[offsets[e]:offsets[e+1]]
+ *   sorted_pairs (T*k_max): pair id p = t*k_max + j, token-major within expert
+ *   active (E+1): active[0] = number of experts with >= 1 pair, then their ids
+ */
+int mobile_permute(const int* idx, const int* k_tok, int T, int k_max, int E, int* offsets,
+                   int* sorted_pairs, int* active, void* stream);
+
+/* ---- expert FFN (grouped, weight-streaming) -----------------------------
+ * toymoe.py:202-204 generalised.  Expert e's weights live at
+ *   w13 = w13_base + slot[e] * expert_stride   ((2I or I) x d, out-major;
+ *         SwiGLU rows are interleaved in groups of 16: 8 gate rows, 8 up rows)
+ *   w2  = w2_base  + slot[e] * expert_stride   (d x I, out-major)
+ * `slot` may be NULL (identity).  `max_active` bounds active[0] (host-known
+ * upper bound, sizes the grid).  `tok_div` maps pair id -> token (k_max).
+ *   gate_up: U[p, :I] = act(h2[p / tok_div] . W13)      (f32)
+ *   down:    Y[p, :d] = U[p] . W2                        (f32)
+ */
+int mobile_expert_gate_up(const float* h2, const int* offsets, const int* sorted_pairs,
+                          const int* active, int max_active, int max_tokens_per_expert, int tok_div,
+                          int d, int I, const void* w13_base, long long expert_stride,
+                          const int* slot, int w_dtype, int activation, float* U, void* stream);
+int mobile_expert_down(const float* U, const int* offsets, const int* sorted_pairs,
+                       const int* active, int max_active, int max_tokens_per_expert, int d, int I,
+                       const void* w2_base, long long expert_stride, const int* slot, int w_dtype,
+                       float* Y, void* stream);
+
+/* ---- combine -------------------------------------------------------------
+ * toymoe.py:192, 204, 207:  moe = sum_j gates[t,j] * Y[t*k_max + j] (selection
+ * order), then + shared (optionally sigmoid(shared_logit[t,s]) * Ys[t][s]),
+ * x_out[t] = x[t] + moe.  Y_shared is (T, n_shared, d) or NULL.
+ */
+int mobile_combine(const float* x, const float* Y, const float* gates, const int* k_tok, int T,
+                   int k_max, int d, const float* Y_shared, int n_shared,
+                   const float* shared_logits, float* x_out, void* stream);
+
+/* ---- expert cache core (memory.py:65-181 semantics) ----------------------
+ * LRU of (layer, expert) keys with pins, in-flight protection, speculative
+ * deferral, CapacityDeadlock.  Each resident entry owns a physical slot
+ * index in [0, slots).  Times are doubles: the simulator mirror passes the
+ * reference's clock; the device runtime passes a logical clock.
+ * If `channel` is non-NULL an issue completes at channel->issue(now)
+ * (memory.py:38-43); otherwise at `ready_if_issued`.
+ */
+typedef struct mobile_cache mobile_cache;
+typedef struct {
+  double t_xfer;
+  double busy_until;
+  long long transfers_issued;
+} mobile_channel;
+
+mobile_cache* mobile_cache_create(int slots);
+void mobile_cache_destroy(mobile_cache* c);
+int mobile_cache_request(mobile_cache* c, int layer, int expert, double now, int speculative,
+                         mobile_channel* channel, double ready_if_issued, int* status_out,
+                         double* ready_out, int* slot_out);
+int mobile_cache_pin(mobile_cache* c, int layer, int expert);
+int mobile_cache_unpin(mobile_cache* c, int layer, int expert);
+int mobile_cache_token_end(mobile_cache* c);
+/* evict the n LRU unpinned entries with ready <= now (now = +inf: only pins
+ * block); writes victims as (layer, expert) pairs; all-or-nothing. */
+int mobile_cache_evict_lru(mobile_cache* c, int n, double now, int* victims_out, int* n_out);
+int mobile_cache_size(const mobile_cache* c);
+int mobile_cache_contains(const mobile_cache* c, int layer, int expert);
+int mobile_cache_lookup(const mobile_cache* c, int layer, int expert, double* ready_out,
+                        int* slot_out);
+int mobile_cache_set_ready(mobile_cache* c, int layer, int expert, double ready);
+/* entries in LRU -> MRU order as (layer, expert) pairs; cap = pairs room */
+int mobile_cache_entries(const mobile_cache* c, int* out, int cap);
+/* stats: hits, coalesced, issued, evictions, deferrals */
+int mobile_cache_stats(const mobile_cache* c, long long* out5);
+
+/* ---- device expert store + copy engine ------------------------------------
+ * The engine.py:98-169 protocol on real hardware: an HBM slot pool, a pinned
+ * host store of every (layer, expert) in device layout, cudaMemcpyAsync on a
+ * side copy stream, one completion event per slot copy and one last-use event
+ * per slot on the compute stream (a slot is never overwritten while a kernel
+ * may still read it).  Cache decisions run through mobile_cache with a
+ * logical clock: an issued entry stays "in flight" until the compute stream
+ * has waited on it and the host has passed a sync point (mobile_offload_sync).
+ */
+typedef struct mobile_offload mobile_offload;
+mobile_offload* mobile_offload_create(int slots, long long expert_bytes, void* slot_pool,
+                                      const void* host_store, long long host_layer_stride,
+                                      long long host_expert_stride, int num_layers,
+                                      int num_experts, void* copy_stream);
+void mobile_offload_destroy(mobile_offload* o);
+/* Required loads for one layer (engine.py:137-145): request + pin each expert,
+ * issue copies for misses, make `compute_stream` wait on every copy, write the
+ * slot of each expert into slot_table_host[expert] (pinned, E ints). Counts
+ * fresh transfers in *issued_out. */
+int mobile_offload_require(mobile_offload* o, int layer, const int* experts, int n,
+                           void* compute_stream, int* slot_table_host, int* issued_out);
+/* Speculative prefetch (engine.py:98-119 _issue_window): returns DEFERRED
+ * when no victim exists. */
+int mobile_offload_prefetch(mobile_offload* o, int layer, int expert, int* status_out);
+/* After the layer's kernels are enqueued: record each slot's last-use event
+ * on compute_stream and unpin (engine.py:152-153). */
+int mobile_offload_release(mobile_offload* o, int layer, const int* experts, int n,
+                           void* compute_stream);
+/* Host passed a synchronisation point with compute_stream: entries it waited
+ * on are settled (logical clock advances). */
+int mobile_offload_sync(mobile_offload* o);
+int mobile_offload_token_end(mobile_offload* o);
+mobile_cache* mobile_offload_cache(mobile_offload* o);
+/* bytes copied H2D so far, transfers issued */
+int mobile_offload_counters(const mobile_offload* o, long long* out2);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOBILE_H_ */

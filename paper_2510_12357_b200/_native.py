@@ -1,0 +1,111 @@
+"""ctypes binding of libmobile.so (include/mobile.h).
+
+The CUDA extension is the product path: if it is missing or fails to load,
+importing the package's compute modules raises -- there is no CPU fallback.
+Status codes are mapped back to the reference's exception types and message
+substrings (toymoe.py:83-86, memory.py:137-144, memory.py:174-177).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("MOBILE_LIB", _PKG / "libmobile.so"))
+
+OK, ERR_INVALID, ERR_K_EXCEEDS, ERR_NONFINITE, ERR_CUDA, ERR_DEADLOCK, ERR_DEFERRED, ERR_UNSUPPORTED, ERR_NOT_FOUND = range(9)
+F32, BF16, F64 = 0, 1, 2
+ACT_RELU, ACT_SWIGLU = 0, 1
+GATE_SELECTED_SOFTMAX, GATE_SOFTMAX_ALL = 0, 1
+STATUS_NAMES = {0: "hit", 1: "in_flight", 2: "issued"}
+
+
+class MobileNativeError(RuntimeError):
+    """CUDA / unsupported-shape failure inside libmobile."""
+
+
+class CapacityDeadlock(RuntimeError):
+    """A required expert load found every cache slot pinned or in flight (memory.py:25-26)."""
+
+
+class mobile_channel(C.Structure):
+    _fields_ = [("t_xfer", C.c_double), ("busy_until", C.c_double), ("transfers_issued", C.c_longlong)]
+
+
+def _load():
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} not found: build the CUDA extension first "
+            f"(python -m paper_2510_12357_b200.build or __graft_entry__.build()); "
+            f"there is no CPU fallback")
+    return C.CDLL(str(LIB_PATH))
+
+
+lib = _load()
+
+P, I32, I64, F, D, SZ = C.c_void_p, C.c_int, C.c_longlong, C.c_float, C.c_double, C.c_size_t
+_SIGS = {
+    "mobile_version": ([], I32),
+    "mobile_last_error": ([], C.c_char_p),
+    "mobile_num_sms": ([], I32),
+    "mobile_router_topk": ([P, P, P, I32, I32, I32, I32, I32, I32, P, P, P, I32, I32, P, P, P, P, P, P], I32),
+    "mobile_topk_rows": ([P, I32, I32, I32, I32, P, P, P], I32),
+    "mobile_head_ws_bytes": ([I32, I32], SZ),
+    "mobile_head_confidence": ([P, P, I32, I32, I32, I32, F, F, P, P, P, P, P, P], I32),
+    "mobile_softmax_rows": ([P, I32, P, I32, I32, I32, P], I32),
+    "mobile_probs_check": ([P, I32, I32, P, P], I32),
+    "mobile_permute": ([P, P, I32, I32, I32, P, P, P, P], I32),
+    "mobile_expert_gate_up": ([P, P, P, P, I32, I32, I32, I32, I32, P, I64, P, I32, I32, P, P], I32),
+    "mobile_expert_down": ([P, P, P, P, I32, I32, I32, I32, P, I64, P, I32, P, P], I32),
+    "mobile_combine": ([P, P, P, P, I32, I32, I32, P, I32, P, P, P], I32),
+    "mobile_cache_create": ([I32], P),
+    "mobile_cache_destroy": ([P], None),
+    "mobile_cache_request": ([P, I32, I32, D, I32, P, D, P, P, P], I32),
+    "mobile_cache_pin": ([P, I32, I32], I32),
+    "mobile_cache_unpin": ([P, I32, I32], I32),
+    "mobile_cache_token_end": ([P], I32),
+    "mobile_cache_evict_lru": ([P, I32, D, P, P], I32),
+    "mobile_cache_size": ([P], I32),
+    "mobile_cache_contains": ([P, I32, I32], I32),
+    "mobile_cache_lookup": ([P, I32, I32, P, P], I32),
+    "mobile_cache_set_ready": ([P, I32, I32, D], I32),
+    "mobile_cache_entries": ([P, P, I32], I32),
+    "mobile_cache_stats": ([P, P], I32),
+    "mobile_offload_create": ([I32, I64, P, P, I64, I64, I32, I32, P], P),
+    "mobile_offload_destroy": ([P], None),
+    "mobile_offload_require": ([P, I32, P, I32, P, P, P], I32),
+    "mobile_offload_prefetch": ([P, I32, I32, P], I32),
+    "mobile_offload_release": ([P, I32, P, I32, P], I32),
+    "mobile_offload_sync": ([P], I32),
+    "mobile_offload_token_end": ([P], I32),
+    "mobile_offload_cache": ([P], P),
+    "mobile_offload_counters": ([P, P], I32),
+}
+EXPORTED = tuple(_SIGS)
+for _name, (_args, _ret) in _SIGS.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _ret
+
+
+def last_error() -> str:
+    return (lib.mobile_last_error() or b"").decode()
+
+
+def check(status: int, what: str = "") -> int:
+    """Raise the reference-compatible exception for a non-OK status."""
+    if status == OK:
+        return status
+    msg = last_error()
+    if status in (ERR_INVALID, ERR_K_EXCEEDS, ERR_NONFINITE, ERR_NOT_FOUND):
+        raise ValueError(msg or what)
+    if status == ERR_DEADLOCK:
+        raise CapacityDeadlock(msg)
+    raise MobileNativeError(f"{what}: {msg} (status {status})")
+
+
+def ptr(t) -> int | None:
+    """Raw device/host pointer of a torch tensor (None for None)."""
+    return None if t is None else t.data_ptr()

@@ -1,0 +1,206 @@
+// Device expert store + copy engine: the engine.py:98-169 protocol on real
+// hardware (HBM slot pool, pinned host store, cudaMemcpyAsync side stream).
+//
+// Cache decisions go through mobile_cache (memory.py semantics) driven by a
+// LOGICAL clock so that they are a deterministic function of the request
+// sequence, independent of copy timing:
+//   - a freshly issued entry is in flight (ready = +inf);
+//   - when a layer requires it, the compute stream waits on its copy event;
+//   - at the next host sync point with the compute stream (mobile_offload_sync)
+//     every entry the compute stream waited on is complete, so it settles at
+//     the current clock value, and the clock advances.
+// A slot is never overwritten while a kernel may still read it: each slot has
+// a last-use event recorded on the compute stream after the layer's expert
+// kernels, and a new copy into the slot waits on it first.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <limits>
+#include <vector>
+
+#include "../../include/mobile.h"
+
+namespace mobile {
+void set_error(const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* where);
+}  // namespace mobile
+
+struct mobile_offload {
+  mobile_cache* cache = nullptr;
+  int slots = 0;
+  long long expert_bytes = 0;
+  char* pool = nullptr;
+  const char* host = nullptr;
+  long long layer_stride = 0, expert_stride = 0;
+  int L = 0, E = 0;
+  cudaStream_t copy = nullptr;
+  std::vector<cudaEvent_t> copy_done, last_use;
+  std::vector<char> last_use_valid;
+  std::vector<int> slot_layer, slot_expert;  // occupant of each slot (-1 = none)
+  double clock = 0.0;
+  std::vector<std::pair<int, int>> awaited;   // waited on since the last sync
+  long long bytes = 0, transfers = 0;
+};
+
+static const double kInf = std::numeric_limits<double>::infinity();
+
+#define OFF_CUDA(call, where)                                         \
+  do {                                                                \
+    cudaError_t _e = (call);                                          \
+    if (_e != cudaSuccess) return mobile::cuda_status(_e, where);     \
+  } while (0)
+
+static int issue_copy(mobile_offload* o, int layer, int expert, int slot) {
+  if (o->last_use_valid[slot]) OFF_CUDA(cudaStreamWaitEvent(o->copy, o->last_use[slot], 0), "copy wait last-use");
+  const char* src = o->host + (long long)layer * o->layer_stride + (long long)expert * o->expert_stride;
+  char* dst = o->pool + (long long)slot * o->expert_bytes;
+  OFF_CUDA(cudaMemcpyAsync(dst, src, (size_t)o->expert_bytes, cudaMemcpyHostToDevice, o->copy), "expert H2D");
+  OFF_CUDA(cudaEventRecord(o->copy_done[slot], o->copy), "copy event");
+  o->slot_layer[slot] = layer;
+  o->slot_expert[slot] = expert;
+  o->bytes += o->expert_bytes;
+  o->transfers++;
+  return MOBILE_OK;
+}
+
+extern "C" {
+
+mobile_offload* mobile_offload_create(int slots, long long expert_bytes, void* slot_pool,
+                                      const void* host_store, long long host_layer_stride,
+                                      long long host_expert_stride, int num_layers, int num_experts,
+                                      void* copy_stream) {
+  if (slots < 1 || expert_bytes <= 0 || !slot_pool || !host_store) {
+    mobile::set_error("offload: bad arguments (slots=%d bytes=%lld)", slots, expert_bytes);
+    return nullptr;
+  }
+  auto* o = new mobile_offload();
+  o->cache = mobile_cache_create(slots);
+  o->slots = slots;
+  o->expert_bytes = expert_bytes;
+  o->pool = (char*)slot_pool;
+  o->host = (const char*)host_store;
+  o->layer_stride = host_layer_stride;
+  o->expert_stride = host_expert_stride;
+  o->L = num_layers;
+  o->E = num_experts;
+  o->copy = (cudaStream_t)copy_stream;
+  o->copy_done.resize(slots);
+  o->last_use.resize(slots);
+  o->last_use_valid.assign(slots, 0);
+  o->slot_layer.assign(slots, -1);
+  o->slot_expert.assign(slots, -1);
+  for (int s = 0; s < slots; ++s) {
+    if (cudaEventCreateWithFlags(&o->copy_done[s], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&o->last_use[s], cudaEventDisableTiming) != cudaSuccess) {
+      mobile::set_error("offload: cudaEventCreate failed");
+      return nullptr;
+    }
+  }
+  return o;
+}
+
+void mobile_offload_destroy(mobile_offload* o) {
+  if (!o) return;
+  for (auto e : o->copy_done) cudaEventDestroy(e);
+  for (auto e : o->last_use) cudaEventDestroy(e);
+  mobile_cache_destroy(o->cache);
+  delete o;
+}
+
+static int settle(mobile_offload* o) {
+  o->clock += 1.0;
+  for (auto& k : o->awaited) {
+    double r;
+    if (mobile_cache_lookup(o->cache, k.first, k.second, &r, nullptr) == MOBILE_OK && r == kInf)
+      mobile_cache_set_ready(o->cache, k.first, k.second, o->clock);
+  }
+  o->awaited.clear();
+  return MOBILE_OK;
+}
+
+int mobile_offload_require(mobile_offload* o, int layer, const int* experts, int n,
+                           void* compute_stream, int* slot_table_host, int* issued_out) {
+  cudaStream_t cs = (cudaStream_t)compute_stream;
+  int fresh = 0;
+  for (int i = 0; i < n; ++i) {
+    const int e = experts[i];
+    int status = 0, slot = -1;
+    double ready = 0;
+    int st = mobile_cache_request(o->cache, layer, e, o->clock, 0, nullptr, kInf, &status, &ready, &slot);
+    if (st == MOBILE_ERR_DEADLOCK && !o->awaited.empty()) {
+      // every slot is pinned or in flight: stall until the compute stream has
+      // consumed what it waited on, settle, and retry (the simulator's stall)
+      OFF_CUDA(cudaStreamSynchronize(cs), "deadlock stall");
+      settle(o);
+      st = mobile_cache_request(o->cache, layer, e, o->clock, 0, nullptr, kInf, &status, &ready, &slot);
+    }
+    if (st != MOBILE_OK) return st;
+    if (status == MOBILE_STATUS_ISSUED) {
+      int r = issue_copy(o, layer, e, slot);
+      if (r) return r;
+      ++fresh;
+    }
+    mobile_cache_pin(o->cache, layer, e);
+    if (ready == kInf) {
+      OFF_CUDA(cudaStreamWaitEvent(cs, o->copy_done[slot], 0), "compute wait copy");
+      o->awaited.emplace_back(layer, e);
+    }
+    if (slot_table_host) slot_table_host[e] = slot;
+  }
+  if (issued_out) *issued_out = fresh;
+  return MOBILE_OK;
+}
+
+int mobile_offload_prefetch(mobile_offload* o, int layer, int expert, int* status_out) {
+  int status = 0, slot = -1;
+  double ready = 0;
+  int st = mobile_cache_request(o->cache, layer, expert, o->clock, 1, nullptr, kInf, &status, &ready, &slot);
+  if (st != MOBILE_OK) return st;  // DEFERRED: retry at the next boundary
+  if (status == MOBILE_STATUS_ISSUED) {
+    int r = issue_copy(o, layer, expert, slot);
+    if (r) return r;
+  }
+  if (status_out) *status_out = status;
+  return MOBILE_OK;
+}
+
+int mobile_offload_release(mobile_offload* o, int layer, const int* experts, int n, void* compute_stream) {
+  cudaStream_t cs = (cudaStream_t)compute_stream;
+  for (int i = 0; i < n; ++i) {
+    int slot = -1;
+    if (mobile_cache_lookup(o->cache, layer, experts[i], nullptr, &slot) == MOBILE_OK) {
+      OFF_CUDA(cudaEventRecord(o->last_use[slot], cs), "last-use event");
+      o->last_use_valid[slot] = 1;
+    }
+    mobile_cache_unpin(o->cache, layer, experts[i]);
+  }
+  return MOBILE_OK;
+}
+
+int mobile_offload_sync(mobile_offload* o) { return settle(o); }
+
+int mobile_offload_token_end(mobile_offload* o) {
+  // Prefetches never consumed by a layer are drained here so no entry stays
+  // in flight across tokens (deterministic: the copy stream is synchronised).
+  OFF_CUDA(cudaStreamSynchronize(o->copy), "token_end drain");
+  o->clock += 1.0;
+  std::vector<int> buf(2 * (size_t)o->slots);
+  const int n = mobile_cache_entries(o->cache, buf.data(), o->slots);
+  for (int i = 0; i < n; ++i) {
+    double r;
+    if (mobile_cache_lookup(o->cache, buf[2 * i], buf[2 * i + 1], &r, nullptr) == MOBILE_OK && r == kInf)
+      mobile_cache_set_ready(o->cache, buf[2 * i], buf[2 * i + 1], o->clock);
+  }
+  o->awaited.clear();
+  return mobile_cache_token_end(o->cache);
+}
+
+mobile_cache* mobile_offload_cache(mobile_offload* o) { return o->cache; }
+
+int mobile_offload_counters(const mobile_offload* o, long long* out2) {
+  out2[0] = o->bytes;
+  out2[1] = o->transfers;
+  return MOBILE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+// Deterministic token permute (counting sort of (token, slot) pairs by expert)
+// and the weighted combine.  Replaces the implicit per-position loop of
+// toymoe.py:193-204 and the accumulation/residual of toymoe.py:192, 204, 207.
+#include "common.cuh"
+
+namespace mobile {
+
+constexpr int kPermThreads = 1024;
+constexpr int kPermWarps = kPermThreads / 32;
+constexpr int kPermMaxE = 256;
+
+// One CTA.  Pass 1 counts pairs per expert; an exclusive scan gives offsets;
+// pass 2 places pairs chunk by chunk: within a warp `match.any` ranks equal
+// experts by lane, across warps a per-warp count table ranks by warp, across
+// chunks a running base.  The order inside every expert list is therefore
+// pair order (token-major, then selection slot): stable and deterministic.
+__global__ void __launch_bounds__(kPermThreads) permute_kernel(const int* __restrict__ idx,
+                                                               const int* __restrict__ k_tok, int T,
+                                                               int k_max, int E, int* offsets,
+                                                               int* sorted_pairs, int* active) {
+  __shared__ int cnt[kPermMaxE];
+  __shared__ int base[kPermMaxE];
+  __shared__ int wcnt[kPermWarps][kPermMaxE];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int P = T * k_max;
+  for (int e = tid; e < E; e += kPermThreads) cnt[e] = 0;
+  for (int i = tid; i < kPermWarps * E; i += kPermThreads) wcnt[i / E][i % E] = 0;
+  __syncthreads();
+  for (int p = tid; p < P; p += kPermThreads) {
+    const int t = p / k_max, j = p - t * k_max;
+    const int kt = k_tok ? k_tok[t] : k_max;
+    const int e = j < kt ? idx[p] : -1;
+    if (e >= 0 && e < E) atomicAdd(&cnt[e], 1);  // integer count: order-free
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int run = 0, na = 0;
+    for (int e = 0; e < E; ++e) {
+      offsets[e] = run;
+      base[e] = run;
+      run += cnt[e];
+      if (cnt[e] > 0) active[1 + na++] = e;
+    }
+    offsets[E] = run;
+    active[0] = na;
+  }
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int c = 0; c < P; c += kPermThreads) {
+    const int p = c + tid;
+    int e = -1;
+    if (p < P) {
+      const int t = p / k_max, j = p - t * k_max;
+      const int kt = k_tok ? k_tok[t] : k_max;
+      e = j < kt ? idx[p] : -1;
+      if (e >= E) e = -1;
+    }
+    const unsigned m = __match_any_sync(0xffffffffu, e);
+    const int rank = __popc(m & lt);
+    if (e >= 0 && rank == 0) wcnt[warp][e] = __popc(m);
+    __syncthreads();
+    if (e >= 0) {
+      int pos = base[e] + rank;
+      for (int w = 0; w < warp; ++w) pos += wcnt[w][e];
+      sorted_pairs[pos] = p;
+    }
+    __syncthreads();
+    for (int e2 = tid; e2 < E; e2 += kPermThreads) {
+      int s = 0;
+      for (int w = 0; w < kPermWarps; ++w) { s += wcnt[w][e2]; wcnt[w][e2] = 0; }
+      base[e2] += s;
+    }
+    __syncthreads();
+  }
+}
+
+// x_out[t] = x[t] + (sum_j g[t,j] * Y[t*k+j]  (selection order)
+//                    + sum_s gate_s(t) * Ys[t][s])          toymoe.py:204, 207
+__global__ void combine_kernel(const float* __restrict__ x, const float* __restrict__ Y,
+                               const float* __restrict__ gates, const int* __restrict__ k_tok,
+                               int k_max, int d, const float* __restrict__ Ys, int n_shared,
+                               const float* __restrict__ shared_logits, int T,
+                               float* __restrict__ x_out) {
+  const int t = blockIdx.x;
+  const int kt = k_tok ? k_tok[t] : k_max;
+  const float* g = gates + (size_t)t * k_max;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    float m = 0.f;
+    for (int j = 0; j < kt; ++j) m = fmaf(g[j], Y[((size_t)t * k_max + j) * d + i], m);
+    for (int s = 0; s < n_shared; ++s) {
+      float ys = Ys[((size_t)t * n_shared + s) * d + i];
+      if (shared_logits) ys = sigmoid_f(shared_logits[(size_t)t * n_shared + s]) * ys;
+      m += ys;
+    }
+    x_out[(size_t)t * d + i] = x[(size_t)t * d + i] + m;
+  }
+}
+
+}  // namespace mobile
+
+using namespace mobile;
+
+extern "C" int mobile_permute(const int* idx, const int* k_tok, int T, int k_max, int E, int* offsets,
+                              int* sorted_pairs, int* active, void* stream) {
+  if (T < 0 || k_max <= 0 || E <= 0) { set_error("permute: bad shape T=%d k=%d E=%d", T, k_max, E); return MOBILE_ERR_INVALID; }
+  if (E > kPermMaxE) { set_error("permute: E=%d exceeds %d", E, kPermMaxE); return MOBILE_ERR_UNSUPPORTED; }
+  permute_kernel<<<1, kPermThreads, 0, (cudaStream_t)stream>>>(idx, k_tok, T, k_max, E, offsets,
+                                                              sorted_pairs, active);
+  MOBILE_CHECK_LAUNCH("permute");
+  return MOBILE_OK;
+}
+
+extern "C" int mobile_combine(const float* x, const float* Y, const float* gates, const int* k_tok,
+                              int T, int k_max, int d, const float* Y_shared, int n_shared,
+                              const float* shared_logits, float* x_out, void* stream) {
+  if (T < 0 || d <= 0 || k_max <= 0 || n_shared < 0) { set_error("combine: bad shape"); return MOBILE_ERR_INVALID; }
+  if (T == 0) return MOBILE_OK;
+  combine_kernel<<<T, 256, 0, (cudaStream_t)stream>>>(x, Y, gates, k_tok, k_max, d, Y_shared,
+                                                      Y_shared ? n_shared : 0, shared_logits, T, x_out);
+  MOBILE_CHECK_LAUNCH("combine");
+  return MOBILE_OK;
+}

@@ -1,0 +1,150 @@
+"""Thin torch-tensor wrappers over the libmobile C ABI.
+
+Tensors must already live on the CUDA device (the C ABI takes raw pointers);
+every call is enqueued on the current torch stream unless `stream` is given.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _native as N
+
+_DT = {torch.float32: N.F32, torch.bfloat16: N.BF16, torch.float64: N.F64}
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise N.MobileNativeError(f"unsupported dtype {t.dtype}") from None
+
+
+def _s(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _dev(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise N.MobileNativeError("libmobile kernels take CUDA tensors only (no CPU fallback)")
+
+
+def router_topk(x, w_router, E, k_max, k_tok, *, n_extra=0, replay=None, replay_mask=None,
+                reuse_gates=False, gate_norm=N.GATE_SELECTED_SOFTMAX, out=None, stream=None):
+    """Fused LN + router GEMV + top-k + replay + gates (toymoe.py:188-201)."""
+    _dev(x, w_router, k_tok, replay, replay_mask)
+    T, d = x.shape
+    dev = x.device
+    if out is None:
+        out = dict(
+            h2=torch.empty(T, d, device=dev, dtype=torch.float32),
+            logits=torch.empty(T, E, device=dev, dtype=torch.float32),
+            extra=torch.empty(T, max(n_extra, 1), device=dev, dtype=torch.float32),
+            idx=torch.empty(T, k_max, device=dev, dtype=torch.int32),
+            gates=torch.empty(T, k_max, device=dev, dtype=torch.float32),
+            flags=torch.zeros(1, device=dev, dtype=torch.int32),
+        )
+    st = N.lib.mobile_router_topk(
+        N.ptr(x), N.ptr(out["h2"]), N.ptr(w_router), dtype_code(w_router), T, d, E, n_extra, k_max,
+        N.ptr(k_tok), N.ptr(replay), N.ptr(replay_mask), int(bool(reuse_gates)), gate_norm,
+        N.ptr(out["logits"]), N.ptr(out["extra"]) if n_extra else None, N.ptr(out["idx"]),
+        N.ptr(out["gates"]), N.ptr(out["flags"]), _s(stream))
+    N.check(st, "router_topk")
+    return out
+
+
+def topk_rows(rows: torch.Tensor, k: int, stream=None):
+    """Stable top-k per row (toymoe.py:80-88) -> (idx (R,k) int32, flags (1,) int32)."""
+    _dev(rows)
+    rows = rows.contiguous()
+    R, E = rows.shape
+    idx = torch.empty(R, max(k, 0), device=rows.device, dtype=torch.int32)
+    flags = torch.zeros(1, device=rows.device, dtype=torch.int32)
+    N.check(N.lib.mobile_topk_rows(N.ptr(rows), dtype_code(rows), R, E, k, N.ptr(idx), N.ptr(flags), _s(stream)),
+            "topk_rows")
+    return idx, flags
+
+
+class HeadWorkspace:
+    def __init__(self, T: int, V: int, device):
+        n = int(N.lib.mobile_head_ws_bytes(T, V))
+        self.buf = torch.zeros(n, dtype=torch.uint8, device=device)  # ticket words start (and stay) 0
+        self.T, self.V = T, V
+
+
+def head_confidence(x, w_head, gamma, logit_scale, *, ws: HeadWorkspace, logits_out=None, out=None,
+                    stream=None):
+    """conf = max softmax(LN(x) @ head * scale), first argmax, fallback = conf <= gamma."""
+    _dev(x, w_head)
+    T, d = x.shape
+    V = w_head.shape[0]
+    if ws.T < T or ws.V != V:
+        raise N.MobileNativeError("head workspace too small")
+    if out is None:
+        out = dict(conf=torch.empty(T, device=x.device, dtype=torch.float32),
+                   argmax=torch.empty(T, device=x.device, dtype=torch.int32),
+                   fallback=torch.empty(T, device=x.device, dtype=torch.uint8))
+    N.check(N.lib.mobile_head_confidence(
+        N.ptr(x), N.ptr(w_head), dtype_code(w_head), T, d, V, float(logit_scale), float(gamma),
+        N.ptr(logits_out), N.ptr(out["conf"]), N.ptr(out["argmax"]), N.ptr(out["fallback"]),
+        N.ptr(ws.buf), _s(stream)), "head_confidence")
+    return out
+
+
+def softmax_rows(logits: torch.Tensor, out_dtype=torch.float64, stream=None):
+    _dev(logits)
+    logits = logits.contiguous()
+    T, V = logits.shape
+    probs = torch.empty(T, V, device=logits.device, dtype=out_dtype)
+    N.check(N.lib.mobile_softmax_rows(N.ptr(logits), dtype_code(logits), N.ptr(probs), dtype_code(probs),
+                                      T, V, _s(stream)), "softmax_rows")
+    return probs
+
+
+def probs_check(probs: torch.Tensor, stream=None):
+    """(sum, max) of a probability row in f64 (policy.py:69-79 inputs)."""
+    _dev(probs)
+    out = torch.empty(2, device=probs.device, dtype=torch.float64)
+    N.check(N.lib.mobile_probs_check(N.ptr(probs.contiguous()), dtype_code(probs), probs.numel(), N.ptr(out),
+                                     _s(stream)), "probs_check")
+    return out
+
+
+def permute(idx, k_tok, E, out=None, stream=None):
+    _dev(idx, k_tok)
+    T, k_max = idx.shape
+    dev = idx.device
+    if out is None:
+        out = dict(offsets=torch.empty(E + 1, device=dev, dtype=torch.int32),
+                   sorted_pairs=torch.empty(max(T * k_max, 1), device=dev, dtype=torch.int32),
+                   active=torch.empty(E + 1, device=dev, dtype=torch.int32))
+    N.check(N.lib.mobile_permute(N.ptr(idx), N.ptr(k_tok), T, k_max, E, N.ptr(out["offsets"]),
+                                 N.ptr(out["sorted_pairs"]), N.ptr(out["active"]), _s(stream)), "permute")
+    return out
+
+
+def expert_gate_up(h2, offsets, sorted_pairs, active, max_active, max_tok, tok_div, d, I, w13_base_ptr,
+                   expert_stride, slot, w_dtype, activation, U, stream=None):
+    N.check(N.lib.mobile_expert_gate_up(
+        N.ptr(h2), N.ptr(offsets), N.ptr(sorted_pairs), N.ptr(active), int(max_active), int(max_tok),
+        int(tok_div), d, I, w13_base_ptr, int(expert_stride), N.ptr(slot), w_dtype, activation, N.ptr(U),
+        _s(stream)), "expert_gate_up")
+
+
+def expert_down(U, offsets, sorted_pairs, active, max_active, max_tok, d, I, w2_base_ptr, expert_stride, slot,
+                w_dtype, Y, stream=None):
+    N.check(N.lib.mobile_expert_down(
+        N.ptr(U), N.ptr(offsets), N.ptr(sorted_pairs), N.ptr(active), int(max_active), int(max_tok), d, I,
+        w2_base_ptr, int(expert_stride), N.ptr(slot), w_dtype, N.ptr(Y), _s(stream)), "expert_down")
+
+
+def combine(x, Y, gates, k_tok, Y_shared=None, n_shared=0, shared_logits=None, x_out=None, stream=None):
+    T, d = x.shape
+    k_max = gates.shape[1]
+    if x_out is None:
+        x_out = torch.empty_like(x)
+    N.check(N.lib.mobile_combine(N.ptr(x), N.ptr(Y), N.ptr(gates), N.ptr(k_tok), T, k_max, d, N.ptr(Y_shared),
+                                 int(n_shared), N.ptr(shared_logits), N.ptr(x_out), _s(stream)), "combine")
+    return x_out

@@ -1,0 +1,289 @@
+"""Device model: the MoBiLE MoE layer (carved out of toymoe.py:188-207) plus
+the surrounding decoder (attention, head) that feeds it.
+
+`MoBiLEMoE.forward` is the hot path: fused router/top-k/replay (libmobile
+router kernel) -> deterministic permute -> grouped expert GEMVs (gate-up,
+down) -> shared experts -> weighted combine + residual.  Attention, embedding
+and the KV cache are plumbing done with torch tensor ops on the device
+(attention is out of scope for custom kernels).
+
+Two execution modes share these kernels:
+  * recompute (`forward_recompute`): the reference's semantics -- the whole
+    sequence is recomputed at the pass width, replay only at the final
+    position (toymoe.py:143-210).  Used by the drop-in `forward`/`generate`.
+  * KV-cached decode (`DecodeSession`): one position per step; a position's
+    K/V come from the pass whose output was accepted (big overwrites).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+import torch.nn.functional as Fn
+
+from . import _native as N
+from . import kernels as K
+from .spec import ModelSpec
+from .weights import DeviceWeights
+
+torch.backends.cuda.matmul.allow_tf32 = False
+torch.backends.cudnn.allow_tf32 = False
+
+_ACT = {"relu": N.ACT_RELU, "swiglu": N.ACT_SWIGLU}
+_GATE = {"selected_softmax": N.GATE_SELECTED_SOFTMAX, "softmax_all": N.GATE_SOFTMAX_ALL}
+
+
+def positional(n: int, d: int, start: int, device) -> torch.Tensor:
+    """Sinusoidal encoding, toymoe.py:135-140 (computed in fp64, stored f32)."""
+    pos = torch.arange(start, start + n, device=device, dtype=torch.float64)[:, None]
+    dim = torch.arange(d, device=device, dtype=torch.float64)[None, :]
+    angle = pos / torch.pow(torch.tensor(10000.0, dtype=torch.float64, device=device), (2 * (dim // 2)) / d)
+    return torch.where(dim.long() % 2 == 0, torch.sin(angle), torch.cos(angle)).to(torch.float32)
+
+
+class ExpertLocation:
+    """Where a layer's routed experts live: resident tensor or cache slot pool."""
+
+    def __init__(self, w13_base: int, w2_base: int, stride: int, slot: torch.Tensor | None):
+        self.w13_base, self.w2_base, self.stride, self.slot = w13_base, w2_base, stride, slot
+
+
+class MoBiLEMoE:
+    """The MoBiLE MoE layer on the device (all layers of one model)."""
+
+    def __init__(self, dw: DeviceWeights):
+        self.dw = dw
+        s = dw.spec
+        self.spec = s
+        self.E, self.d, self.I = s.num_experts, s.hidden_dim, s.ffn
+        self.S, self.Is = s.n_shared, s.shared_ffn
+        self.wcode = K.dtype_code(torch.empty(0, dtype=dw.wdtype))
+        self.act = _ACT[s.activation]
+        self.gate_norm = _GATE[s.gate_norm]
+        self._scratch: dict = {}
+
+    def resident(self, layer: int) -> ExpertLocation:
+        dw = self.dw
+        base = dw.experts[layer].data_ptr()
+        return ExpertLocation(base, base + dw.w13_elems * dw.elem_bytes, dw.expert_bytes, None)
+
+    def scratch(self, T: int, k_max: int) -> dict:
+        key = (T, k_max)
+        sc = self._scratch.get(key)
+        if sc is not None:
+            return sc
+        dev, E, d = self.dw.device, self.E, self.d
+        f32, i32 = torch.float32, torch.int32
+        ne = max(self.dw.n_gate_rows, 1)
+        sc = dict(
+            router=dict(h2=torch.empty(T, d, device=dev, dtype=f32), logits=torch.empty(T, E, device=dev, dtype=f32),
+                        extra=torch.empty(T, ne, device=dev, dtype=f32), idx=torch.empty(T, k_max, device=dev, dtype=i32),
+                        gates=torch.empty(T, k_max, device=dev, dtype=f32), flags=torch.zeros(1, device=dev, dtype=i32)),
+            perm=dict(offsets=torch.empty(E + 1, device=dev, dtype=i32),
+                      sorted_pairs=torch.empty(T * k_max, device=dev, dtype=i32),
+                      active=torch.empty(E + 1, device=dev, dtype=i32)),
+            U=torch.empty(T * k_max, self.I, device=dev, dtype=f32),
+            Y=torch.empty(T * k_max, d, device=dev, dtype=f32),
+            x_out=torch.empty(T, d, device=dev, dtype=f32),
+        )
+        if self.S:
+            S = self.S
+            sc["s_offsets"] = torch.arange(0, (S + 1) * T, T, device=dev, dtype=i32)
+            # expert s's pairs are t*S + s for t = 0..T-1 (token-major)
+            sc["s_pairs"] = (torch.arange(T, device=dev, dtype=i32)[None, :] * S +
+                             torch.arange(S, device=dev, dtype=i32)[:, None]).reshape(-1).contiguous()
+            sc["s_active"] = torch.cat([torch.tensor([S], dtype=i32), torch.arange(S, dtype=i32)]).to(dev)
+            sc["Us"] = torch.empty(T * S, self.Is, device=dev, dtype=f32)
+            sc["Ys"] = torch.empty(T * S, d, device=dev, dtype=f32)
+        self._scratch[key] = sc
+        return sc
+
+    def forward(self, x: torch.Tensor, layer: int, k_tok: torch.Tensor, k_max: int, *, replay=None,
+                replay_mask=None, reuse_gates=False, experts: ExpertLocation | None = None,
+                pre_experts=None):
+        """x (T, d) f32 residual -> (x_out, scratch).  `pre_experts(idx)` is an
+        optional hook run between routing and the expert kernels (the offload
+        runtime uses it to make the selected experts resident)."""
+        T = x.shape[0]
+        dw, E, d = self.dw, self.E, self.d
+        sc = self.scratch(T, k_max)
+        r = K.router_topk(x, dw.router[layer], E, k_max, k_tok, n_extra=dw.n_gate_rows, replay=replay,
+                          replay_mask=replay_mask, reuse_gates=reuse_gates, gate_norm=self.gate_norm,
+                          out=sc["router"])
+        p = K.permute(r["idx"], k_tok, E, out=sc["perm"])
+        if pre_experts is not None:
+            experts = pre_experts(layer, r, p)
+        loc = experts if experts is not None else self.resident(layer)
+        max_active = min(E, T * k_max)
+        K.expert_gate_up(r["h2"], p["offsets"], p["sorted_pairs"], p["active"], max_active, T, k_max, d, self.I,
+                         loc.w13_base, loc.stride, loc.slot, self.wcode, self.act, sc["U"])
+        K.expert_down(sc["U"], p["offsets"], p["sorted_pairs"], p["active"], max_active, T, d, self.I,
+                      loc.w2_base, loc.stride, loc.slot, self.wcode, sc["Y"])
+        Ys = None
+        if self.S:
+            sh = dw.shared[layer]
+            base = sh.data_ptr()
+            sb = dw.shared_bytes
+            K.expert_gate_up(r["h2"], sc["s_offsets"], sc["s_pairs"], sc["s_active"], self.S, T, self.S, d, self.Is,
+                             base, sb, None, self.wcode, self.act, sc["Us"])
+            K.expert_down(sc["Us"], sc["s_offsets"], sc["s_pairs"], sc["s_active"], self.S, T, d, self.Is,
+                          base + dw.s_w13_elems * dw.elem_bytes, sb, None, self.wcode, sc["Ys"])
+            Ys = sc["Ys"]
+        shared_logits = r["extra"] if dw.n_gate_rows else None
+        K.combine(x, sc["Y"], r["gates"], k_tok, Ys, self.S, shared_logits, x_out=sc["x_out"])
+        return sc["x_out"], sc
+
+
+class DeviceModel:
+    """Decoder around the MoBiLE layer (recompute and KV-cached modes)."""
+
+    def __init__(self, dw: DeviceWeights):
+        self.dw = dw
+        self.spec: ModelSpec = dw.spec
+        self.moe = MoBiLEMoE(dw)
+        self.device = dw.device
+        self.head_ws: dict = {}
+
+    # ------------------------------------------------------------- pieces
+    def _mm(self, h: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+        if w.dtype == torch.float32:
+            return h @ w
+        return (h.to(w.dtype) @ w).to(torch.float32)
+
+    def attention_full(self, x: torch.Tensor, layer: int) -> torch.Tensor:
+        """toymoe.py:178-186 over all n positions (causal), n_heads generalised."""
+        dw, s = self.dw, self.spec
+        n, d = x.shape
+        h = Fn.layer_norm(x, (d,), eps=1e-5)
+        q, k, v = self._mm(h, dw.q[layer]), self._mm(h, dw.k[layer]), self._mm(h, dw.v[layer])
+        H = s.n_heads
+        hd = d // H
+        qh, kh, vh = (t.view(n, H, hd).transpose(0, 1) for t in (q, k, v))
+        scores = (qh @ kh.transpose(1, 2)) / math.sqrt(hd)
+        mask = torch.ones(n, n, dtype=torch.bool, device=x.device).triu(1)
+        scores = scores.masked_fill(mask, float("-inf"))
+        attn = torch.softmax(scores, dim=-1)
+        out = (attn @ vh).transpose(0, 1).reshape(n, d)
+        return x + self._mm(out, dw.o[layer])
+
+    def head_workspace(self, T: int) -> K.HeadWorkspace:
+        ws = self.head_ws.get(T)
+        if ws is None:
+            ws = self.head_ws[T] = K.HeadWorkspace(T, self.spec.vocab_size, self.device)
+        return ws
+
+    # ------------------------------------------------------------- recompute
+    def forward_recompute(self, tokens, k: int, replay_states=None, reuse_gates=False):
+        """toymoe.forward on the device.  Returns device tensors
+        (probs f64 (V,), states f32 (L, E), selections int32 (L, k), flags)."""
+        s, dw = self.spec, self.dw
+        dev = self.device
+        n = len(tokens)
+        tok = torch.as_tensor(np.asarray(tokens, dtype=np.int64)).to(dev)
+        x = dw.embed[tok] + positional(n, s.hidden_dim, 0, dev)
+        k_tok = torch.full((n,), k, dtype=torch.int32, device=dev)
+        replay = mask = None
+        if replay_states is not None:
+            rs = torch.as_tensor(np.asarray(replay_states, dtype=np.float32)).to(dev)
+            replay = torch.zeros(n, s.num_experts, device=dev, dtype=torch.float32)
+            mask = torch.zeros(n, device=dev, dtype=torch.uint8)
+            mask[-1] = 1
+        states = torch.empty(s.num_layers, s.num_experts, device=dev, dtype=torch.float32)
+        sels = torch.empty(s.num_layers, k, device=dev, dtype=torch.int32)
+        flags = torch.zeros(1, device=dev, dtype=torch.int32)
+        for layer in range(s.num_layers):
+            x = self.attention_full(x, layer)
+            if replay is not None:
+                replay[-1] = rs[layer]
+            x_new, sc = self.moe.forward(x, layer, k_tok, k, replay=replay, replay_mask=mask, reuse_gates=reuse_gates)
+            states[layer] = sc["router"]["logits"][-1]
+            sels[layer] = sc["router"]["idx"][-1]
+            flags |= sc["router"]["flags"]
+            sc["router"]["flags"].zero_()
+            x = x_new.clone()
+        logits = torch.empty(1, s.vocab_size, device=dev, dtype=torch.float32)
+        K.head_confidence(x[-1:].contiguous(), dw.head, 0.0, s.logit_scale, ws=self.head_workspace(1),
+                          logits_out=logits)
+        probs = K.softmax_rows(logits, torch.float64)[0]
+        return probs, states, sels, flags
+
+
+class DecodeSession:
+    """KV-cached decode for B sequences at a common position."""
+
+    def __init__(self, model: DeviceModel, batch: int, max_len: int):
+        s = model.spec
+        self.m, self.B, self.max_len = model, batch, max_len
+        dev = model.device
+        self.kc = torch.zeros(s.num_layers, batch, max_len, s.hidden_dim, device=dev, dtype=torch.float32)
+        self.vc = torch.zeros_like(self.kc)
+        self.pos = 0
+
+    def _attn_step(self, x: torch.Tensor, layer: int, rows: torch.Tensor | None, pos: int, n: int):
+        """Attention for n new positions [pos, pos+n) of the sequences `rows`
+        (None = all); writes their K/V into the cache."""
+        m, s = self.m, self.m.spec
+        dw = m.dw
+        Bn = x.shape[0] // n
+        d = s.hidden_dim
+        H = s.n_heads
+        hd = d // H
+        h = Fn.layer_norm(x, (d,), eps=1e-5)
+        q, k, v = m._mm(h, dw.q[layer]), m._mm(h, dw.k[layer]), m._mm(h, dw.v[layer])
+        q, k, v = (t.view(Bn, n, d) for t in (q, k, v))
+        if rows is None:
+            self.kc[layer, :, pos:pos + n] = k
+            self.vc[layer, :, pos:pos + n] = v
+            K_, V_ = self.kc[layer, :, :pos + n], self.vc[layer, :, :pos + n]
+        else:
+            self.kc[layer, rows, pos:pos + n] = k
+            self.vc[layer, rows, pos:pos + n] = v
+            K_, V_ = self.kc[layer, rows, :pos + n], self.vc[layer, rows, :pos + n]
+        qh = q.view(Bn, n, H, hd).transpose(1, 2)
+        kh = K_.view(Bn, pos + n, H, hd).transpose(1, 2)
+        vh = V_.view(Bn, pos + n, H, hd).transpose(1, 2)
+        scores = (qh @ kh.transpose(-1, -2)) / math.sqrt(hd)
+        if n > 1:
+            mask = torch.ones(n, pos + n, dtype=torch.bool, device=x.device).triu(1 + pos)
+            scores = scores.masked_fill(mask, float("-inf"))
+        attn = torch.softmax(scores, dim=-1)
+        out = (attn @ vh).transpose(1, 2).reshape(Bn * n, d)
+        return x + m._mm(out, dw.o[layer])
+
+    def run(self, tokens: torch.Tensor, k_tok: torch.Tensor, k_max: int, *, rows=None, replay=None,
+            replay_mask=None, reuse_gates=False, advance=True, expert_hook=None, layer_hook=None):
+        """Process `tokens` (Bn, n) at positions [pos, pos+n).  Returns
+        (x_last (Bn, d), states (L, Bn*n, E) view of last-position logits, idx (L, Bn, k_max)).
+        `replay` (L, Bn, E) applies to the last position of every row with replay_mask."""
+        m, s = self.m, self.m.spec
+        dw, dev = m.dw, m.device
+        Bn, n = tokens.shape
+        pos = self.pos
+        x = dw.embed[tokens.reshape(-1)] + positional(n, s.hidden_dim, pos, dev).repeat(Bn, 1)
+        T = Bn * n
+        states = torch.empty(s.num_layers, Bn, s.num_experts, device=dev, dtype=torch.float32)
+        idx = torch.empty(s.num_layers, Bn, k_max, device=dev, dtype=torch.int32)
+        rep_full = rep_mask_full = None
+        if replay is not None:
+            rep_full = torch.zeros(T, s.num_experts, device=dev, dtype=torch.float32)
+            rep_mask_full = torch.zeros(T, device=dev, dtype=torch.uint8)
+            last = torch.arange(Bn, device=dev) * n + (n - 1)
+            rep_mask_full[last] = replay_mask if replay_mask is not None else 1
+        for layer in range(s.num_layers):
+            if layer_hook is not None:
+                layer_hook(layer)
+            x = self._attn_step(x, layer, rows, pos, n)
+            if replay is not None:
+                rep_full[last] = replay[layer]
+            x_new, sc = m.moe.forward(x, layer, k_tok, k_max, replay=rep_full, replay_mask=rep_mask_full,
+                                      reuse_gates=reuse_gates, pre_experts=expert_hook)
+            lg = sc["router"]["logits"].view(Bn, n, s.num_experts)
+            states[layer] = lg[:, -1]
+            idx[layer] = sc["router"]["idx"].view(Bn, n, k_max)[:, -1]
+            x = x_new.clone()
+        if advance:
+            self.pos += n
+        x_last = x.view(Bn, n, s.hidden_dim)[:, -1].contiguous()
+        return x_last, states, idx

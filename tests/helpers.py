@@ -1,0 +1,53 @@
+"""Shared test helpers: matched oracle / device weights."""
+from __future__ import annotations
+
+import numpy as np
+
+from oracle import moe_ref as R
+
+
+def ospec(**kw) -> R.OracleSpec:
+    return R.OracleSpec(**kw)
+
+
+def round_bf16(a: np.ndarray) -> np.ndarray:
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).to(torch.float64).numpy()
+
+
+def matched(spec_kw: dict, dtype: str = "float32", device="cuda"):
+    """(OracleWeights, ModelSpec, DeviceModel) on identical weights.
+
+    For bf16 the oracle sees the bf16-rounded values so the comparison isolates
+    the kernels' fp32 arithmetic from the storage rounding."""
+    from paper_2510_12357_b200 import ModelSpec
+    from paper_2510_12357_b200.model import DeviceModel
+    from paper_2510_12357_b200.weights import DeviceWeights, HostWeights
+
+    o = R.build_weights(R.OracleSpec(**spec_kw))
+    if dtype == "bfloat16":
+        for name in ("attn_q", "attn_k", "attn_v", "attn_o", "router", "expert_in", "expert_out", "head",
+                     "expert_up", "shared_in", "shared_up", "shared_out", "shared_gate_w"):
+            v = getattr(o, name)
+            if v is not None:
+                setattr(o, name, round_bf16(v))
+    ms = ModelSpec(**spec_kw, dtype=dtype)
+    hw = HostWeights(o.embed, o.attn_q, o.attn_k, o.attn_v, o.attn_o, o.router, o.expert_in, o.expert_out, o.head,
+                     o.expert_up, o.shared_in, o.shared_up, o.shared_out, o.shared_gate_w)
+    dm = DeviceModel(DeviceWeights.from_host(ms, hw, device))
+    return o, ms, dm
+
+
+def rel_err(a, b) -> float:
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+# reduced real-shape specs exercising every extension (SwiGLU, shared experts,
+# sigmoid shared gate, multi-head attention) at sizes the oracle finishes fast
+QWEN_MINI = dict(num_layers=2, num_experts=12, k_big=4, hidden_dim=128, vocab_size=512, seed=5, ffn_dim=64,
+                 activation="swiglu", n_shared=1, shared_ffn_dim=256, shared_gate="sigmoid", n_heads=4)
+DSEEK_MINI = dict(num_layers=2, num_experts=16, k_big=6, k_little=3, hidden_dim=128, vocab_size=300, seed=6,
+                  ffn_dim=64, activation="swiglu", n_shared=2, shared_ffn_dim=64, n_heads=2)
+OLMOE_MINI = dict(num_layers=2, num_experts=16, k_big=8, hidden_dim=256, vocab_size=400, seed=8, ffn_dim=128,
+                  activation="swiglu", gate_norm="softmax_all", n_heads=4)
