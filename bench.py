@@ -1,0 +1,441 @@
+"""Benchmark: decode tokens/s, MoBiLE vs the full-top-k offload baseline,
+Qwen1.5-MoE-A2.7B shape (BASELINE.json metric; configs[2] = C3).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (C3): Qwen1.5-MoE-A2.7B shape (d2048, 24 layers, 60 routed experts
+top-4 / little top-2, one 5632-wide sigmoid-gated shared expert, V151936),
+random-init bf16 weights.  Routed experts live in pinned host DRAM; the HBM
+expert cache is capped by the reference's own budget formula
+(hbm_expert_slots, config.py:204-218) at the paper's 16 GiB / 6 GiB-reserved
+consumer setting (rtx4080.json) -> 477 slots of 1440 experts.  Batch-1 greedy
+decode after a 512-token prompt; the fallback ratio is pinned at the paper's
+Qwen r = 0.11 with engine.injected_fallback_flags.  A step is
+one decoded token.  Every token streams ~4.7 GB of weights (>> 126 MB L2), so
+no L2 flush is needed between steps.
+
+The full-top-k baseline (every token at k=4, experts loaded on demand, the
+reference's simulate_full_stream) runs on the same stack in the same process;
+its tokens/s and the MoBiLE/full speed-up are reported beside `value`.
+
+`--impl reference` times the reference's CPU path of the same decode (the
+oracle's NumPy restatement in fp32 on the host cores; the reference package
+cannot build d=2048 models) and prints the same JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "decode tokens/s, MoBiLE vs full-top-k offload baseline, Qwen1.5-MoE-A2.7B"
+WORKLOAD = ("C3: Qwen1.5-MoE-A2.7B shape, experts in pinned host DRAM, capped HBM expert cache "
+            "(477 slots = hbm_expert_slots at 16 GiB cap / 6 GiB reserved), batch-1 greedy decode, "
+            "prompt 512, injected fallback ratio r=0.11")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=16)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--prompt-len", type=int, default=512)
+    ap.add_argument("--r", type=float, default=0.11)
+    ap.add_argument("--cap-gib", type=float, default=16.0)
+    ap.add_argument("--reserved-gib", type=float, default=6.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=6)
+    ap.add_argument("--layers", type=int, default=0, help="debug only: fewer layers (invalidates the number)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- dist
+def dist_init(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(ws, v: float, device=None) -> float:
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        import statistics
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and "Active" in r[3 + i]
+                          and "Not" not in r[3 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- roofline timer
+class KernelTimer:
+    """CUDA events around every gate-up launch (on the launching stream)."""
+
+    def __init__(self, bytes_of):
+        self.pairs, self.bytes_of, self.on = [], bytes_of, False
+        self._cur = None
+
+    def start(self):
+        if not self.on:
+            return
+        import torch
+        self._cur = torch.cuda.Event(enable_timing=True)
+        self._cur.record()
+
+    def stop(self, tag):
+        if not self.on:
+            return
+        import torch
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.pairs.append((self._cur, e, self.bytes_of(tag)))
+
+    def result(self):
+        tot_ms = sum(a.elapsed_time(b) for a, b, _ in self.pairs)
+        tot_b = sum(n for _, _, n in self.pairs)
+        return tot_b, tot_ms, len(self.pairs)
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "fallback": True}
+
+
+def ncu_traffic():
+    p = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        d = json.loads(p.read_text())
+        return d.get("gate_up_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, ws, rank, local):
+    import numpy as np
+    import torch
+
+    from paper_2510_12357_b200 import PolicySpec, hbm_expert_slots
+    from paper_2510_12357_b200 import kernels as K
+    from paper_2510_12357_b200.runtime import StepEngine
+    from paper_2510_12357_b200.model import DeviceModel
+    from paper_2510_12357_b200.offload import OffloadRuntime
+    from paper_2510_12357_b200.policy import injected_fallback_flags
+    from paper_2510_12357_b200.presets import QWEN15_MOE, with_byte_sizes
+    from paper_2510_12357_b200.spec import HardwareSpec
+    from paper_2510_12357_b200.weights import DeviceWeights
+    from dataclasses import replace
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    spec = QWEN15_MOE if not args.layers else replace(QWEN15_MOE, num_layers=args.layers)
+    spec = with_byte_sizes(spec)
+    hw = HardwareSpec(hbm_capacity=int(args.cap_gib * 2**30), reserved=int(args.reserved_gib * 2**30))
+    slots = hbm_expert_slots(spec, hw)
+    t0 = time.time()
+    dw = DeviceWeights.random(spec, dev, seed=rank, experts_on_device=False)
+    t_init = time.time() - t0
+    dm = DeviceModel(dw)
+    prompt = np.random.default_rng(1 + rank).integers(1, spec.vocab_size, size=args.prompt_len).tolist()
+    K_, W_ = args.steps, args.warmup
+    flags = injected_fallback_flags(W_ + K_, args.r)
+    policy = PolicySpec(gamma=0.7)
+    max_len = args.prompt_len + W_ + K_ + 8
+    w13_r = dw.w13_elems * dw.elem_bytes
+    w13_s = dw.s_w13_elems * dw.elem_bytes
+
+    def gate_up_bytes(tag):
+        """Algorithmic bytes of one fused gate-up launch: the W13 rows of the
+        routed experts it reads (T*k distinct experts at batch 1) and of the
+        shared expert(s), plus activations in and out (f32)."""
+        kind, T, k = tag
+        S = spec.n_shared
+        w = min(spec.num_experts, T * k) * w13_r + S * w13_s
+        act = T * spec.hidden_dim * 4 + T * (k * spec.ffn + S * spec.shared_ffn) * 4
+        return w + act
+
+    # synthetic input stream: the step inputs are teacher-forced random ids so
+    # routing varies token to token as in real text (greedy feedback on random
+    # weights collapses onto one repeated token and a 100%-hit cache).
+    stream = np.random.default_rng(100 + rank).integers(1, spec.vocab_size, size=W_ + K_ + 1).tolist()
+
+    def make_engine(graphs=True):
+        rt = OffloadRuntime(dw, slots, lookahead=2)
+        eng = StepEngine(dm, 1, max_len, runtime=rt, graphs=graphs).build(gamma=policy.gamma)
+        return rt, eng
+
+    def timed_decode(full: bool):
+        rt, eng = make_engine()
+        eng.prefill(prompt)
+        for i in range(W_):
+            eng.step(flags[i], full=full, next_token=stream[i])
+        torch.cuda.synchronize()
+        barrier(ws)
+        launches0 = K.LAUNCHES[0]
+        bytes0, xfer0 = rt.counters()
+        stats0 = rt.cache.stats
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            torch.cuda.synchronize()
+            ev0.record(eng.stream)
+            w0 = time.perf_counter()
+            fb = 0
+            for i in range(W_, W_ + K_):
+                _, f = eng.step(flags[i], full=full, next_token=stream[i])
+                fb += f
+            ev1.record(eng.stream)
+            torch.cuda.synchronize()
+            wall = time.perf_counter() - w0
+        dev_s = ev0.elapsed_time(ev1) / 1e3
+        bytes1, xfer1 = rt.counters()
+        st = rt.cache.stats
+        n_graph_kernels = kernels_per_pass(eng, "full" if full else "little")
+        out = dict(dev_s=dev_s, wall_s=wall, launches=K.LAUNCHES[0] - launches0, fallbacks=fb,
+                   h2d_bytes=bytes1 - bytes0, transfers=xfer1 - xfer0,
+                   hits=st.hits - stats0.hits, issued=st.issued - stats0.issued,
+                   coalesced=st.coalesced - stats0.coalesced, clocks=clk.summary(), graph_kernels=n_graph_kernels)
+        del eng, rt
+        torch.cuda.empty_cache()
+        return out
+
+    mob = timed_decode(full=False)
+    base = timed_decode(full=True)
+
+    # live roofline of the dominant kernel: same decode, eager (un-graphed) so
+    # CUDA events can bracket every gate-up launch on its stream
+    rt, eng = make_engine(graphs=False)
+    timer = KernelTimer(gate_up_bytes)
+    eng.timer = timer
+    eng.prefill(prompt)
+    for i in range(4):
+        eng.step(flags[i], next_token=stream[i])
+    timer.on = True
+    with torch.cuda.stream(eng.stream):
+        for i in range(4, 4 + min(K_, 16)):
+            eng.step(flags[i], next_token=stream[i])
+    torch.cuda.synchronize()
+    timer.on = False
+    mob["timer"] = timer.result()
+    del eng, rt
+    torch.cuda.empty_cache()
+
+    # isolated PCIe H2D peak (pinned, 1 GiB) for the copy-engine roofline
+    hbuf = torch.empty(2**30, dtype=torch.uint8, pin_memory=True)
+    dbuf = torch.empty(2**30, dtype=torch.uint8, device=dev)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        dbuf.copy_(hbuf, non_blocking=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(4):
+            dbuf.copy_(hbuf, non_blocking=True)
+        e1.record(s)
+    torch.cuda.synchronize()
+    pcie_peak = 4 * 2**30 / (e0.elapsed_time(e1) / 1e3) / 1e9
+    del hbuf, dbuf
+
+    # end-to-end: the public decode() call with host inputs (prompt + K teacher-forced ids),
+    # including the 512-token prefill, H2D of every input id and D2H of every output id
+    rt, eng = make_engine()
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    toks, _ = eng.decode(list(prompt), K_, fallback_flags=flags[:K_], inputs=stream[:K_])
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - w0
+    del eng, rt
+    torch.cuda.empty_cache()
+
+    dev_s = max_over_ranks(ws, mob["dev_s"], dev)
+    base_s = max_over_ranks(ws, base["dev_s"], dev)
+    e2e_s = max_over_ranks(ws, e2e_s, dev)
+    value = ws * K_ / dev_s
+    base_value = ws * K_ / base_s
+
+    tot_b, tot_ms, n_l = mob["timer"]
+    P = peaks()
+    achieved = (tot_b / (tot_ms / 1e3)) / 1e9 if tot_ms > 0 else 0.0
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_leg(spec, args.cpu_steps, args.r)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "tokens/s", "n_gpus": ws, "steps": K_,
+            "warmup": W_, "ms_per_step": round(dev_s / K_ * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init bf16 weights on the device, random 512-token prompt)",
+            "config": {"workload": WORKLOAD, "model": "Qwen1.5-MoE-A2.7B-shape", "global_batch": ws,
+                       "seq_len": args.prompt_len + W_ + K_, "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                       "hbm_expert_slots": slots, "routed_experts": spec.num_layers * spec.num_experts,
+                       "r_injected": args.r, "lookahead": 2, "gamma": 0.7,
+                       "l2": "inputs > L2: ~4.7 GB of weights streamed per token (no flush)",
+                       "layers": spec.num_layers},
+            "baseline_full_topk": {"value": round(base_value, 3), "unit": "tokens/s",
+                                   "ms_per_step": round(base_s / K_ * 1e3, 3), "h2d_bytes": base["h2d_bytes"],
+                                   "cache_hits": base["hits"], "transfers": base["transfers"]},
+            "speedup_vs_full_topk": round(value / base_value, 4),
+            "mobile": {"fallbacks": mob["fallbacks"], "h2d_bytes": mob["h2d_bytes"], "transfers": mob["transfers"],
+                       "cache_hits": mob["hits"], "cache_coalesced": mob["coalesced"],
+                       "wall_ms_per_step": round(mob["wall_s"] / K_ * 1e3, 3)},
+            "pcie": {"bound": "pcie_h2d", "achieved_gbs": round(mob["h2d_bytes"] / mob["dev_s"] / 1e9, 2),
+                     "peak_gbs": round(pcie_peak, 2), "peak_note": "measured in this run: 1 GiB pinned H2D",
+                     "frac": round(mob["h2d_bytes"] / mob["dev_s"] / 1e9 / pcie_peak, 4)},
+            "roofline": {"bound": "hbm", "kernel": "stream_gemv_kernel: fused routed+shared expert gate-up (W13) launch",
+                         "achieved": round(achieved, 1), "peak": P.get("hbm_gbs"), "unit": "GB/s",
+                         "frac": round(achieved / P.get("hbm_gbs", 6543.1), 4), "traffic": ncu_traffic(),
+                         "launches_timed": n_l, "bytes_per_launch": int(tot_b / max(n_l, 1)),
+                         "peak_note": "MEASURED_PEAKS.json hbm_gbs (copy)"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(K_ / e2e_s * ws, 3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int((args.prompt_len + K_) * 8 / K_),
+                    "d2h_bytes_per_step": int(4 + 4 + 1 + 4 * (spec.num_experts + 1) * spec.num_layers),
+                    "note": "wall clock of StepEngine.decode(prompt host list, K) incl. 512-token prefill"},
+            "gpu_launches": mob["launches"] + mob["graph_kernels"] * (K_ + mob["fallbacks"]),
+            "clocks": mob["clocks"],
+            "init_s": round(t_init, 1),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def kernels_per_pass(eng, kind):
+    """libmobile kernels inside one captured pass (graph replays are not
+    counted by the wrapper counter): per layer qkv, attention, o, router,
+    permute, gate-up, down (+ shared gate-up, down), combine; embed; head."""
+    s = eng.spec
+    per_layer = 8 + (2 if s.n_shared else 0)
+    return s.num_layers * per_layer + 2
+
+
+def cpu_leg(spec, steps, r):
+    import numpy as np
+
+    from oracle import cpu_baseline as CB
+    from paper_2510_12357_b200.policy import injected_fallback_flags
+    os_ = CB.oracle_spec_from(spec)
+    W = CB.aliased_weights(os_)
+    prompt = np.random.default_rng(1).integers(1, spec.vocab_size, size=4).tolist()
+    flags = injected_fallback_flags(1 + steps, r)
+    if steps >= 1 and not any(flags[1:]):
+        flags[1 + steps // 2] = True  # make the sample contain one replayed big pass
+    secs, fb = CB.time_decode(W, prompt, flags, 1, steps)
+    return {"value": round(steps / secs, 4), "unit": "tokens/s", "cores": CB.cores(), "kind": "port",
+            "sample": f"{steps} decode tokens ({fb} fallback) of the same Qwen shape in fp32 NumPy "
+                      f"(oracle KVDecoder), prompt 4, expert/attention matrices aliased to pools > LLC"}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle import cpu_baseline as CB
+    from paper_2510_12357_b200.policy import injected_fallback_flags
+    from paper_2510_12357_b200.presets import QWEN15_MOE
+    os_ = CB.oracle_spec_from(QWEN15_MOE)
+    W = CB.aliased_weights(os_)
+    prompt = np.random.default_rng(1).integers(1, QWEN15_MOE.vocab_size, size=4).tolist()
+    flags = injected_fallback_flags(args.warmup + args.steps, args.r)
+    secs, fb = CB.time_decode(W, prompt, flags, args.warmup, args.steps)
+    v = args.steps / secs
+    line = {"metric": METRIC, "value": round(v, 4), "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(secs / args.steps * 1e3, 2), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "impl": "reference",
+            "data": "synthetic (random-init fp32 weights, random prompt)",
+            "config": {"workload": WORKLOAD, "model": "Qwen1.5-MoE-A2.7B-shape", "global_batch": 1},
+            "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "cores": CB.cores(), "kind": "port",
+                             "sample": f"{args.steps} decode tokens ({fb} fallback), fp32 NumPy oracle KV decode, "
+                                       f"prompt 4, matrices aliased to pools > LLC"},
+            "e2e": {"value": round(v, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        ws = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference(args, ws, rank)
+        return
+    ws, rank, local = dist_init(args)
+    run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

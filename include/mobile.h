@@ -77,12 +77,17 @@ int mobile_num_sms(void);
  *   gates_out (T, k_max) f32 gate weights in selection order, 0 beyond k_tok
  *   flags    (1,) int32 device word; bit 0 set if any logit was non-finite,
  *            bit 1 if any k_tok[t] > E.  Caller zeroes it.
+ *   perm_*   optional mobile_permute outputs (offsets, sorted_pairs, active):
+ *            when given, the permute is fused into the router's leader CTA
+ *            for decode-sized launches (T <= 4, T*k_max <= 32) and run as a
+ *            separate kernel otherwise -- same results either way.
  */
 int mobile_router_topk(const float* x, float* h2_out, const void* w_router, int w_dtype,
                        int T, int d, int E, int n_extra, int k_max, const int* k_tok,
                        const float* replay, const uint8_t* replay_mask, int reuse_gates,
                        int gate_norm, float* logits_out, float* extra_out, int* idx_out,
-                       float* gates_out, int* flags, void* stream);
+                       float* gates_out, int* flags, int* perm_offsets, int* perm_pairs,
+                       int* perm_active, void* stream);
 
 /* Row-wise top-k (toymoe.py:80-88) over R rows of E logits (f32 or f64):
  * used by top_k(), build_mobile_plan (policy.py:98-103) and
@@ -141,14 +146,69 @@ int mobile_expert_down(const float* U, const int* offsets, const int* sorted_pai
                        const void* w2_base, long long expert_stride, const int* slot, int w_dtype,
                        float* Y, void* stream);
 
+/* ---- bulk-copy streaming GEMV (decode engine) -----------------------------
+ * One launch computes several groups of weight-row dot products, streaming
+ * weights through shared memory with cp.async.bulk on an mbarrier ring.
+ * Group semantics (per pair p of expert e, see mobile_expert_gate_up):
+ *   epi 0 STORE : out[p, r] = (residual[p, r] +) x[p / x_div] . W_e[r]
+ *   epi 1 RELU  : out[p, r] = max(x[p / x_div] . W_e[r], 0)
+ *   epi 2 SWIGLU: rows in 16-row groups [8 gate | 8 up] ->
+ *                 out[p, f] = silu(g_f) * u_f,  out_dim = rows / 2
+ * active == NULL means one dense "expert" (weights at w_base) applied to
+ * pairs 0..dense_T-1.  max_tokens bounds tokens per expert (1..4 fast path;
+ * more are processed in chunks of 4).
+ */
+typedef struct {
+  const void* w_base;
+  long long stride;
+  const int* slot;
+  const float* x;
+  int x_div;
+  const int* offsets;
+  const int* pairs;
+  const int* active;
+  int dense_T;
+  int max_active;
+  int K;
+  int rows;
+  float* out;
+  const float* residual;
+  int epi;
+} mobile_sg_group;
+int mobile_stream_gemv(const mobile_sg_group* groups, int n_groups, int w_dtype, int max_tokens,
+                       void* stream);
+
 /* ---- combine -------------------------------------------------------------
  * toymoe.py:192, 204, 207:  moe = sum_j gates[t,j] * Y[t*k_max + j] (selection
  * order), then + shared (optionally sigmoid(shared_logit[t,s]) * Ys[t][s]),
- * x_out[t] = x[t] + moe.  Y_shared is (T, n_shared, d) or NULL.
+ * x_out[t] = x[t] + moe.  Y_shared is (T, n_shared, d) or NULL.  If ln_out is
+ * non-NULL it also receives LN(x_out[t]) (the next layer's attention input).
  */
 int mobile_combine(const float* x, const float* Y, const float* gates, const int* k_tok, int T,
                    int k_max, int d, const float* Y_shared, int n_shared,
-                   const float* shared_logits, float* x_out, void* stream);
+                   const float* shared_logits, float* x_out, float* ln_out, void* stream);
+
+/* ---- decode-step kernels around the layer --------------------------------
+ * (toymoe.py:171-186 semantics, KV-cached, position read from device memory
+ * so a whole decode step can be captured in one CUDA graph.)
+ *   dense_gemv: y[t, r] = (residual ? residual[t, r] : 0) + (LN?(x[t])) . W[r]
+ *               W (N, d) out-major, T <= 8 rows (attention q/k/v and o).
+ *   attn_decode: qkv (B, 3d); writes k/v at pos[b] into k/v caches
+ *               (B, max_len, d) f32, out (B, d) = softmax(q k^T / sqrt(hd)) v.
+ *   embed:      x[b] = embed[tok[b]] + pe[pos[b]]  (pe = sinusoidal table);
+ *               ln_out (optional) = LN(x[b]).
+ *   advance:    pos[b] += 1; tok[b] = next_tok[b] if next_tok.
+ */
+int mobile_dense_gemv(const float* x, int T, int d, int do_ln, const void* w, int w_dtype, int N,
+                      const float* residual, float* y, void* stream);
+int mobile_attn_decode(const float* qkv, float* k_cache, float* v_cache, const int* pos, int B, int d,
+                       int H, int max_len, float* out, void* stream);
+int mobile_embed(const int* tok, const int* pos, const float* embed, const float* pe, int B, int d, float* x,
+                 float* ln_out, void* stream);
+int mobile_advance(int* pos, int B, int* tok, const int* next_tok, void* stream);
+/* cudaMemcpyAsync(kind = default) on `stream` (graph-capturable H2D/D2H of
+ * pinned slot tables and routing lists). */
+int mobile_memcpy_async(void* dst, const void* src, size_t bytes, void* stream);
 
 /* ---- expert cache core (memory.py:65-181 semantics) ----------------------
  * LRU of (layer, expert) keys with pins, in-flight protection, speculative

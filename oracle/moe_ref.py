@@ -49,6 +49,7 @@ class OracleSpec:
     gate_norm: str = "selected_softmax"  # toymoe.py:201 | "softmax_all" (HF norm_topk_prob=False)
     n_heads: int = 1
     logit_scale: float = LOGIT_SCALE
+    embed_scale: float = 0.0  # 0 -> 1/sqrt(d) as the toy (toymoe.py:109-112)
 
     def __post_init__(self):
         if self.k_little == 0:
@@ -155,7 +156,7 @@ def build_weights(spec: OracleSpec) -> OracleWeights:
     def mat(*shape, fan_in=d):
         return rng.uniform(-1.0, 1.0, size=shape) * (1.0 / np.sqrt(fan_in))
 
-    embed = mat(V, d)
+    embed = mat(V, d, fan_in=1.0 / spec.embed_scale**2 if spec.embed_scale else d)
     q, k, v, o = mat(L, d, d), mat(L, d, d), mat(L, d, d), mat(L, d, d)
     router = mat(L, d, E)
     w_in = mat(L, E, d, I)
@@ -393,8 +394,9 @@ class KVDecoder:
         self.W = W
         s = W.spec
         self.prefill_k = s.k_big if prefill_k is None else prefill_k
-        self.k_cache = [np.zeros((0, s.hidden_dim)) for _ in range(s.num_layers)]
-        self.v_cache = [np.zeros((0, s.hidden_dim)) for _ in range(s.num_layers)]
+        dt = W.embed.dtype
+        self.k_cache = [np.zeros((0, s.hidden_dim), dtype=dt) for _ in range(s.num_layers)]
+        self.v_cache = [np.zeros((0, s.hidden_dim), dtype=dt) for _ in range(s.num_layers)]
 
     @property
     def length(self) -> int:
@@ -405,7 +407,7 @@ class KVDecoder:
         selections_last, new_kv).  Does NOT commit the K/V rows."""
         W, s = self.W, self.W.spec
         n = len(tokens)
-        x = W.embed[np.asarray(tokens)] + positional(n, s.hidden_dim, self.length)
+        x = W.embed[np.asarray(tokens)] + positional(n, s.hidden_dim, self.length).astype(W.embed.dtype)
         states = np.empty((s.num_layers, s.num_experts))
         sels, new_kv = [], []
         mask = None

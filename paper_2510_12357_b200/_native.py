@@ -30,6 +30,13 @@ class CapacityDeadlock(RuntimeError):
     """A required expert load found every cache slot pinned or in flight (memory.py:25-26)."""
 
 
+class mobile_sg_group(C.Structure):
+    _fields_ = [("w_base", C.c_void_p), ("stride", C.c_longlong), ("slot", C.c_void_p), ("x", C.c_void_p),
+                ("x_div", C.c_int), ("offsets", C.c_void_p), ("pairs", C.c_void_p), ("active", C.c_void_p),
+                ("dense_T", C.c_int), ("max_active", C.c_int), ("K", C.c_int), ("rows", C.c_int),
+                ("out", C.c_void_p), ("residual", C.c_void_p), ("epi", C.c_int)]
+
+
 class mobile_channel(C.Structure):
     _fields_ = [("t_xfer", C.c_double), ("busy_until", C.c_double), ("transfers_issued", C.c_longlong)]
 
@@ -50,7 +57,8 @@ _SIGS = {
     "mobile_version": ([], I32),
     "mobile_last_error": ([], C.c_char_p),
     "mobile_num_sms": ([], I32),
-    "mobile_router_topk": ([P, P, P, I32, I32, I32, I32, I32, I32, P, P, P, I32, I32, P, P, P, P, P, P], I32),
+    "mobile_router_topk": ([P, P, P, I32, I32, I32, I32, I32, I32, P, P, P, I32, I32, P, P, P, P, P, P, P, P, P],
+                           I32),
     "mobile_topk_rows": ([P, I32, I32, I32, I32, P, P, P], I32),
     "mobile_head_ws_bytes": ([I32, I32], SZ),
     "mobile_head_confidence": ([P, P, I32, I32, I32, I32, F, F, P, P, P, P, P, P], I32),
@@ -59,7 +67,13 @@ _SIGS = {
     "mobile_permute": ([P, P, I32, I32, I32, P, P, P, P], I32),
     "mobile_expert_gate_up": ([P, P, P, P, I32, I32, I32, I32, I32, P, I64, P, I32, I32, P, P], I32),
     "mobile_expert_down": ([P, P, P, P, I32, I32, I32, I32, P, I64, P, I32, P, P], I32),
-    "mobile_combine": ([P, P, P, P, I32, I32, I32, P, I32, P, P, P], I32),
+    "mobile_combine": ([P, P, P, P, I32, I32, I32, P, I32, P, P, P, P], I32),
+    "mobile_stream_gemv": ([P, I32, I32, I32, P], I32),
+    "mobile_dense_gemv": ([P, I32, I32, I32, P, I32, I32, P, P, P], I32),
+    "mobile_attn_decode": ([P, P, P, P, I32, I32, I32, I32, P, P], I32),
+    "mobile_embed": ([P, P, P, P, I32, I32, P, P, P], I32),
+    "mobile_advance": ([P, I32, P, P, P], I32),
+    "mobile_memcpy_async": ([P, P, SZ, P], I32),
     "mobile_cache_create": ([I32], P),
     "mobile_cache_destroy": ([P], None),
     "mobile_cache_request": ([P, I32, I32, D, I32, P, D, P, P, P], I32),

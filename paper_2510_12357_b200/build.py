@@ -1,6 +1,6 @@
 """Build libmobile.so in-tree with nvcc for sm_100a (no torch extension JIT).
 
-    python -m paper_2510_12357_b200.build
+    python paper_2510_12357_b200/build.py      (or __graft_entry__.build())
 
 Objects are compiled in parallel into paper_2510_12357_b200/build/, then linked
 into paper_2510_12357_b200/libmobile.so (git-ignored, travels with gpurun).

@@ -3,6 +3,8 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <mutex>
+#include <unordered_map>
 
 #include "../../include/mobile.h"
 
@@ -22,7 +24,29 @@ int cuda_status(cudaError_t e, const char* where) {
   return MOBILE_ERR_CUDA;
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel (and only
+// when the requested size grows), so launches stay legal inside CUDA-graph
+// capture and cost nothing on the hot path.
+int set_smem_once(const void* func, size_t smem) {
+  if (smem <= 48 * 1024) return MOBILE_OK;
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> done;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = done[func];
+  if (smem <= cur) return MOBILE_OK;
+  cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
+  cur = smem;
+  return MOBILE_OK;
+}
+
 }  // namespace mobile
+
+extern "C" int mobile_memcpy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream);
+  if (e != cudaSuccess) return mobile::cuda_status(e, "memcpy_async");
+  return MOBILE_OK;
+}
 
 extern "C" int mobile_version(void) { return 1; }
 extern "C" const char* mobile_last_error(void) { return mobile::g_err; }

@@ -13,6 +13,7 @@ constexpr int kWarp = 32;
 // ---------------------------------------------------------------- error state
 void set_error(const char* fmt, ...);
 int sm_count();
+int set_smem_once(const void* func, size_t smem);
 int cuda_status(cudaError_t e, const char* where);
 #define MOBILE_CHECK_LAUNCH(name) \
   do { cudaError_t _e = cudaGetLastError(); if (_e != cudaSuccess) return ::mobile::cuda_status(_e, name); } while (0)

@@ -1,0 +1,286 @@
+// Decode-step kernels around the MoE layer: token embedding + position,
+// (LN +) dense GEMV for the attention projections, and single-query
+// attention over the KV cache.  They exist so the whole per-token step is
+// libmobile kernels reading the position from device memory -- capturable in
+// one CUDA graph -- instead of a few hundred framework ops.  Semantics follow
+// toymoe.py:171-186 (sinusoidal positions added to the embedding; pre-LN
+// attention, scale 1/sqrt(head_dim), softmax, residual).
+#include "common.cuh"
+
+namespace mobile {
+
+constexpr int kGemvThreads = 256;
+constexpr int kGemvWarps = kGemvThreads / 32;
+
+// y[t, r] = (residual ? residual[t, r] : 0) + sum_k xin[t, k] * W[r, k]
+// xin = LN(x[t]) if do_ln else x[t].  One pass of TT tokens; warps stream two
+// weight rows at a time with no-allocate 16-byte loads.
+template <typename W, int TT>
+__global__ void __launch_bounds__(kGemvThreads) dense_gemv_kernel(const float* __restrict__ x, int T, int d,
+                                                                  int do_ln, const W* __restrict__ w, int N,
+                                                                  const float* __restrict__ residual,
+                                                                  float* __restrict__ y) {
+  extern __shared__ __align__(16) float sh[];
+  float* h = sh;  // TT * d
+  __shared__ float red[kGemvWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nt = min(TT, T);
+  for (int t = 0; t < nt; ++t) {
+    const float* xr = x + (size_t)t * d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) h[(size_t)t * d + i] = xr[i];
+  }
+  __syncthreads();
+  if (do_ln) {
+    for (int t = 0; t < nt; ++t) {
+      float* row = h + (size_t)t * d;
+      float s = 0.f;
+      for (int i = threadIdx.x; i < d; i += blockDim.x) s += row[i];
+      s = warp_sum(s);
+      if (lane == 0) red[warp] = s;
+      __syncthreads();
+      float mean = 0.f;
+      for (int i = 0; i < kGemvWarps; ++i) mean += red[i];
+      mean /= (float)d;
+      __syncthreads();
+      float q = 0.f;
+      for (int i = threadIdx.x; i < d; i += blockDim.x) { float c = row[i] - mean; q += c * c; }
+      q = warp_sum(q);
+      if (lane == 0) red[warp] = q;
+      __syncthreads();
+      float var = 0.f;
+      for (int i = 0; i < kGemvWarps; ++i) var += red[i];
+      const float inv = 1.0f / sqrtf(var / (float)d + 1e-5f);
+      __syncthreads();
+      for (int i = threadIdx.x; i < d; i += blockDim.x) row[i] = (row[i] - mean) * inv;
+    }
+    __syncthreads();
+  }
+  constexpr int Vn = WVec<W>::N;
+  const int nvec = d / Vn;
+  const int rows_per_iter = 2 * kGemvWarps;
+  for (int r0 = blockIdx.x * rows_per_iter; r0 < N; r0 += gridDim.x * rows_per_iter) {
+    const int r = r0 + warp * 2;
+    if (r >= N) continue;
+    const bool two = r + 1 < N;
+    float acc[2][TT];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int t = 0; t < TT; ++t) acc[i][t] = 0.f;
+    const W* w0 = w + (size_t)r * d;
+    const W* w1 = w0 + d;
+    for (int vi = lane; vi < nvec; vi += 64) {
+      const bool hi = vi + 32 < nvec;
+      uint4 u[4];
+      u[0] = ld_stream_u4(w0 + (size_t)vi * Vn);
+      if (two) u[1] = ld_stream_u4(w1 + (size_t)vi * Vn);
+      if (hi) {
+        u[2] = ld_stream_u4(w0 + (size_t)(vi + 32) * Vn);
+        if (two) u[3] = ld_stream_u4(w1 + (size_t)(vi + 32) * Vn);
+      }
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        if (hh == 1 && !hi) break;
+        const int k0 = (vi + hh * 32) * Vn;
+        float f0[Vn], f1[Vn];
+        WVec<W>::widen(u[hh * 2], f0);
+        if (two) WVec<W>::widen(u[hh * 2 + 1], f1);
+#pragma unroll
+        for (int t = 0; t < TT; ++t) {
+          if (t < nt) {
+            const float* hr = h + (size_t)t * d + k0;
+#pragma unroll
+            for (int q = 0; q < Vn; ++q) {
+              acc[0][t] = fmaf(f0[q], hr[q], acc[0][t]);
+              if (two) acc[1][t] = fmaf(f1[q], hr[q], acc[1][t]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      if (i == 1 && !two) break;
+#pragma unroll
+      for (int t = 0; t < TT; ++t) {
+        if (t < nt) {
+          float v = warp_sum(acc[i][t]);
+          if (lane == 0) {
+            const size_t o = (size_t)t * N + r + i;
+            y[o] = residual ? residual[o] + v : v;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Single-query attention over the KV cache for B sequences (one new position
+// each, at pos[b]).  qkv (B, 3d) = [q | k | v]; the new k/v rows are written to
+// the cache first.  One CTA per (sequence, head), head_dim <= 256.
+__global__ void attn_decode_kernel(const float* __restrict__ qkv, float* __restrict__ kc,
+                                   float* __restrict__ vc, const int* __restrict__ pos, int d, int H,
+                                   int max_len, float* __restrict__ out) {
+  extern __shared__ __align__(16) float sc[];  // max_len scores + hd q
+  __shared__ float red[32];
+  const int b = blockIdx.x / H, hh = blockIdx.x % H;
+  const int hd = d / H;
+  const int p = pos[b];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  float* q = sc + max_len;
+  const float* src = qkv + (size_t)b * 3 * d;
+  float* kr = kc + ((size_t)b * max_len + p) * d + hh * hd;
+  float* vr = vc + ((size_t)b * max_len + p) * d + hh * hd;
+  for (int e = threadIdx.x; e < hd; e += blockDim.x) {
+    q[e] = src[hh * hd + e];
+    kr[e] = src[d + hh * hd + e];
+    vr[e] = src[2 * d + hh * hd + e];
+  }
+  __threadfence_block();
+  __syncthreads();
+  const float scale = 1.0f / sqrtf((float)hd);
+  // scores: one warp per position
+  float mx = -INFINITY;
+  for (int j = warp; j <= p; j += nw) {
+    const float* kj = kc + ((size_t)b * max_len + j) * d + hh * hd;
+    float s = 0.f;
+    for (int e = lane; e < hd; e += 32) s = fmaf(q[e], kj[e], s);
+    s = warp_sum(s) * scale;
+    if (lane == 0) sc[j] = s;
+    mx = fmaxf(mx, s);
+  }
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  mx = -INFINITY;
+  for (int i = 0; i < nw; ++i) mx = fmaxf(mx, red[i]);
+  __syncthreads();
+  float sum = 0.f;
+  for (int j = threadIdx.x; j <= p; j += blockDim.x) {
+    float e = expf(sc[j] - mx);
+    sc[j] = e;
+    sum += e;
+  }
+  sum = warp_sum(sum);
+  if (lane == 0) red[warp] = sum;
+  __syncthreads();
+  sum = 0.f;
+  for (int i = 0; i < nw; ++i) sum += red[i];
+  const float inv = 1.0f / sum;
+  for (int e = threadIdx.x; e < hd; e += blockDim.x) {
+    float acc = 0.f;
+    for (int j = 0; j <= p; ++j) acc = fmaf(sc[j], vc[((size_t)b * max_len + j) * d + hh * hd + e], acc);
+    out[(size_t)b * d + hh * hd + e] = acc * inv;
+  }
+}
+
+// x[b] = embed[tok[b]] + pe[pos[b]]  (toymoe.py:172), optionally ln_out = LN(x)
+__global__ void embed_kernel(const int* __restrict__ tok, const int* __restrict__ pos,
+                             const float* __restrict__ embed, const float* __restrict__ pe, int d,
+                             float* __restrict__ x, float* __restrict__ ln_out) {
+  __shared__ float red[32];
+  const int b = blockIdx.x;
+  const float* er = embed + (size_t)tok[b] * d;
+  const float* pr = pe + (size_t)pos[b] * d;
+  float sum = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float v = er[i] + pr[i];
+    x[(size_t)b * d + i] = v;
+    sum += v;
+  }
+  if (!ln_out) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  sum = warp_sum(sum);
+  if (lane == 0) red[warp] = sum;
+  __syncthreads();
+  float mean = 0.f;
+  for (int w = 0; w < nw; ++w) mean += red[w];
+  mean /= (float)d;
+  __syncthreads();
+  float q = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float c = x[(size_t)b * d + i] - mean;
+    q += c * c;
+  }
+  q = warp_sum(q);
+  if (lane == 0) red[warp] = q;
+  __syncthreads();
+  float var = 0.f;
+  for (int w = 0; w < nw; ++w) var += red[w];
+  const float inv = 1.0f / sqrtf(var / (float)d + 1e-5f);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) ln_out[(size_t)b * d + i] = (x[(size_t)b * d + i] - mean) * inv;
+}
+
+__global__ void advance_kernel(int* pos, int B, int* tok, const int* next_tok) {
+  const int b = threadIdx.x;
+  if (b < B) {
+    pos[b] += 1;
+    if (next_tok) tok[b] = next_tok[b];
+  }
+}
+
+template <typename W>
+static int launch_gemv(const float* x, int T, int d, int do_ln, const W* w, int N, const float* res, float* y,
+                       cudaStream_t s) {
+  const size_t smem = sizeof(float) * (size_t)((T <= 1 ? 1 : T <= 2 ? 2 : T <= 4 ? 4 : 8)) * d;
+  const int rows_per_iter = 2 * kGemvWarps;
+  int grid = (N + rows_per_iter - 1) / rows_per_iter;
+  const int cap = sm_count() * 4;
+  if (grid > cap) grid = cap;
+#define GEMV_CASE(TTV)                                                                              \
+  {                                                                                                 \
+    auto k = dense_gemv_kernel<W, TTV>;                                                             \
+    set_smem_once((const void*)k, smem);                                                           \
+    k<<<grid, kGemvThreads, smem, s>>>(x, T, d, do_ln, w, N, res, y);                               \
+  }
+  if (T <= 1) GEMV_CASE(1) else if (T <= 2) GEMV_CASE(2) else if (T <= 4) GEMV_CASE(4) else GEMV_CASE(8)
+#undef GEMV_CASE
+  MOBILE_CHECK_LAUNCH("dense_gemv");
+  return MOBILE_OK;
+}
+
+}  // namespace mobile
+
+using namespace mobile;
+
+extern "C" int mobile_dense_gemv(const float* x, int T, int d, int do_ln, const void* w, int w_dtype, int N,
+                                 const float* residual, float* y, void* stream) {
+  if (T < 0 || T > 8 || d <= 0 || N <= 0) { set_error("dense_gemv: bad shape T=%d d=%d N=%d (T <= 8)", T, d, N); return MOBILE_ERR_INVALID; }
+  if (T == 0) return MOBILE_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (w_dtype == MOBILE_BF16) {
+    if (d % 8) { set_error("dense_gemv: d=%d must be a multiple of 8", d); return MOBILE_ERR_UNSUPPORTED; }
+    return launch_gemv<__nv_bfloat16>(x, T, d, do_ln, (const __nv_bfloat16*)w, N, residual, y, s);
+  }
+  if (w_dtype == MOBILE_F32) {
+    if (d % 4) { set_error("dense_gemv: d=%d must be a multiple of 4", d); return MOBILE_ERR_UNSUPPORTED; }
+    return launch_gemv<float>(x, T, d, do_ln, (const float*)w, N, residual, y, s);
+  }
+  set_error("dense_gemv: unsupported dtype %d", w_dtype);
+  return MOBILE_ERR_UNSUPPORTED;
+}
+
+extern "C" int mobile_attn_decode(const float* qkv, float* k_cache, float* v_cache, const int* pos, int B, int d,
+                                  int H, int max_len, float* out, void* stream) {
+  if (B <= 0 || d <= 0 || H <= 0 || d % H || max_len <= 0) { set_error("attn_decode: bad shape"); return MOBILE_ERR_INVALID; }
+  const size_t smem = sizeof(float) * ((size_t)max_len + d / H);
+  if (smem > 200 * 1024) { set_error("attn_decode: max_len=%d too long", max_len); return MOBILE_ERR_UNSUPPORTED; }
+  set_smem_once((const void*)attn_decode_kernel, smem);
+  attn_decode_kernel<<<B * H, 128, smem, (cudaStream_t)stream>>>(qkv, k_cache, v_cache, pos, d, H, max_len, out);
+  MOBILE_CHECK_LAUNCH("attn_decode");
+  return MOBILE_OK;
+}
+
+extern "C" int mobile_embed(const int* tok, const int* pos, const float* embed, const float* pe, int B, int d,
+                            float* x, float* ln_out, void* stream) {
+  if (B <= 0 || d <= 0) { set_error("embed: bad shape"); return MOBILE_ERR_INVALID; }
+  embed_kernel<<<B, 256, 0, (cudaStream_t)stream>>>(tok, pos, embed, pe, d, x, ln_out);
+  MOBILE_CHECK_LAUNCH("embed");
+  return MOBILE_OK;
+}
+
+extern "C" int mobile_advance(int* pos, int B, int* tok, const int* next_tok, void* stream) {
+  if (B <= 0 || B > 1024) { set_error("advance: bad B"); return MOBILE_ERR_INVALID; }
+  advance_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(pos, B, tok, next_tok);
+  MOBILE_CHECK_LAUNCH("advance");
+  return MOBILE_OK;
+}

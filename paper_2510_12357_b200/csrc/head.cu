@@ -283,10 +283,10 @@ extern "C" int mobile_head_confidence(const float* x, const void* w_head, int w_
   cudaStream_t s = (cudaStream_t)stream;
   dim3 grid(gx, ty), block(kHeadThreads);
   if (w_dtype == MOBILE_BF16) {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(head_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem_once((const void*)head_kernel<__nv_bfloat16>, smem);
     head_kernel<__nv_bfloat16><<<grid, block, smem, s>>>(a);
   } else if (w_dtype == MOBILE_F32) {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(head_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem_once((const void*)head_kernel<float>, smem);
     head_kernel<float><<<grid, block, smem, s>>>(a);
   } else {
     set_error("head: unsupported weight dtype %d", w_dtype);

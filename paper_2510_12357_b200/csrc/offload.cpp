@@ -118,6 +118,20 @@ static int settle(mobile_offload* o) {
   return MOBILE_OK;
 }
 
+// Every copy has landed (caller synchronised the copy stream): settle all
+// in-flight entries at the next clock value.
+static void settle_all(mobile_offload* o) {
+  o->clock += 1.0;
+  std::vector<int> buf(2 * (size_t)o->slots);
+  const int n = mobile_cache_entries(o->cache, buf.data(), o->slots);
+  for (int i = 0; i < n; ++i) {
+    double r;
+    if (mobile_cache_lookup(o->cache, buf[2 * i], buf[2 * i + 1], &r, nullptr) == MOBILE_OK && r == kInf)
+      mobile_cache_set_ready(o->cache, buf[2 * i], buf[2 * i + 1], o->clock);
+  }
+  o->awaited.clear();
+}
+
 int mobile_offload_require(mobile_offload* o, int layer, const int* experts, int n,
                            void* compute_stream, int* slot_table_host, int* issued_out) {
   cudaStream_t cs = (cudaStream_t)compute_stream;
@@ -127,11 +141,14 @@ int mobile_offload_require(mobile_offload* o, int layer, const int* experts, int
     int status = 0, slot = -1;
     double ready = 0;
     int st = mobile_cache_request(o->cache, layer, e, o->clock, 0, nullptr, kInf, &status, &ready, &slot);
-    if (st == MOBILE_ERR_DEADLOCK && !o->awaited.empty()) {
+    if (st == MOBILE_ERR_DEADLOCK) {
       // every slot is pinned or in flight: stall until the compute stream has
-      // consumed what it waited on, settle, and retry (the simulator's stall)
-      OFF_CUDA(cudaStreamSynchronize(cs), "deadlock stall");
-      settle(o);
+      // consumed what it waited on and every issued copy has landed, settle,
+      // and retry (the simulator's stall); a second failure means every slot
+      // is pinned by this layer -- a true CapacityDeadlock.
+      OFF_CUDA(cudaStreamSynchronize(cs), "deadlock stall (compute)");
+      OFF_CUDA(cudaStreamSynchronize(o->copy), "deadlock stall (copy)");
+      settle_all(o);
       st = mobile_cache_request(o->cache, layer, e, o->clock, 0, nullptr, kInf, &status, &ready, &slot);
     }
     if (st != MOBILE_OK) return st;
@@ -183,15 +200,7 @@ int mobile_offload_token_end(mobile_offload* o) {
   // Prefetches never consumed by a layer are drained here so no entry stays
   // in flight across tokens (deterministic: the copy stream is synchronised).
   OFF_CUDA(cudaStreamSynchronize(o->copy), "token_end drain");
-  o->clock += 1.0;
-  std::vector<int> buf(2 * (size_t)o->slots);
-  const int n = mobile_cache_entries(o->cache, buf.data(), o->slots);
-  for (int i = 0; i < n; ++i) {
-    double r;
-    if (mobile_cache_lookup(o->cache, buf[2 * i], buf[2 * i + 1], &r, nullptr) == MOBILE_OK && r == kInf)
-      mobile_cache_set_ready(o->cache, buf[2 * i], buf[2 * i + 1], o->clock);
-  }
-  o->awaited.clear();
+  settle_all(o);
   return mobile_cache_token_end(o->cache);
 }
 

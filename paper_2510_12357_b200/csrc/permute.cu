@@ -76,24 +76,62 @@ __global__ void __launch_bounds__(kPermThreads) permute_kernel(const int* __rest
 
 // x_out[t] = x[t] + (sum_j g[t,j] * Y[t*k+j]  (selection order)
 //                    + sum_s gate_s(t) * Ys[t][s])          toymoe.py:204, 207
-__global__ void combine_kernel(const float* __restrict__ x, const float* __restrict__ Y,
-                               const float* __restrict__ gates, const int* __restrict__ k_tok,
-                               int k_max, int d, const float* __restrict__ Ys, int n_shared,
-                               const float* __restrict__ shared_logits, int T,
-                               float* __restrict__ x_out) {
+// and, if ln_out, ln_out[t] = LN(x_out[t]) -- the next layer's attention input
+// (toymoe.py:178), fused here because this CTA already holds the whole row.
+__global__ void __launch_bounds__(1024) combine_kernel(const float* __restrict__ x, const float* __restrict__ Y,
+                                                      const float* __restrict__ gates, const int* __restrict__ k_tok,
+                                                      int k_max, int d, const float* __restrict__ Ys, int n_shared,
+                                                      const float* __restrict__ shared_logits, int T,
+                                                      float* __restrict__ x_out, float* __restrict__ ln_out) {
+  __shared__ float red[32];
+  __shared__ float sg[16];    // gates (selection order) then shared-expert gates
   const int t = blockIdx.x;
   const int kt = k_tok ? k_tok[t] : k_max;
-  const float* g = gates + (size_t)t * k_max;
+  if (threadIdx.x < kt) sg[threadIdx.x] = gates[(size_t)t * k_max + threadIdx.x];
+  if (threadIdx.x < n_shared)
+    sg[8 + threadIdx.x] = shared_logits ? sigmoid_f(shared_logits[(size_t)t * n_shared + threadIdx.x]) : 1.0f;
+  __syncthreads();
+  float sum = 0.f;
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    // issue every independent load first, then accumulate in selection order
+    float yv[8], ys[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) yv[j] = j < kt ? Y[((size_t)t * k_max + j) * d + i] : 0.f;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) ys[s] = s < n_shared ? Ys[((size_t)t * n_shared + s) * d + i] : 0.f;
+    const float xv = x[(size_t)t * d + i];
     float m = 0.f;
-    for (int j = 0; j < kt; ++j) m = fmaf(g[j], Y[((size_t)t * k_max + j) * d + i], m);
-    for (int s = 0; s < n_shared; ++s) {
-      float ys = Ys[((size_t)t * n_shared + s) * d + i];
-      if (shared_logits) ys = sigmoid_f(shared_logits[(size_t)t * n_shared + s]) * ys;
-      m += ys;
-    }
-    x_out[(size_t)t * d + i] = x[(size_t)t * d + i] + m;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) if (j < kt) m = fmaf(sg[j], yv[j], m);
+    for (int j = 8; j < kt; ++j) m = fmaf(gates[(size_t)t * k_max + j], Y[((size_t)t * k_max + j) * d + i], m);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) if (s < n_shared) m += sg[8 + s] * ys[s];
+    const float v = xv + m;
+    x_out[(size_t)t * d + i] = v;
+    sum += v;
   }
+  if (!ln_out) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  sum = warp_sum(sum);
+  if (lane == 0) red[warp] = sum;
+  __syncthreads();
+  float mean = 0.f;
+  for (int w = 0; w < nw; ++w) mean += red[w];
+  mean /= (float)d;
+  __syncthreads();
+  float q = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float c = x_out[(size_t)t * d + i] - mean;
+    q += c * c;
+  }
+  q = warp_sum(q);
+  if (lane == 0) red[warp] = q;
+  __syncthreads();
+  float var = 0.f;
+  for (int w = 0; w < nw; ++w) var += red[w];
+  const float inv = 1.0f / sqrtf(var / (float)d + 1e-5f);
+  for (int i = threadIdx.x; i < d; i += blockDim.x)
+    ln_out[(size_t)t * d + i] = (x_out[(size_t)t * d + i] - mean) * inv;
 }
 
 }  // namespace mobile
@@ -112,11 +150,13 @@ extern "C" int mobile_permute(const int* idx, const int* k_tok, int T, int k_max
 
 extern "C" int mobile_combine(const float* x, const float* Y, const float* gates, const int* k_tok,
                               int T, int k_max, int d, const float* Y_shared, int n_shared,
-                              const float* shared_logits, float* x_out, void* stream) {
+                              const float* shared_logits, float* x_out, float* ln_out, void* stream) {
   if (T < 0 || d <= 0 || k_max <= 0 || n_shared < 0) { set_error("combine: bad shape"); return MOBILE_ERR_INVALID; }
   if (T == 0) return MOBILE_OK;
-  combine_kernel<<<T, 256, 0, (cudaStream_t)stream>>>(x, Y, gates, k_tok, k_max, d, Y_shared,
-                                                      Y_shared ? n_shared : 0, shared_logits, T, x_out);
+  if (n_shared > 8) { set_error("combine: at most 8 shared experts"); return MOBILE_ERR_UNSUPPORTED; }
+  const int threads = d >= 1024 ? 1024 : ((d + 31) / 32) * 32;
+  combine_kernel<<<T, threads, 0, (cudaStream_t)stream>>>(x, Y, gates, k_tok, k_max, d, Y_shared,
+                                                      Y_shared ? n_shared : 0, shared_logits, T, x_out, ln_out);
   MOBILE_CHECK_LAUNCH("combine");
   return MOBILE_OK;
 }

@@ -36,7 +36,54 @@ struct RouterArgs {
   int* idx_out;
   float* gates_out;
   int* flags;
+  int* perm_offsets;   // fused permute (single token tile, T*k_max <= 32), else NULL
+  int* perm_pairs;
+  int* perm_active;
 };
+
+// Deterministic stable permute of <= 32 (token, slot) pairs by one warp
+// (the mobile_permute contract): bitonic sort of keys (expert << 6 | pair).
+__device__ void warp_permute(const RouterArgs& a) {
+  const int lane = threadIdx.x & 31;
+  const int P = a.T * a.k_max;
+  int key = 0x7fffffff;
+  if (lane < P) {
+    const int t = lane / a.k_max, j = lane - t * a.k_max;
+    const int kt = a.k_tok ? a.k_tok[t] : a.k_max;
+    const int e = j < kt ? a.idx_out[lane] : -1;
+    if (e >= 0 && e < a.E) key = (e << 6) | lane;
+  }
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int other = __shfl_xor_sync(0xffffffffu, key, j);
+      const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+      key = (lower == up) ? min(key, other) : max(key, other);
+    }
+  }
+  const bool valid = key != 0x7fffffff;
+  const int nvalid = __popc(__ballot_sync(0xffffffffu, valid));
+  const int e_me = valid ? (key >> 6) : 0x7fffffff;
+  if (valid) a.perm_pairs[lane] = key & 63;
+  const int e_prev = __shfl_up_sync(0xffffffffu, e_me, 1);
+  const bool first = valid && (lane == 0 || e_prev != e_me);
+  const unsigned fm = __ballot_sync(0xffffffffu, first);
+  if (first) a.perm_active[1 + __popc(fm & ((1u << lane) - 1u))] = e_me;
+  if (lane == 0) a.perm_active[0] = __popc(fm);
+  // offsets[e] = #pairs with expert < e  (uniform trip count: every lane
+  // takes part in every shuffle)
+  for (int base = 0; base <= a.E; base += 32) {
+    const int e = base + lane;
+    int c = 0;
+    for (int j = 0; j < 32; ++j) {
+      const int ej = __shfl_sync(0xffffffffu, e_me, j);
+      c += ej < e;
+    }
+    if (e <= a.E) a.perm_offsets[e] = c;
+  }
+  (void)nvalid;
+}
 
 // Block-wide LayerNorm statistics for TT rows held in smem (two-pass, like
 // numpy: mean, then mean of squared deviations; toymoe.py:129-132).
@@ -274,6 +321,10 @@ __global__ void __launch_bounds__(kRouterThreads) router_kernel(RouterArgs a) {
     // compact own logits (first E of the Etot row) are contiguous already
     warp_route_token(a, t0 + t, logits + (size_t)t * Etot);
   }
+  if (a.perm_offsets) {  // 4. fused permute (decode): every token of the launch is in this tile
+    __syncthreads();
+    if (warp == 0) warp_permute(a);
+  }
 }
 
 template <typename W, int TT>
@@ -283,10 +334,7 @@ static int launch_router(const RouterArgs& a, cudaStream_t stream) {
   if (a.T <= 8) cs = min(8, max(1, (Etot + 7) / 8));
   const size_t smem = sizeof(float) * ((size_t)TT * a.d + (size_t)TT * Etot + 64);
   auto kern = router_kernel<W, TT>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_status(e, "router smem attr");
-  }
+  if (int st = set_smem_once((const void*)kern, smem)) return st;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs, (a.T + TT - 1) / TT, 1);
   cfg.blockDim = dim3(kRouterThreads, 1, 1);
@@ -354,21 +402,35 @@ __global__ void topk_rows_kernel(const F* __restrict__ rows, int R, int E, int k
 
 using namespace mobile;
 
+extern "C" int mobile_permute(const int* idx, const int* k_tok, int T, int k_max, int E, int* offsets,
+                              int* sorted_pairs, int* active, void* stream);
+
 extern "C" int mobile_router_topk(const float* x, float* h2_out, const void* w_router, int w_dtype,
                                   int T, int d, int E, int n_extra, int k_max, const int* k_tok,
                                   const float* replay, const uint8_t* replay_mask, int reuse_gates,
                                   int gate_norm, float* logits_out, float* extra_out, int* idx_out,
-                                  float* gates_out, int* flags, void* stream) {
+                                  float* gates_out, int* flags, int* perm_offsets, int* perm_pairs,
+                                  int* perm_active, void* stream) {
   if (T < 0 || d <= 0 || E <= 0 || k_max <= 0) { set_error("router: bad shape T=%d d=%d E=%d k=%d", T, d, E, k_max); return MOBILE_ERR_INVALID; }
   if (E > kMaxE) { set_error("router: E=%d exceeds kernel limit %d", E, kMaxE); return MOBILE_ERR_UNSUPPORTED; }
   if (n_extra < 0 || n_extra > kMaxExtra) { set_error("router: n_extra=%d unsupported", n_extra); return MOBILE_ERR_UNSUPPORTED; }
   if (k_max > E) { set_error("k (%d) exceeds number of experts (%d)", k_max, E); return MOBILE_ERR_K_EXCEEDS; }
   if (T == 0) return MOBILE_OK;
   if (d % 4 != 0 || (w_dtype == MOBILE_BF16 && d % 8 != 0)) { set_error("router: d=%d must be a multiple of 8", d); return MOBILE_ERR_UNSUPPORTED; }
-  RouterArgs a{x, h2_out, w_router, T, d, E, n_extra, k_max, k_tok, replay, replay_mask, reuse_gates,
-               gate_norm, logits_out, extra_out, idx_out, gates_out, flags};
-  cudaStream_t s = (cudaStream_t)stream;
   const int TT = T == 1 ? 1 : (T == 2 ? 2 : 4);
+  const bool fuse = perm_offsets && perm_pairs && perm_active && T <= TT && T * k_max <= 32;
+  RouterArgs a{x, h2_out, w_router, T, d, E, n_extra, k_max, k_tok, replay, replay_mask, reuse_gates,
+               gate_norm, logits_out, extra_out, idx_out, gates_out, flags,
+               fuse ? perm_offsets : nullptr, fuse ? perm_pairs : nullptr, fuse ? perm_active : nullptr};
+  cudaStream_t s = (cudaStream_t)stream;
+  if (perm_offsets && !fuse) {
+    int st = MOBILE_OK;
+    if (w_dtype == MOBILE_BF16) st = TT == 4 ? launch_router<__nv_bfloat16, 4>(a, s) : TT == 2 ? launch_router<__nv_bfloat16, 2>(a, s) : launch_router<__nv_bfloat16, 1>(a, s);
+    else if (w_dtype == MOBILE_F32) st = TT == 4 ? launch_router<float, 4>(a, s) : TT == 2 ? launch_router<float, 2>(a, s) : launch_router<float, 1>(a, s);
+    else { set_error("router: unsupported weight dtype %d", w_dtype); return MOBILE_ERR_UNSUPPORTED; }
+    if (st) return st;
+    return mobile_permute(idx_out, k_tok, T, k_max, E, perm_offsets, perm_pairs, perm_active, stream);
+  }
   if (w_dtype == MOBILE_BF16) {
     if (TT == 1) return launch_router<__nv_bfloat16, 1>(a, s);
     if (TT == 2) return launch_router<__nv_bfloat16, 2>(a, s);
@@ -394,10 +456,10 @@ extern "C" int mobile_topk_rows(const void* rows, int dtype, int R, int E, int k
   cudaStream_t s = (cudaStream_t)stream;
   dim3 grid((R + wpb - 1) / wpb), block(32 * wpb);
   if (dtype == MOBILE_F64) {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(topk_rows_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem_once((const void*)topk_rows_kernel<double>, smem);
     topk_rows_kernel<double><<<grid, block, smem, s>>>((const double*)rows, R, E, k, idx_out, flags);
   } else if (dtype == MOBILE_F32) {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(topk_rows_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem_once((const void*)topk_rows_kernel<float>, smem);
     topk_rows_kernel<float><<<grid, block, smem, s>>>((const float*)rows, R, E, k, idx_out, flags);
   } else {
     set_error("topk_rows: unsupported dtype %d", dtype);

@@ -61,6 +61,7 @@ class MobileGenerator:
         self.head_out = dict(conf=torch.empty(1, device=dev), argmax=torch.empty(1, device=dev, dtype=torch.int32),
                              fallback=torch.empty(1, device=dev, dtype=torch.uint8))
         self.stats = DecodeStats()
+        self.timer = None  # optional kernel timer (bench roofline)
 
     def _head(self, x_last, gamma):
         return K.head_confidence(x_last, self.dm.dw.head, gamma, self.spec.logit_scale, ws=self.ws, out=self.head_out)
@@ -78,13 +79,32 @@ class MobileGenerator:
                 self.runtime.token_end()
         return sess
 
+    def step_full(self, sess: DecodeSession, last: int, record: bool = False) -> KVDecision:
+        """Full-top-k baseline step: one k_big pass with its own routing,
+        experts loaded on demand (engine.simulate_full_stream, on_demand plan)."""
+        s, dev = self.spec, self.dm.device
+        tok = torch.tensor([[last]], dtype=torch.long, device=dev)
+        rt = self.runtime
+        hook = rt.demand_hook("full") if rt else None
+        x, states, idx = sess.run(tok, self.k_b, s.k_big, advance=False, expert_hook=hook, timer=self.timer)
+        out = self._head(x, 1.0)
+        token = int(out["argmax"].item())
+        if rt:
+            rt.sync_point()
+            rt.token_end()
+        sess.pos += 1
+        self.stats.tokens += 1
+        self.stats.big_passes += 1
+        return KVDecision(token, ACCEPTED_BIG, float(out["conf"].item()) if record else float("nan"),
+                          [], idx[:, 0].cpu().tolist() if record else None, None)
+
     def step(self, sess: DecodeSession, last: int, policy: PolicySpec, forced_fallback: bool | None = None,
              record: bool = False) -> KVDecision:
         s, dev = self.spec, self.dm.device
         tok = torch.tensor([[last]], dtype=torch.long, device=dev)
         rt = self.runtime
         hook = rt.demand_hook("little") if rt else None
-        x, states, idx_l = sess.run(tok, self.k_l, s.k_little, advance=False, expert_hook=hook)
+        x, states, idx_l = sess.run(tok, self.k_l, s.k_little, advance=False, expert_hook=hook, timer=self.timer)
         out = self._head(x, policy.gamma)
         self.stats.little_passes += 1
         fb_dev = out["fallback"]
@@ -93,15 +113,17 @@ class MobileGenerator:
         else:
             fb = bool(forced_fallback)
         conf = float(out["conf"].item()) if record else float("nan")
+        if rt:
+            torch.cuda.current_stream().synchronize()
+            rt.sync_point()
         if fb:
             if rt:
-                rt.token_end(keep_pins=False)
                 plan_hook, layer_hook = rt.plan_hooks(states[:, 0], s.k_big)
             else:
                 plan_hook = layer_hook = None
             xb, _, idx_b = sess.run(tok, self.k_b, s.k_big, replay=states, replay_mask=self.one,
                                     reuse_gates=policy.reuse_little_gates, advance=False,
-                                    expert_hook=plan_hook, layer_hook=layer_hook)
+                                    expert_hook=plan_hook, layer_hook=layer_hook, timer=self.timer)
             out = self._head(xb, policy.gamma)
             self.stats.big_passes += 1
             self.stats.fallbacks += 1
@@ -118,7 +140,7 @@ class MobileGenerator:
         return KVDecision(token, ACCEPTED_BIG if fb else ACCEPTED_LITTLE, conf, [], None, None)
 
     def generate(self, prompt: list[int], policy: PolicySpec, max_new: int, fallback_flags=None,
-                 record: bool = True, stop_at_eos: bool = True):
+                 record: bool = True, stop_at_eos: bool = True, full: bool = False):
         if not prompt:
             raise ValueError("prompt is empty")
         if max_new < 1:
@@ -129,7 +151,10 @@ class MobileGenerator:
         tokens, decisions = list(prompt), []
         while len(decisions) < max_new:
             forced = None if fallback_flags is None else bool(fallback_flags[len(decisions)])
-            d = self.step(sess, tokens[-1], policy, forced, record)
+            if full:
+                d = self.step_full(sess, tokens[-1], record)
+            else:
+                d = self.step(sess, tokens[-1], policy, forced, record)
             decisions.append(d)
             tokens.append(d.token)
             if stop_at_eos and d.token == self.spec.eos_token:

@@ -12,6 +12,13 @@ from . import _native as N
 
 _DT = {torch.float32: N.F32, torch.bfloat16: N.BF16, torch.float64: N.F64}
 
+# number of libmobile kernel launches issued through these wrappers (bench's gpu_launches)
+LAUNCHES = [0]
+
+
+def _count(n: int = 1) -> None:
+    LAUNCHES[0] += n
+
 
 def dtype_code(t: torch.Tensor) -> int:
     try:
@@ -32,8 +39,9 @@ def _dev(*ts):
 
 
 def router_topk(x, w_router, E, k_max, k_tok, *, n_extra=0, replay=None, replay_mask=None,
-                reuse_gates=False, gate_norm=N.GATE_SELECTED_SOFTMAX, out=None, stream=None):
-    """Fused LN + router GEMV + top-k + replay + gates (toymoe.py:188-201)."""
+                reuse_gates=False, gate_norm=N.GATE_SELECTED_SOFTMAX, out=None, perm=None, stream=None):
+    """Fused LN + router GEMV + top-k + replay + gates (toymoe.py:188-201).
+    With `perm` (dict offsets/sorted_pairs/active) the permute is fused too."""
     _dev(x, w_router, k_tok, replay, replay_mask)
     T, d = x.shape
     dev = x.device
@@ -50,7 +58,10 @@ def router_topk(x, w_router, E, k_max, k_tok, *, n_extra=0, replay=None, replay_
         N.ptr(x), N.ptr(out["h2"]), N.ptr(w_router), dtype_code(w_router), T, d, E, n_extra, k_max,
         N.ptr(k_tok), N.ptr(replay), N.ptr(replay_mask), int(bool(reuse_gates)), gate_norm,
         N.ptr(out["logits"]), N.ptr(out["extra"]) if n_extra else None, N.ptr(out["idx"]),
-        N.ptr(out["gates"]), N.ptr(out["flags"]), _s(stream))
+        N.ptr(out["gates"]), N.ptr(out["flags"]),
+        N.ptr(perm["offsets"]) if perm else None, N.ptr(perm["sorted_pairs"]) if perm else None,
+        N.ptr(perm["active"]) if perm else None, _s(stream))
+    _count()
     N.check(st, "router_topk")
     return out
 
@@ -62,6 +73,7 @@ def topk_rows(rows: torch.Tensor, k: int, stream=None):
     R, E = rows.shape
     idx = torch.empty(R, max(k, 0), device=rows.device, dtype=torch.int32)
     flags = torch.zeros(1, device=rows.device, dtype=torch.int32)
+    _count()
     N.check(N.lib.mobile_topk_rows(N.ptr(rows), dtype_code(rows), R, E, k, N.ptr(idx), N.ptr(flags), _s(stream)),
             "topk_rows")
     return idx, flags
@@ -86,6 +98,7 @@ def head_confidence(x, w_head, gamma, logit_scale, *, ws: HeadWorkspace, logits_
         out = dict(conf=torch.empty(T, device=x.device, dtype=torch.float32),
                    argmax=torch.empty(T, device=x.device, dtype=torch.int32),
                    fallback=torch.empty(T, device=x.device, dtype=torch.uint8))
+    _count()
     N.check(N.lib.mobile_head_confidence(
         N.ptr(x), N.ptr(w_head), dtype_code(w_head), T, d, V, float(logit_scale), float(gamma),
         N.ptr(logits_out), N.ptr(out["conf"]), N.ptr(out["argmax"]), N.ptr(out["fallback"]),
@@ -98,6 +111,7 @@ def softmax_rows(logits: torch.Tensor, out_dtype=torch.float64, stream=None):
     logits = logits.contiguous()
     T, V = logits.shape
     probs = torch.empty(T, V, device=logits.device, dtype=out_dtype)
+    _count()
     N.check(N.lib.mobile_softmax_rows(N.ptr(logits), dtype_code(logits), N.ptr(probs), dtype_code(probs),
                                       T, V, _s(stream)), "softmax_rows")
     return probs
@@ -107,6 +121,7 @@ def probs_check(probs: torch.Tensor, stream=None):
     """(sum, max) of a probability row in f64 (policy.py:69-79 inputs)."""
     _dev(probs)
     out = torch.empty(2, device=probs.device, dtype=torch.float64)
+    _count()
     N.check(N.lib.mobile_probs_check(N.ptr(probs.contiguous()), dtype_code(probs), probs.numel(), N.ptr(out),
                                      _s(stream)), "probs_check")
     return out
@@ -120,6 +135,7 @@ def permute(idx, k_tok, E, out=None, stream=None):
         out = dict(offsets=torch.empty(E + 1, device=dev, dtype=torch.int32),
                    sorted_pairs=torch.empty(max(T * k_max, 1), device=dev, dtype=torch.int32),
                    active=torch.empty(E + 1, device=dev, dtype=torch.int32))
+    _count()
     N.check(N.lib.mobile_permute(N.ptr(idx), N.ptr(k_tok), T, k_max, E, N.ptr(out["offsets"]),
                                  N.ptr(out["sorted_pairs"]), N.ptr(out["active"]), _s(stream)), "permute")
     return out
@@ -127,6 +143,7 @@ def permute(idx, k_tok, E, out=None, stream=None):
 
 def expert_gate_up(h2, offsets, sorted_pairs, active, max_active, max_tok, tok_div, d, I, w13_base_ptr,
                    expert_stride, slot, w_dtype, activation, U, stream=None):
+    _count()
     N.check(N.lib.mobile_expert_gate_up(
         N.ptr(h2), N.ptr(offsets), N.ptr(sorted_pairs), N.ptr(active), int(max_active), int(max_tok),
         int(tok_div), d, I, w13_base_ptr, int(expert_stride), N.ptr(slot), w_dtype, activation, N.ptr(U),
@@ -135,16 +152,85 @@ def expert_gate_up(h2, offsets, sorted_pairs, active, max_active, max_tok, tok_d
 
 def expert_down(U, offsets, sorted_pairs, active, max_active, max_tok, d, I, w2_base_ptr, expert_stride, slot,
                 w_dtype, Y, stream=None):
+    _count()
     N.check(N.lib.mobile_expert_down(
         N.ptr(U), N.ptr(offsets), N.ptr(sorted_pairs), N.ptr(active), int(max_active), int(max_tok), d, I,
         w2_base_ptr, int(expert_stride), N.ptr(slot), w_dtype, N.ptr(Y), _s(stream)), "expert_down")
 
 
-def combine(x, Y, gates, k_tok, Y_shared=None, n_shared=0, shared_logits=None, x_out=None, stream=None):
+def combine(x, Y, gates, k_tok, Y_shared=None, n_shared=0, shared_logits=None, x_out=None, ln_out=None,
+            stream=None):
     T, d = x.shape
     k_max = gates.shape[1]
     if x_out is None:
         x_out = torch.empty_like(x)
+    _count()
     N.check(N.lib.mobile_combine(N.ptr(x), N.ptr(Y), N.ptr(gates), N.ptr(k_tok), T, k_max, d, N.ptr(Y_shared),
-                                 int(n_shared), N.ptr(shared_logits), N.ptr(x_out), _s(stream)), "combine")
+                                 int(n_shared), N.ptr(shared_logits), N.ptr(x_out), N.ptr(ln_out), _s(stream)),
+            "combine")
     return x_out
+
+
+EPI_STORE, EPI_RELU, EPI_SWIGLU = 0, 1, 2
+
+
+def sg_group(*, w_base: int, K: int, rows: int, x, out, epi=EPI_STORE, stride=0, slot=None, x_div=1,
+             offsets=None, pairs=None, active=None, max_active=1, dense_T=0, residual=None):
+    return N.mobile_sg_group(w_base, int(stride), N.ptr(slot), N.ptr(x), int(x_div), N.ptr(offsets), N.ptr(pairs),
+                             N.ptr(active), int(dense_T), int(max_active), int(K), int(rows), N.ptr(out),
+                             N.ptr(residual), int(epi))
+
+
+def stream_gemv(groups, w_dtype: int, max_tokens: int, stream=None):
+    """Bulk-copy streaming GEMV over 1..4 groups in one launch (mobile_stream_gemv)."""
+    arr = (N.mobile_sg_group * len(groups))(*groups)
+    _count()
+    N.check(N.lib.mobile_stream_gemv(arr, len(groups), w_dtype, int(max_tokens), _s(stream)), "stream_gemv")
+
+
+def dense_gemv(x, w, *, do_ln=False, residual=None, out=None, stream=None):
+    """y = (residual +) LN?(x) @ w.T for T <= 8 rows; w (N, d) out-major."""
+    _dev(x, w)
+    T, d = x.shape
+    n_out = w.shape[0]
+    if out is None:
+        out = torch.empty(T, n_out, device=x.device, dtype=torch.float32)
+    _count()
+    _native_check(T, d, do_ln, x, w, n_out, residual, out, stream)
+    return out
+
+
+def attn_decode(qkv, k_cache, v_cache, pos, n_heads, out=None, stream=None):
+    B, d3 = qkv.shape
+    d = d3 // 3
+    max_len = k_cache.shape[1]
+    if out is None:
+        out = torch.empty(B, d, device=qkv.device, dtype=torch.float32)
+    _count()
+    N.check(N.lib.mobile_attn_decode(N.ptr(qkv), N.ptr(k_cache), N.ptr(v_cache), N.ptr(pos), B, d, n_heads, max_len,
+                                     N.ptr(out), _s(stream)), "attn_decode")
+    return out
+
+
+def embed(tok, pos, table, pe, out, ln_out=None, stream=None):
+    B = tok.shape[0]
+    _count()
+    N.check(N.lib.mobile_embed(N.ptr(tok), N.ptr(pos), N.ptr(table), N.ptr(pe), B, table.shape[1], N.ptr(out),
+                               N.ptr(ln_out), _s(stream)), "embed")
+    return out
+
+
+def advance(pos, tok=None, next_tok=None, stream=None):
+    _count()
+    N.check(N.lib.mobile_advance(N.ptr(pos), pos.shape[0], N.ptr(tok), N.ptr(next_tok), _s(stream)), "advance")
+
+
+def _native_check(T, d, do_ln, x, w, n_out, residual, out, stream):
+    N.check(N.lib.mobile_dense_gemv(N.ptr(x), T, d, int(bool(do_ln)), N.ptr(w), dtype_code(w), n_out,
+                                    N.ptr(residual), N.ptr(out), _s(stream)), "dense_gemv")
+
+
+def memcpy_async(dst: torch.Tensor, src: torch.Tensor, stream=None):
+    """Raw cudaMemcpyAsync (graph-capturable) between pinned host and device tensors."""
+    n = src.numel() * src.element_size()
+    N.check(N.lib.mobile_memcpy_async(N.ptr(dst), N.ptr(src), n, _s(stream)), "memcpy_async")

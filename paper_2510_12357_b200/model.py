@@ -18,6 +18,7 @@ Two execution modes share these kernels:
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 import torch
@@ -32,6 +33,9 @@ torch.backends.cuda.matmul.allow_tf32 = False
 torch.backends.cudnn.allow_tf32 = False
 
 _ACT = {"relu": N.ACT_RELU, "swiglu": N.ACT_SWIGLU}
+# expert FFN implementation: "stream" (bulk-copy TMA streaming, default) or
+# "warp" (register-streaming warp kernels); both are libmobile sm_100a kernels
+FFN_IMPL = os.environ.get("MOBILE_FFN", "stream")
 _GATE = {"selected_softmax": N.GATE_SELECTED_SOFTMAX, "softmax_all": N.GATE_SOFTMAX_ALL}
 
 
@@ -100,40 +104,115 @@ class MoBiLEMoE:
         self._scratch[key] = sc
         return sc
 
-    def forward(self, x: torch.Tensor, layer: int, k_tok: torch.Tensor, k_max: int, *, replay=None,
-                replay_mask=None, reuse_gates=False, experts: ExpertLocation | None = None,
-                pre_experts=None):
-        """x (T, d) f32 residual -> (x_out, scratch).  `pre_experts(idx)` is an
-        optional hook run between routing and the expert kernels (the offload
-        runtime uses it to make the selected experts resident)."""
+    def route(self, x: torch.Tensor, layer: int, k_tok: torch.Tensor, k_max: int, *, replay=None,
+              replay_mask=None, reuse_gates=False, logits_out=None, idx_out=None) -> dict:
+        """Router + permute (toymoe.py:188-201): returns the scratch dict with
+        `router` (h2, logits, idx, gates, ...) and `perm` (offsets, pairs, active)."""
+        T = x.shape[0]
+        sc = self.scratch(T, k_max)
+        rout = sc["router"]
+        if logits_out is not None or idx_out is not None:
+            rout = dict(rout)
+            if logits_out is not None:
+                rout["logits"] = logits_out
+            if idx_out is not None:
+                rout["idx"] = idx_out
+        r = K.router_topk(x, self.dw.router[layer], self.E, k_max, k_tok, n_extra=self.dw.n_gate_rows,
+                          replay=replay, replay_mask=replay_mask, reuse_gates=reuse_gates,
+                          gate_norm=self.gate_norm, out=rout, perm=sc["perm"])
+        return dict(sc, router=r)
+
+    def experts(self, x: torch.Tensor, layer: int, sc: dict, k_tok: torch.Tensor, k_max: int,
+                loc: ExpertLocation | None = None, timer=None, ln_out=None) -> torch.Tensor:
+        """Grouped expert FFN + shared experts + combine/residual (toymoe.py:202-207).
+
+        Default path: two bulk-copy streaming launches (gate-up of routed +
+        shared experts, then down of both) and the combine.  FFN_IMPL="warp"
+        selects the register-streaming warp kernels (mobile_expert_gate_up/down)."""
         T = x.shape[0]
         dw, E, d = self.dw, self.E, self.d
-        sc = self.scratch(T, k_max)
-        r = K.router_topk(x, dw.router[layer], E, k_max, k_tok, n_extra=dw.n_gate_rows, replay=replay,
-                          replay_mask=replay_mask, reuse_gates=reuse_gates, gate_norm=self.gate_norm,
-                          out=sc["router"])
-        p = K.permute(r["idx"], k_tok, E, out=sc["perm"])
-        if pre_experts is not None:
-            experts = pre_experts(layer, r, p)
-        loc = experts if experts is not None else self.resident(layer)
+        r, p = sc["router"], sc["perm"]
+        loc = loc if loc is not None else self.resident(layer)
         max_active = min(E, T * k_max)
+        if FFN_IMPL == "warp":
+            return self._experts_warp(x, layer, sc, k_tok, k_max, loc, timer, ln_out)
+        act_epi = K.EPI_SWIGLU if self.act == N.ACT_SWIGLU else K.EPI_RELU
+        rows13 = 2 * self.I if self.act == N.ACT_SWIGLU else self.I
+        g_up = [K.sg_group(w_base=loc.w13_base, stride=loc.stride, slot=loc.slot, K=d, rows=rows13, x=r["h2"],
+                           x_div=k_max, offsets=p["offsets"], pairs=p["sorted_pairs"], active=p["active"],
+                           max_active=max_active, out=sc["U"], epi=act_epi)]
+        g_dn = [K.sg_group(w_base=loc.w2_base, stride=loc.stride, slot=loc.slot, K=self.I, rows=d, x=sc["U"],
+                           offsets=p["offsets"], pairs=p["sorted_pairs"], active=p["active"],
+                           max_active=max_active, out=sc["Y"])]
+        Ys = None
+        if self.S:
+            base, sb = dw.shared[layer].data_ptr(), dw.shared_bytes
+            rows13s = 2 * self.Is if self.act == N.ACT_SWIGLU else self.Is
+            g_up.append(K.sg_group(w_base=base, stride=sb, K=d, rows=rows13s, x=r["h2"], x_div=self.S,
+                                   offsets=sc["s_offsets"], pairs=sc["s_pairs"], active=sc["s_active"],
+                                   max_active=self.S, out=sc["Us"], epi=act_epi))
+            g_dn.append(K.sg_group(w_base=base + dw.s_w13_elems * dw.elem_bytes, stride=sb, K=self.Is, rows=d,
+                                   x=sc["Us"], offsets=sc["s_offsets"], pairs=sc["s_pairs"], active=sc["s_active"],
+                                   max_active=self.S, out=sc["Ys"]))
+            Ys = sc["Ys"]
+        if timer is not None:
+            timer.start()
+        K.stream_gemv(g_up, self.wcode, T)
+        if timer is not None:
+            timer.stop(("gate_up", T, k_max))
+        K.stream_gemv(g_dn, self.wcode, T)
+        shared_logits = r["extra"] if dw.n_gate_rows else None
+        K.combine(x, sc["Y"], r["gates"], k_tok, Ys, self.S, shared_logits, x_out=sc["x_out"], ln_out=ln_out)
+        return sc["x_out"]
+
+    def _experts_warp(self, x, layer, sc, k_tok, k_max, loc, timer, ln_out):
+        T = x.shape[0]
+        dw, E, d = self.dw, self.E, self.d
+        r, p = sc["router"], sc["perm"]
+        max_active = min(E, T * k_max)
+        if timer is not None:
+            timer.start()
         K.expert_gate_up(r["h2"], p["offsets"], p["sorted_pairs"], p["active"], max_active, T, k_max, d, self.I,
                          loc.w13_base, loc.stride, loc.slot, self.wcode, self.act, sc["U"])
+        if timer is not None:
+            timer.stop(("routed", T, k_max))
         K.expert_down(sc["U"], p["offsets"], p["sorted_pairs"], p["active"], max_active, T, d, self.I,
                       loc.w2_base, loc.stride, loc.slot, self.wcode, sc["Y"])
         Ys = None
         if self.S:
-            sh = dw.shared[layer]
-            base = sh.data_ptr()
+            base = dw.shared[layer].data_ptr()
             sb = dw.shared_bytes
+            if timer is not None:
+                timer.start()
             K.expert_gate_up(r["h2"], sc["s_offsets"], sc["s_pairs"], sc["s_active"], self.S, T, self.S, d, self.Is,
                              base, sb, None, self.wcode, self.act, sc["Us"])
+            if timer is not None:
+                timer.stop(("shared", T, self.S))
             K.expert_down(sc["Us"], sc["s_offsets"], sc["s_pairs"], sc["s_active"], self.S, T, d, self.Is,
                           base + dw.s_w13_elems * dw.elem_bytes, sb, None, self.wcode, sc["Ys"])
             Ys = sc["Ys"]
         shared_logits = r["extra"] if dw.n_gate_rows else None
-        K.combine(x, sc["Y"], r["gates"], k_tok, Ys, self.S, shared_logits, x_out=sc["x_out"])
-        return sc["x_out"], sc
+        K.combine(x, sc["Y"], r["gates"], k_tok, Ys, self.S, shared_logits, x_out=sc["x_out"], ln_out=ln_out)
+        return sc["x_out"]
+
+    def forward(self, x: torch.Tensor, layer: int, k_tok: torch.Tensor, k_max: int, *, replay=None,
+                replay_mask=None, reuse_gates=False, experts: ExpertLocation | None = None,
+                hook=None, timer=None):
+        """x (T, d) f32 residual -> (x_out, scratch): route, then experts.
+
+        `hook` (optional) has `pre(layer, router_out, perm) -> ExpertLocation`,
+        run between routing and the expert kernels (the offload runtime makes
+        the selected experts resident there: engine.py:137-149), and
+        `post(layer)`, run once the layer's kernels are enqueued (unpin +
+        last-use events: engine.py:152-153).  `timer` (optional) brackets the
+        gate-up launches with CUDA events for the live roofline."""
+        sc = self.route(x, layer, k_tok, k_max, replay=replay, replay_mask=replay_mask, reuse_gates=reuse_gates)
+        if hook is not None:
+            experts = hook.pre(layer, sc["router"], sc["perm"])
+        x_out = self.experts(x, layer, sc, k_tok, k_max, experts, timer)
+        if hook is not None:
+            hook.post(layer)
+        return x_out, sc
 
 
 class DeviceModel:
@@ -147,26 +226,27 @@ class DeviceModel:
         self.head_ws: dict = {}
 
     # ------------------------------------------------------------- pieces
-    def _mm(self, h: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    def _lin(self, h: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+        """h @ w.T for an out-major weight (N, d)."""
         if w.dtype == torch.float32:
-            return h @ w
-        return (h.to(w.dtype) @ w).to(torch.float32)
+            return Fn.linear(h, w)
+        return Fn.linear(h.to(w.dtype), w).to(torch.float32)
 
     def attention_full(self, x: torch.Tensor, layer: int) -> torch.Tensor:
         """toymoe.py:178-186 over all n positions (causal), n_heads generalised."""
         dw, s = self.dw, self.spec
         n, d = x.shape
         h = Fn.layer_norm(x, (d,), eps=1e-5)
-        q, k, v = self._mm(h, dw.q[layer]), self._mm(h, dw.k[layer]), self._mm(h, dw.v[layer])
+        q, k, v = self._lin(h, dw.qkv[layer]).split(d, dim=-1)
         H = s.n_heads
         hd = d // H
-        qh, kh, vh = (t.view(n, H, hd).transpose(0, 1) for t in (q, k, v))
+        qh, kh, vh = (t.reshape(n, H, hd).transpose(0, 1) for t in (q, k, v))
         scores = (qh @ kh.transpose(1, 2)) / math.sqrt(hd)
         mask = torch.ones(n, n, dtype=torch.bool, device=x.device).triu(1)
         scores = scores.masked_fill(mask, float("-inf"))
         attn = torch.softmax(scores, dim=-1)
         out = (attn @ vh).transpose(0, 1).reshape(n, d)
-        return x + self._mm(out, dw.o[layer])
+        return x + self._lin(out, dw.o[layer])
 
     def head_workspace(self, T: int) -> K.HeadWorkspace:
         ws = self.head_ws.get(T)
@@ -231,8 +311,8 @@ class DecodeSession:
         H = s.n_heads
         hd = d // H
         h = Fn.layer_norm(x, (d,), eps=1e-5)
-        q, k, v = m._mm(h, dw.q[layer]), m._mm(h, dw.k[layer]), m._mm(h, dw.v[layer])
-        q, k, v = (t.view(Bn, n, d) for t in (q, k, v))
+        q, k, v = m._lin(h, dw.qkv[layer]).split(d, dim=-1)
+        q, k, v = (t.reshape(Bn, n, d) for t in (q, k, v))
         if rows is None:
             self.kc[layer, :, pos:pos + n] = k
             self.vc[layer, :, pos:pos + n] = v
@@ -250,10 +330,10 @@ class DecodeSession:
             scores = scores.masked_fill(mask, float("-inf"))
         attn = torch.softmax(scores, dim=-1)
         out = (attn @ vh).transpose(1, 2).reshape(Bn * n, d)
-        return x + m._mm(out, dw.o[layer])
+        return x + m._lin(out, dw.o[layer])
 
     def run(self, tokens: torch.Tensor, k_tok: torch.Tensor, k_max: int, *, rows=None, replay=None,
-            replay_mask=None, reuse_gates=False, advance=True, expert_hook=None, layer_hook=None):
+            replay_mask=None, reuse_gates=False, advance=True, expert_hook=None, layer_hook=None, timer=None):
         """Process `tokens` (Bn, n) at positions [pos, pos+n).  Returns
         (x_last (Bn, d), states (L, Bn*n, E) view of last-position logits, idx (L, Bn, k_max)).
         `replay` (L, Bn, E) applies to the last position of every row with replay_mask."""
@@ -278,7 +358,7 @@ class DecodeSession:
             if replay is not None:
                 rep_full[last] = replay[layer]
             x_new, sc = m.moe.forward(x, layer, k_tok, k_max, replay=rep_full, replay_mask=rep_mask_full,
-                                      reuse_gates=reuse_gates, pre_experts=expert_hook)
+                                      reuse_gates=reuse_gates, hook=expert_hook, timer=timer)
             lg = sc["router"]["logits"].view(Bn, n, s.num_experts)
             states[layer] = lg[:, -1]
             idx[layer] = sc["router"]["idx"].view(Bn, n, k_max)[:, -1]

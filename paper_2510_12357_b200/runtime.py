@@ -1,0 +1,311 @@
+"""Graph-captured decode step (the B200 hot loop around the MoBiLE layer).
+
+One decode step of B sequences is built from libmobile kernels only -- embed,
+per layer [LN+QKV GEMV, KV-cache attention, O GEMV + residual, fused router /
+top-k / replay, permute, grouped expert GEMVs, shared experts, combine], head +
+confidence -- with every position read from device memory, so each pass kind
+is captured once in CUDA graphs and replayed per token:
+
+  little : k_little experts, own routing                  (toymoe.little_forward)
+  big    : k_big experts, selection replayed from the little
+           pass's recorded logits (h_s)                      (toymoe.big_forward)
+  full   : k_big experts, own routing (full-top-k baseline)   (toymoe.full_forward)
+
+HBM-resident experts: a pass is ONE graph launch.  Offloaded experts: a pass
+is L+1 graph segments cut at each layer's routing, because the on-demand
+passes need the layer's selection on the host to issue expert copies
+(engine.py:243-244); the segment boundary is the single host sync per layer.
+Each segment starts with the H2D of the layer's slot table (a memcpy node
+reading pinned host memory written by the C++ cache runtime) and ends with
+the D2H of the next layer's active-expert list.  The replayed big pass needs
+no sync at all: its plan is known up front (policy.py:86-106), so all its
+segments, prefetches and waits are enqueued back to back.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _native as N
+from . import kernels as K
+from .model import DecodeSession, DeviceModel, positional
+from .policy import plan_from_targets
+
+KINDS = ("little", "big", "full")
+
+
+class StepEngine:
+    def __init__(self, dm: DeviceModel, batch: int, max_len: int, runtime=None, graphs: bool = True):
+        s = dm.spec
+        if batch > 8:
+            raise ValueError("StepEngine: batch <= 8 (GEMV decode path)")
+        self.dm, self.spec, self.B, self.max_len = dm, s, batch, max_len
+        self.rt = runtime
+        self.use_graphs = graphs
+        dev = dm.device
+        L, E, d, B = s.num_layers, s.num_experts, s.hidden_dim, batch
+        self.sess = DecodeSession(dm, batch, max_len)
+        f32, i32 = torch.float32, torch.int32
+        self.pe = positional(max_len, d, 0, dev).contiguous()
+        self.tok = torch.zeros(B, dtype=i32, device=dev)
+        self.pos = torch.zeros(B, dtype=i32, device=dev)
+        self.tok_host = torch.zeros(B, dtype=i32, pin_memory=True)
+        self.x = torch.empty(B, d, dtype=f32, device=dev)
+        self.ln = torch.empty(B, d, dtype=f32, device=dev)  # LN of the layer input (from embed / combine)
+        self.qkv = torch.empty(B, 3 * d, dtype=f32, device=dev)
+        self.att = torch.empty(B, d, dtype=f32, device=dev)
+        self.xa = torch.empty(B, d, dtype=f32, device=dev)
+        self.k = {"little": s.k_little, "big": s.k_big, "full": s.k_big}
+        self.k_tok = {kd: torch.full((B,), self.k[kd], dtype=i32, device=dev) for kd in KINDS}
+        self.states = {kd: torch.empty(L, B, E, dtype=f32, device=dev) for kd in KINDS}
+        self.idx = {kd: torch.empty(L, B, self.k[kd], dtype=i32, device=dev) for kd in KINDS}
+        self.ones = torch.ones(B, dtype=torch.uint8, device=dev)
+        self.head = {kd: dict(conf=torch.empty(B, dtype=f32, device=dev), argmax=torch.empty(B, dtype=i32, device=dev),
+                              fallback=torch.empty(B, dtype=torch.uint8, device=dev)) for kd in KINDS}
+        self.head_ws = K.HeadWorkspace(B, s.vocab_size, dev)
+        self.gamma = torch.zeros(1)  # host value baked at capture; see set_gamma
+        self._gamma = 0.7
+        self.graphs: dict = {}
+        self.stream = torch.cuda.Stream(device=dev)
+        if runtime is not None:
+            self.active_host = torch.zeros(L, E + 1, dtype=i32, pin_memory=True)
+        self.reuse_gates = False
+        self.timer = None  # kernel timer (eager mode only: events are not graph nodes here)
+
+    # ------------------------------------------------------------------ kernels
+    def _attn(self, l: int, x_in: torch.Tensor) -> torch.Tensor:
+        """q,k,v = LN(x) Wqkv (self.ln holds LN(x_in)); attention; x + att Wo."""
+        dw, s = self.dm.dw, self.spec
+        d, B = s.hidden_dim, self.B
+        wc = self.dm.moe.wcode
+        K.stream_gemv([K.sg_group(w_base=dw.qkv[l].data_ptr(), K=d, rows=3 * d, x=self.ln, dense_T=B,
+                                  out=self.qkv)], wc, B)
+        K.attn_decode(self.qkv, self.sess.kc[l], self.sess.vc[l], self.pos, s.n_heads, out=self.att)
+        K.stream_gemv([K.sg_group(w_base=dw.o[l].data_ptr(), K=d, rows=d, x=self.att, dense_T=B, out=self.xa,
+                                  residual=x_in)], wc, B)
+        return self.xa
+
+    def _route(self, l: int, kind: str) -> dict:
+        moe = self.dm.moe
+        replay = self.states["little"][l] if kind == "big" else None
+        mask = self.ones if kind == "big" else None
+        return moe.route(self.xa, l, self.k_tok[kind], self.k[kind], replay=replay, replay_mask=mask,
+                         reuse_gates=self.reuse_gates and kind == "big",
+                         logits_out=self.states[kind][l], idx_out=self.idx[kind][l])
+
+    def _experts(self, l: int, kind: str, sc: dict, loc) -> torch.Tensor:
+        return self.dm.moe.experts(self.xa, l, sc, self.k_tok[kind], self.k[kind], loc,
+                                   timer=None if self.use_graphs else self.timer, ln_out=self.ln)
+
+    def _head(self, x_last: torch.Tensor, kind: str):
+        s = self.spec
+        K.head_confidence(x_last, self.dm.dw.head, self._gamma, s.logit_scale, ws=self.head_ws, out=self.head[kind])
+
+    def _offload_loc(self, l: int, kind: str):
+        row = 1 if kind == "big" else 0
+        return self.rt._location(l, row), row
+
+    # ------------------------------------------------------------------ segments
+    def _seg(self, kind: str, l: int):
+        """Segment l of an offloaded pass: experts(l-1) [+ attn/route(l)]."""
+        L = self.spec.num_layers
+        if l == 0:
+            K.embed(self.tok, self.pos, self.dm.dw.embed, self.pe, self.x, ln_out=self.ln)
+            x_in = self.x
+        else:
+            loc, row = self._offload_loc(l - 1, kind)
+            K.memcpy_async(self.rt.slot_dev[row, l - 1], self.rt.slot_host[row, l - 1])
+            x_in = self._experts(l - 1, kind, self._sc[kind][l - 1], loc)
+        if l == L:
+            self._head(x_in, kind)
+            return
+        self._attn(l, x_in)
+        sc = self._route(l, kind)
+        self._sc[kind][l] = sc
+        if kind != "big":
+            K.memcpy_async(self.active_host[l], sc["perm"]["active"])
+
+    def _whole_pass(self, kind: str):
+        """A pass with HBM-resident experts (one graph)."""
+        K.embed(self.tok, self.pos, self.dm.dw.embed, self.pe, self.x, ln_out=self.ln)
+        x_in = self.x
+        for l in range(self.spec.num_layers):
+            self._attn(l, x_in)
+            sc = self._route(l, kind)
+            x_in = self._experts(l, kind, sc, None)
+        self._head(x_in, kind)
+
+    def _capture(self, key, fn):
+        if not self.use_graphs:
+            return fn
+        g = torch.cuda.CUDAGraph()
+        # warm up once eagerly (sets kernel attributes, allocates scratch)
+        with torch.cuda.stream(self.stream):
+            fn()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=self.stream):
+            fn()
+        self.graphs[key] = g
+        return g.replay
+
+    def build(self, gamma: float = 0.7, reuse_gates: bool = False):
+        """Capture the graphs for every pass kind (gamma / reuse are baked in)."""
+        self._gamma, self.reuse_gates = gamma, reuse_gates
+        L = self.spec.num_layers
+        self._sc = {kd: [None] * L for kd in KINDS}
+        self.run = {}
+        if self.rt is None:
+            for kd in KINDS:
+                self.run[kd] = self._capture(kd, lambda kd=kd: self._whole_pass(kd))
+        else:
+            # offload: warm-up needs valid slot tables; point every table at slot 0
+            self.rt.slot_dev.zero_()
+            self.rt.slot_host.zero_()
+            for kd in KINDS:
+                self.run[kd] = [self._capture((kd, l), lambda kd=kd, l=l: self._seg(kd, l)) for l in range(L + 1)]
+        torch.cuda.synchronize()
+        return self
+
+    # ------------------------------------------------------------------ passes
+    def _launch(self, fn):
+        with torch.cuda.stream(self.stream):
+            fn()
+
+    def pass_resident(self, kind: str):
+        self._launch(self.run[kind])
+
+    def pass_offload(self, kind: str):
+        """Drive the L+1 segments with the engine.py:121-169 protocol."""
+        rt, L = self.rt, self.spec.num_layers
+        segs = self.run[kind]
+        row = 1 if kind == "big" else 0
+        st = C.c_int()
+        if kind == "big":
+            with torch.cuda.stream(self.stream):
+                idx, _ = K.topk_rows(self.states["little"][:, 0].contiguous(), self.spec.k_big)
+                targets = idx.cpu().tolist()  # one D2H for the whole planned pass
+            waiting = list(plan_from_targets(targets, rt.lookahead).entries)
+        prev = None
+        for l in range(L):
+            if kind == "big":  # (1) issue window at the layer boundary (engine.py:98-119)
+                kept = []
+                for i, e in enumerate(waiting):
+                    if e.earliest_issue_layer > l:
+                        kept.extend(waiting[i:])
+                        break
+                    if e.expert.layer < l:
+                        continue
+                    rc = N.lib.mobile_offload_prefetch(rt.h, e.expert.layer, e.expert.expert, C.byref(st))
+                    if rc == N.ERR_DEFERRED:
+                        kept.append(e)
+                    else:
+                        N.check(rc, "offload prefetch")
+                waiting = kept
+            self._launch(segs[l])  # experts(l-1), (2) attention(l), routing(l)
+            if prev is not None:
+                self._release(l - 1, prev)
+            if kind == "big":
+                experts = targets[l]
+            else:  # on demand: the layer's selection comes back to the host
+                self.stream.synchronize()
+                N.lib.mobile_offload_sync(rt.h)
+                a = self.active_host[l]
+                experts = a[1:1 + int(a[0])].tolist()
+            # (3) request + pin, issue misses, (4) compute stream waits on their copies
+            self._require(l, experts, row)
+            prev = experts
+        self._launch(segs[L])  # (5) experts(L-1) + head
+        self._release(L - 1, prev)
+
+    def _require(self, l, experts, row):
+        rt = self.rt
+        arr = (C.c_int * len(experts))(*experts)
+        issued = C.c_int()
+        N.check(N.lib.mobile_offload_require(rt.h, l, arr, len(experts), self.stream.cuda_stream,
+                                             rt.slot_host[row, l].data_ptr(), C.byref(issued)), "offload require")
+        rt.fresh += issued.value
+
+    def _release(self, l, experts):  # (6) unpin + last-use events (engine.py:152-153)
+        arr = (C.c_int * len(experts))(*experts)
+        N.check(N.lib.mobile_offload_release(self.rt.h, l, arr, len(experts), self.stream.cuda_stream),
+                "offload release")
+
+    def run_pass(self, kind: str):
+        if self.rt is None:
+            self.pass_resident(kind)
+        else:
+            self.pass_offload(kind)
+
+    # ------------------------------------------------------------------ decode API
+    def prefill(self, prompt: list[int], prefill_k: int | None = None):
+        """Context positions [0, n-1) through the torch-free-of-graphs session
+        path (T = n-1 tokens), then the last prompt token becomes the first
+        step's input."""
+        if self.B != 1:
+            raise ValueError("prefill: batch-1 engine")
+        s = self.spec
+        kpf = s.k_big if prefill_k is None else prefill_k
+        ctx = list(prompt[:-1])
+        self.sess.pos = 0
+        if ctx:
+            t = torch.tensor([ctx], dtype=torch.long, device=self.dm.device)
+            k = torch.full((len(ctx),), kpf, dtype=torch.int32, device=self.dm.device)
+            hook = self.rt.demand_hook("prefill") if self.rt else None
+            with torch.cuda.stream(self.stream):
+                self.sess.run(t, k, kpf, expert_hook=hook)
+            if self.rt:
+                self.stream.synchronize()
+                self.rt.token_end()
+        self.pos.fill_(len(ctx))
+        self.tok.fill_(prompt[-1])
+        torch.cuda.synchronize()
+
+    def step(self, forced_fallback: bool | None = None, full: bool = False, next_token: int | None = None):
+        """One decoded token (batch 1).  Returns (token, fell_back)."""
+        rt = self.rt
+        if full:
+            self.run_pass("full")
+            h = self.head["full"]
+            fb = False
+        else:
+            self.run_pass("little")
+            h = self.head["little"]
+            if forced_fallback is None:
+                with torch.cuda.stream(self.stream):
+                    fb = bool(h["fallback"].item())
+            else:
+                self.stream.synchronize()
+                fb = bool(forced_fallback)
+            if rt:
+                N.lib.mobile_offload_sync(rt.h)
+            if fb:
+                self.run_pass("big")
+                h = self.head["big"]
+        with torch.cuda.stream(self.stream):
+            if next_token is None:  # greedy feedback on the device
+                K.advance(self.pos, self.tok, h["argmax"])
+            else:  # teacher-forced input stream (synthetic token ids from the host)
+                K.advance(self.pos)
+                self.tok_host[0] = next_token
+                K.memcpy_async(self.tok, self.tok_host)
+            token = int(h["argmax"].item())
+        if rt:
+            rt.token_end()
+        return token, fb
+
+    def decode(self, prompt: list[int], n_tokens: int, fallback_flags=None, inputs: list[int] | None = None,
+               prefill_k: int | None = None, full: bool = False):
+        """Public decode call: prefill `prompt`, then `n_tokens` MoBiLE steps.
+        `inputs` (optional) teacher-forces the next input ids (synthetic
+        streams); otherwise greedy feedback.  Returns (tokens, fallbacks)."""
+        self.prefill(prompt, prefill_k)
+        out, fbs = [], 0
+        for i in range(n_tokens):
+            forced = None if fallback_flags is None else bool(fallback_flags[i])
+            nxt = None if inputs is None else int(inputs[i])
+            tok, fb = self.step(forced, full=full, next_token=nxt)
+            out.append(tok)
+            fbs += fb
+        return out, fbs

@@ -15,7 +15,8 @@ input dim, so every GEMV row is one contiguous stream):
            W13 = (2I, d) SwiGLU gate/up rows interleaved in groups of 8+8
                  (or (I, d) = W_in^T for ReLU), W2 = (d, I) = W_out^T
   shared   (L, S, Ps)           same packing with the shared ffn dim
-  attn     q/k/v/o (L, d, d)    (in, out) as in the reference (`h @ W`)
+  qkv      (L, 3d, d)           [Wq^T; Wk^T; Wv^T] (one GEMV per layer)
+  o        (L, d, d)            Wo^T
   head     (V, d)               = head^T
   embed    (V, d) f32
 """
@@ -78,7 +79,7 @@ def init_host_weights(spec: ModelSpec) -> HostWeights:
     def draw(*shape, fan_in=d):
         return rng.uniform(-1.0, 1.0, size=shape) * (1.0 / np.sqrt(fan_in))
 
-    embed = draw(V, d)
+    embed = draw(V, d, fan_in=1.0 / spec.embed_scale**2 if spec.embed_scale else d)
     q, k, v, o = (draw(L, d, d) for _ in range(4))
     router = draw(L, d, E)
     w_in = draw(L, E, d, I)
@@ -127,7 +128,7 @@ class DeviceWeights:
         self.s_w13_elems, self.shared_elems = expert_elems(d, spec.shared_ffn, spec.activation)
         self.elem_bytes = 2 if self.wdtype == torch.bfloat16 else 4
         self.n_gate_rows = spec.n_shared if spec.shared_gate == "sigmoid" else 0
-        self.embed = self.q = self.k = self.v = self.o = None
+        self.embed = self.qkv = self.o = None
         self.router = self.experts = self.shared = self.head = None
         self.host_experts = None  # pinned host store when experts are offloaded
 
@@ -149,7 +150,9 @@ class DeviceWeights:
             return torch.from_numpy(np.ascontiguousarray(a)).to(device=dev, dtype=dtype)
 
         dw.embed = T(hw.embed, torch.float32)
-        dw.q, dw.k, dw.v, dw.o = T(hw.attn_q), T(hw.attn_k), T(hw.attn_v), T(hw.attn_o)
+        tr = lambda a: np.transpose(a, (0, 2, 1))  # noqa: E731  (L, in, out) -> (L, out, in)
+        dw.qkv = T(np.concatenate([tr(hw.attn_q), tr(hw.attn_k), tr(hw.attn_v)], axis=1))
+        dw.o = T(tr(hw.attn_o))
         rt = np.transpose(hw.router, (0, 2, 1))  # (L, E, d)
         if dw.n_gate_rows:
             rt = np.concatenate([rt, np.transpose(hw.shared_gate_w, (0, 2, 1))], axis=1)
@@ -181,8 +184,9 @@ class DeviceWeights:
             t.uniform_(-1.0, 1.0, generator=g).mul_(1.0 / np.sqrt(fan_in))
             return t.to(dtype)
 
-        dw.embed = U(V, d, dtype=torch.float32)
-        dw.q, dw.k, dw.v, dw.o = (U(L, d, d) for _ in range(4))
+        dw.embed = U(V, d, fan_in=1.0 / spec.embed_scale**2 if spec.embed_scale else d, dtype=torch.float32)
+        dw.qkv = U(L, 3 * d, d)
+        dw.o = U(L, d, d)
         dw.router = U(L, E + dw.n_gate_rows, d)
         dw.head = U(V, d)
         # packed experts: W13 rows have fan_in d, W2 rows fan_in I
@@ -215,7 +219,7 @@ class DeviceWeights:
 
     def device_bytes(self) -> int:
         n = 0
-        for t in (self.embed, self.q, self.k, self.v, self.o, self.router, self.experts, self.shared, self.head):
+        for t in (self.embed, self.qkv, self.o, self.router, self.experts, self.shared, self.head):
             if t is not None:
                 n += t.numel() * t.element_size()
         return n

@@ -51,3 +51,25 @@ DSEEK_MINI = dict(num_layers=2, num_experts=16, k_big=6, k_little=3, hidden_dim=
                   ffn_dim=64, activation="swiglu", n_shared=2, shared_ffn_dim=64, n_heads=2)
 OLMOE_MINI = dict(num_layers=2, num_experts=16, k_big=8, hidden_dim=256, vocab_size=400, seed=8, ffn_dim=128,
                   activation="swiglu", gate_norm="softmax_all", n_heads=4)
+
+
+def selections_agree(got, want, logits, tol=2e-5):
+    """Layer selections equal, except where the oracle's own logits make the
+    order a near-tie (|gap| < tol * max|logit|): then only membership/order
+    among near-equal logits may differ.  Returns (ok, n_near_ties)."""
+    near = 0
+    for l, (g, w) in enumerate(zip(got, want)):
+        if list(g) == list(w):
+            continue
+        row = np.asarray(logits[l], dtype=np.float64)
+        scale = max(np.max(np.abs(row)), 1e-30)
+        srt = np.sort(row)[::-1]
+        k = len(w)
+        # every differing position must be a near tie in the oracle's ranking
+        for a, b in zip(g, w):
+            if a != b and abs(row[a] - row[b]) > tol * scale:
+                return False, near
+        if set(g) != set(w) and (k >= len(srt) or srt[k - 1] - srt[k] > tol * scale):
+            return False, near
+        near += 1
+    return True, near

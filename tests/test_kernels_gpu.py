@@ -149,8 +149,12 @@ def test_permute_stable(dev, T, k, E):
     (dict(num_layers=1, num_experts=16, k_big=4, hidden_dim=256, vocab_size=256, seed=0), "float32"),
     (QWEN_MINI, "bfloat16"), (DSEEK_MINI, "bfloat16"), (OLMOE_MINI, "bfloat16"), (QWEN_MINI, "float32")])
 @pytest.mark.parametrize("T", [1, 2, 5, 33])
-def test_moe_layer_vs_oracle(dev, spec_kw, dtype, T):
-    """The whole MoE block (router..combine) at per-token widths with replay."""
+@pytest.mark.parametrize("impl", ["stream", "warp"])
+def test_moe_layer_vs_oracle(dev, spec_kw, dtype, T, impl, monkeypatch):
+    """The whole MoE block (router..combine) at per-token widths with replay,
+    through both expert-FFN kernels (bulk-copy streaming and warp streaming)."""
+    from paper_2510_12357_b200 import model as M
+    monkeypatch.setattr(M, "FFN_IMPL", impl)
     o, ms, dm = matched(spec_kw, dtype)
     rng = np.random.default_rng(T)
     d, E = ms.hidden_dim, ms.num_experts
@@ -219,3 +223,46 @@ def test_qwen_full_size_layer(dev):
         ref = R.moe_block(o, 0, h2, k_tok)
         assert sc["router"]["idx"].cpu().tolist() == [s for s in ref.selections]
         assert rel_err(xo.cpu().numpy() - x.astype(np.float32), ref.out) < 1e-4
+
+
+@pytest.mark.parametrize("wdt", ["float32", "bfloat16"])
+@pytest.mark.parametrize("T", [1, 2, 3, 4, 7])
+@pytest.mark.parametrize("K_,N_", [(128, 48), (2048, 64), (4096, 32), (1408, 2048), (5632, 16), (256, 7)])
+def test_stream_gemv_dense(dev, wdt, T, K_, N_):
+    """Dense STORE groups (+ residual): multi-chunk K, ragged rows, 1..7 tokens."""
+    from paper_2510_12357_b200 import kernels as K
+    rng = np.random.default_rng(K_ + N_ + T)
+    w = rng.uniform(-1, 1, size=(N_, K_)) / np.sqrt(K_)
+    if wdt == "bfloat16":
+        w = round_bf16(w)
+    x = rng.normal(size=(T, K_)).astype(np.float32)
+    res = rng.normal(size=(T, N_)).astype(np.float32)
+    tdt = torch.bfloat16 if wdt == "bfloat16" else torch.float32
+    wt = torch.tensor(w, device=dev, dtype=tdt)
+    out = torch.empty(T, N_, device=dev)
+    xt, rt = torch.tensor(x, device=dev), torch.tensor(res, device=dev)
+    K.stream_gemv([K.sg_group(w_base=wt.data_ptr(), K=K_, rows=N_, x=xt, dense_T=T, out=out, residual=rt)],
+                  K.dtype_code(wt), T)
+    want = res + x.astype(np.float64) @ w.T
+    assert rel_err(out.cpu().numpy(), want) < 2e-5
+
+
+@pytest.mark.parametrize("T,k", [(1, 2), (1, 4), (1, 8), (2, 6), (3, 4), (4, 8), (5, 4), (9, 2)])
+def test_router_fused_permute(dev, T, k):
+    """Router with fused permute (decode sizes) == router + separate permute kernel."""
+    from paper_2510_12357_b200 import kernels as K
+    rng = np.random.default_rng(T * 10 + k)
+    d, E = 256, 64
+    w = torch.tensor(rng.uniform(-1, 1, size=(E, d)) / 16, dtype=torch.bfloat16, device=dev)
+    x = torch.tensor(rng.normal(size=(T, d)), dtype=torch.float32, device=dev)
+    k_tok = torch.tensor(rng.integers(1, k + 1, size=T), dtype=torch.int32, device=dev)
+    perm = dict(offsets=torch.full((E + 1,), -7, dtype=torch.int32, device=dev),
+                sorted_pairs=torch.full((T * k,), -7, dtype=torch.int32, device=dev),
+                active=torch.full((E + 1,), -7, dtype=torch.int32, device=dev))
+    r = K.router_topk(x, w, E, k, k_tok, perm=perm)
+    ref = K.permute(r["idx"], k_tok, E)
+    n = int(ref["offsets"][E])
+    assert perm["offsets"].tolist() == ref["offsets"].tolist()
+    assert perm["sorted_pairs"][:n].tolist() == ref["sorted_pairs"][:n].tolist()
+    na = int(ref["active"][0])
+    assert perm["active"][:1 + na].tolist() == ref["active"][:1 + na].tolist()
