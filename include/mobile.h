@@ -149,6 +149,9 @@ int mobile_expert_down(const float* U, const int* offsets, const int* sorted_pai
 /* ---- bulk-copy streaming GEMV (decode engine) -----------------------------
  * One launch computes several groups of weight-row dot products, streaming
  * weights through shared memory with cp.async.bulk on an mbarrier ring.
+ * Weights must be in the TILED layout: tiles of 16 rows x 4 KB of K
+ * (2048 bf16 / 1024 f32 elements), contiguous in (row block, K chunk) order;
+ * for K <= the chunk this is plain row-major (see weights.py tile_rows).
  * Group semantics (per pair p of expert e, see mobile_expert_gate_up):
  *   epi 0 STORE : out[p, r] = (residual[p, r] +) x[p / x_div] . W_e[r]
  *   epi 1 RELU  : out[p, r] = max(x[p / x_div] . W_e[r], 0)
@@ -177,6 +180,15 @@ typedef struct {
 } mobile_sg_group;
 int mobile_stream_gemv(const mobile_sg_group* groups, int n_groups, int w_dtype, int max_tokens,
                        void* stream);
+/* Output head + confidence on the same engine (toymoe.py:209-210, 273;
+ * policy.py:69-79): logits = x_ln[t] . head_row * scale (x_ln already
+ * layer-normalised), conf[t] = max softmax, first argmax, fallback =
+ * conf <= gamma.  T <= 4.  workspace >= mobile_stream_head_ws_bytes(), zeroed
+ * once (the kernel leaves it zeroed). */
+size_t mobile_stream_head_ws_bytes(void);
+int mobile_stream_head(const float* x_ln, int T, int d, const void* w_head, int w_dtype, int V,
+                       float logit_scale, float gamma, float* logits_out, float* conf_out, int* argmax_out,
+                       uint8_t* fallback_out, void* workspace, void* stream);
 
 /* ---- combine -------------------------------------------------------------
  * toymoe.py:192, 204, 207:  moe = sum_j gates[t,j] * Y[t*k_max + j] (selection

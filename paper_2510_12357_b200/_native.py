@@ -69,6 +69,8 @@ _SIGS = {
     "mobile_expert_down": ([P, P, P, P, I32, I32, I32, I32, P, I64, P, I32, P, P], I32),
     "mobile_combine": ([P, P, P, P, I32, I32, I32, P, I32, P, P, P, P], I32),
     "mobile_stream_gemv": ([P, I32, I32, I32, P], I32),
+    "mobile_stream_head_ws_bytes": ([], SZ),
+    "mobile_stream_head": ([P, I32, I32, P, I32, I32, F, F, P, P, P, P, P, P], I32),
     "mobile_dense_gemv": ([P, I32, I32, I32, P, I32, I32, P, P, P], I32),
     "mobile_attn_decode": ([P, P, P, P, I32, I32, I32, I32, P, P], I32),
     "mobile_embed": ([P, P, P, P, I32, I32, P, P, P], I32),

@@ -1,74 +1,90 @@
 // Bulk-copy (TMA) weight-streaming GEMV engine for batch-1..4 decode.
 //
 // Every decode-time matrix product on the MoBiLE path is HBM-bound: each
-// weight byte is used by 1-4 tokens.  This kernel streams weight tiles into
-// shared memory with cp.async.bulk (the Blackwell bulk-copy/TMA engine; SASS
-// UBLKCP) on a full/empty mbarrier ring of 6 x 32 KB stages per CTA, one CTA
-// per SM, so ~192 KB per SM is in flight with no register cost.  Warp 8 is the
-// producer (one lane issues the copies); warps 0-7 consume: warp w owns rows
-// {w, w+8} of every 16-row unit, so each output is one warp's dot product and
-// the epilogue needs no block barrier (SwiGLU pairs gate row w with up row
-// w+8 in the same warp).
+// weight byte is used by 1-4 tokens.  This kernel streams weights into shared
+// memory with cp.async.bulk (the Blackwell bulk-copy engine; SASS UBLKCP) on a
+// full/empty mbarrier ring of 3 x 64 KB stages per CTA, one CTA per SM, so
+// ~192 KB per SM is in flight with no register cost.
 //
-// Work is a list of UNITS = (group, active expert, block of R output rows).
-// A launch can carry several groups (e.g. routed + shared experts), so one
-// launch covers a layer's whole gate-up (or down) and the unit count is large
-// enough to balance 148 SMs.  Weight rows of a unit are streamed in K chunks
-// of 2 KB (R bulk copies per chunk, one per row), accumulators
-// live across chunks, and the epilogue runs on the unit's last chunk:
+// Weights are stored TILED (see weights.py): a matrix of `rows` x K is cut
+// into tiles of 16 rows x 4 KB of K (2048 bf16 / 1024 f32) laid out
+// contiguously in (row block, K chunk) order -- for K <= the chunk this is
+// plain row-major.  One tile = one 64 KB bulk copy = one pipeline item, so the
+// copy engine sees a few large requests instead of many row-sized ones.
+//
+// Warp 8 is the producer (one lane issues copies); warps 0-7 consume: warp w
+// owns rows {w, w+8} of every 16-row tile, so each output is one warp's
+// fixed-order dot product and every epilogue is warp-local:
 //   STORE  : y = acc (+ residual)
-//   RELU   : y = max(acc, 0)                       (toy expert, toymoe.py:203)
-//   SWIGLU : 16-row groups [8 gate | 8 up] -> silu(g) * u for 8 features
-// Reductions are fixed-order (butterfly within warps, then warp order), so the
-// results are deterministic.
+//   RELU   : y = max(acc, 0)                      (toy expert, toymoe.py:203)
+//   SWIGLU : tile rows [8 gate | 8 up] -> silu(g_w) * u_w   (extension)
+//   HEAD   : logits = acc * scale; online (max, sum-exp, first argmax) per
+//            token; CTA partials merged by the last CTA (atomic ticket) into
+//            conf = 1 / sum, argmax, fallback = conf <= gamma
+//            (toymoe.py:209-210, 273; policy.py:69-79)
+// Work is a list of UNITS = (group, active expert, 16-row block); a launch can
+// carry several groups (routed + shared experts) so one launch covers a
+// layer's whole gate-up (or down) and balances 148 SMs.
 #include "common.cuh"
 
 namespace mobile {
 
 constexpr int kSgConsumerWarps = 8;
 constexpr int kSgThreads = (kSgConsumerWarps + 1) * 32;  // + 1 producer warp
-constexpr int kSgStages = 6;
-constexpr int kSgStageBytes = 32 * 1024;
-constexpr int kSgRowChunkBytes = 2048;  // bytes of one weight row per K chunk
+constexpr int kSgStages = 3;
+constexpr int kSgStageBytes = 64 * 1024;
+constexpr int kSgTileRows = 16;
+constexpr int kSgTileRowBytes = 4096;  // K chunk per tile row
 constexpr int kSgMaxGroups = 4;
+constexpr int kSgMaxTok = 4;
 
-enum SgEpi { kEpiStore = 0, kEpiRelu = 1, kEpiSwiglu = 2 };
+enum SgEpi { kEpiStore = 0, kEpiRelu = 1, kEpiSwiglu = 2, kEpiHead = 3 };
 
 struct SgGroup {
-  const char* w_base;       // weights of expert e at w_base + slot[e] * stride (bytes)
+  const char* w_base;       // tiled weights of expert e at w_base + slot[e] * stride (bytes)
   long long stride;
   const int* slot;          // NULL = identity
   const float* x;           // activation rows (K floats each)
   int x_div;                // activation row = pair / x_div
-  const int* offsets;       // (E+1) or NULL (dense: one expert, pairs 0..T-1)
+  const int* offsets;       // (E+1); NULL = dense (one expert, pairs 0..T-1)
   const int* pairs;
-  const int* active;        // [n, ids...] or NULL (dense)
+  const int* active;        // [n, ids...]
   int dense_T;
   int max_active;
-  int K;                    // input dim (weight row length)
-  int rows;                 // weight rows per expert
-  int R;                    // rows per unit
-  int out_dim;              // output features per pair
+  int K;
+  int rows;
+  int out_dim;
   float* out;
-  const float* residual;    // STORE only, same indexing as out
+  const float* residual;
   int epi;
-  int units;                // max_active * (rows / R)
+  int units;                // max_active * ceil(rows / 16)
+};
+
+struct SgHead {             // HEAD epilogue state (one dense group)
+  float scale, gamma;
+  float* conf;
+  int* argmax;
+  uint8_t* fallback;
+  float* partials;          // gridDim.x * kSgMaxTok * 3
+  unsigned* ticket;         // left at 0
 };
 
 struct SgArgs {
   SgGroup g[kSgMaxGroups];
+  SgHead head;
   int n_groups;
   int total_units;
 };
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -89,12 +105,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // Iterator over this CTA's (unit, token-chunk, k-chunk) items.
-template <int TT>
 struct SgIter {
-  int unit;      // global unit index (strided by gridDim.x)
-  int g, a, rb;  // decoded unit
-  int e, p0, n;  // expert, first pair index, #pairs of the expert
-  int tc, kc;    // token chunk, k chunk
+  int unit;
+  int g, a, rb, rr;  // group, active slot, row block, rows in block
+  int e, p0, n;      // expert, first pair index, #pairs
+  int tc, kc;
   bool valid;
 
   __device__ bool decode(const SgArgs& A) {
@@ -105,10 +120,11 @@ struct SgIter {
     }
     if (g >= A.n_groups) return false;
     const SgGroup& G = A.g[g];
-    const int upe = G.rows / G.R;
+    const int upe = (G.rows + kSgTileRows - 1) / kSgTileRows;
     a = u / upe;
     rb = u - a * upe;
-    if (G.active) {
+    rr = min(kSgTileRows, G.rows - rb * kSgTileRows);
+    if (G.offsets) {
       if (a >= G.active[0]) return false;
       e = G.active[1 + a];
       p0 = G.offsets[e];
@@ -120,7 +136,7 @@ struct SgIter {
     }
     return n > 0;
   }
-  __device__ void seek(const SgArgs& A) {  // advance to the first valid unit >= unit
+  __device__ void seek(const SgArgs& A) {
     while (unit < A.total_units && !decode(A)) unit += gridDim.x;
     valid = unit < A.total_units;
     tc = kc = 0;
@@ -129,34 +145,42 @@ struct SgIter {
     unit = blockIdx.x;
     seek(A);
   }
-  __device__ void next(const SgArgs& A, int kc_elems) {
+  __device__ void next(const SgArgs& A, int kc_elems, int tt) {
     const SgGroup& G = A.g[g];
-    const int nk = (G.K + kc_elems - 1) / kc_elems;
-    if (++kc < nk) return;
+    if (++kc * kc_elems < G.K) return;
     kc = 0;
-    if (++tc * TT < n) return;
+    if (++tc * tt < n) return;
     unit += gridDim.x;
     seek(A);
   }
 };
 
-// Issue the bulk copies of one item into a stage.
-template <typename W, int TT>
-__device__ void sg_issue(const SgArgs& A, const SgIter<TT>& it, char* stage, uint64_t* bar) {
+template <typename W>
+__device__ void sg_issue(const SgArgs& A, const SgIter& it, char* stage, uint64_t* bar) {
+  constexpr int KC = kSgTileRowBytes / sizeof(W);
   const SgGroup& G = A.g[it.g];
   const int s = G.slot ? G.slot[it.e] : it.e;
-  const char* base = G.w_base + (long long)s * G.stride + (size_t)it.rb * G.R * G.K * sizeof(W);
-  constexpr int KC = kSgRowChunkBytes / sizeof(W);
   const int k0 = it.kc * KC;
   const int kn = min(KC, G.K - k0);
-  const uint32_t row_bytes = (uint32_t)(kn * sizeof(W));
-  mbar_expect_tx(bar, row_bytes * G.R);
-  for (int r = 0; r < G.R; ++r)
-    bulk_g2s(stage + (size_t)r * row_bytes, base + ((size_t)r * G.K + k0) * sizeof(W), row_bytes, bar);
+  const size_t off = (size_t)it.rb * kSgTileRows * G.K + (size_t)k0 * it.rr;  // tiled layout
+  const uint32_t bytes = (uint32_t)(it.rr * kn * sizeof(W));
+  mbar_expect_tx(bar, bytes);
+  bulk_g2s(stage, G.w_base + (long long)s * G.stride + off * sizeof(W), bytes, bar);
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void online_add(float& m, float& s, int& arg, float l, int idx) {
+  if (l > m) {
+    s = s * expf(m - l) + 1.0f;
+    m = l;
+    arg = idx;
+  } else {
+    s += expf(l - m);
+  }
+}
+__device__ __forceinline__ void online_merge2(float& M, float& S, int& A_, float m, float s, int a) {
+  if (s == 0.f) return;
+  if (m > M) { S = S * expf(M - m) + s; M = m; A_ = a; }
+  else { S += s * expf(m - M); if (m == M && a < A_) A_ = a; }
 }
 
 template <typename W, int TT>
@@ -164,9 +188,11 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) uint64_t full[kSgStages];
   __shared__ __align__(8) uint64_t empty[kSgStages];
+  __shared__ float hred[kSgConsumerWarps][kSgMaxTok][3];
+  __shared__ bool is_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int V = WVec<W>::N;
-  constexpr int KC = kSgRowChunkBytes / sizeof(W);
+  constexpr int KC = kSgTileRowBytes / sizeof(W);
 
   if (tid == 0) {
     for (int s = 0; s < kSgStages; ++s) {
@@ -180,7 +206,7 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
   if (warp == kSgConsumerWarps) {
     // ---------------- producer: one lane streams every item of this CTA
     if (lane == 0) {
-      SgIter<TT> prod;
+      SgIter prod;
       prod.start(A);
       int stage = 0;
       uint32_t empty_phase = 0;
@@ -190,16 +216,16 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
           empty_phase ^= 1u << stage;
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
-        sg_issue<W, TT>(A, prod, smem + (size_t)stage * kSgStageBytes, &full[stage]);
-        prod.next(A, KC);
+        sg_issue<W>(A, prod, smem + (size_t)stage * kSgStageBytes, &full[stage]);
+        prod.next(A, KC, TT);
         stage = stage + 1 == kSgStages ? 0 : stage + 1;
       }
     }
     return;
   }
 
-  // ---------------- consumers: warp w owns rows {w, w + 8} of each unit
-  SgIter<TT> cons;
+  // ---------------- consumers: warp w owns rows {w, w + 8} of each tile
+  SgIter cons;
   cons.start(A);
   uint32_t full_phase = 0;
   int stage = 0;
@@ -208,18 +234,21 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int t = 0; t < TT; ++t) acc[i][t] = 0.f;
+  float hm[TT], hs[TT];
+  int ha[TT];
+#pragma unroll
+  for (int t = 0; t < TT; ++t) { hm[t] = -INFINITY; hs[t] = 0.f; ha[t] = 0x7fffffff; }
 
   while (cons.valid) {
     const SgGroup& G = A.g[cons.g];
-    const int R = G.R;
     const int k0 = cons.kc * KC;
     const int kn = min(KC, G.K - k0);
     const int nt = min(TT, cons.n - cons.tc * TT);
-    const bool has0 = warp < R, has1 = warp + 8 < R;
+    const bool has0 = warp < cons.rr, has1 = warp + 8 < cons.rr;
     int pair[TT];
 #pragma unroll
     for (int t = 0; t < TT; ++t)
-      pair[t] = t < nt ? (G.active ? G.pairs[cons.p0 + cons.tc * TT + t] : cons.tc * TT + t) : 0;
+      pair[t] = t < nt ? (G.offsets ? G.pairs[cons.p0 + cons.tc * TT + t] : cons.tc * TT + t) : 0;
     mbar_wait(&full[stage], (full_phase >> stage) & 1u);
     full_phase ^= 1u << stage;
     if (has0) {
@@ -265,22 +294,33 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
     stage = stage + 1 == kSgStages ? 0 : stage + 1;
 
     if ((cons.kc + 1) * KC >= G.K) {
-      // ---------------- warp-local epilogue for (unit, token chunk)
+      // ---------------- warp-local epilogue for (tile, token chunk)
       if (has0) {
+        const int r0 = cons.rb * kSgTileRows + warp;  // output row of acc[0]
 #pragma unroll
         for (int t = 0; t < TT; ++t) {
           const float s0 = warp_sum(acc[0][t]);
           const float s1 = has1 ? warp_sum(acc[1][t]) : 0.f;
-          if (lane == 0 && t < nt) {
-            if (G.epi == kEpiSwiglu) {  // row w = gate f, row w+8 = up f
-              G.out[(size_t)pair[t] * G.out_dim + cons.rb * 8 + warp] = silu_f(s0) * s1;
-            } else {
-              const size_t o0 = (size_t)pair[t] * G.out_dim + (size_t)cons.rb * R + warp;
-              float v0 = s0, v1 = s1;
-              if (G.epi == kEpiRelu) { v0 = fmaxf(v0, 0.f); v1 = fmaxf(v1, 0.f); }
-              else if (G.residual) { v0 += G.residual[o0]; if (has1) v1 += G.residual[o0 + 8]; }
-              G.out[o0] = v0;
-              if (has1) G.out[o0 + 8] = v1;
+          if (t < nt) {
+            if (G.epi == kEpiHead) {
+              const float l0 = s0 * A.head.scale, l1 = s1 * A.head.scale;
+              if (lane == 0 && G.out) {
+                G.out[(size_t)pair[t] * G.out_dim + r0] = l0;
+                if (has1) G.out[(size_t)pair[t] * G.out_dim + r0 + 8] = l1;
+              }
+              online_add(hm[t], hs[t], ha[t], l0, r0);
+              if (has1) online_add(hm[t], hs[t], ha[t], l1, r0 + 8);
+            } else if (lane == 0) {
+              if (G.epi == kEpiSwiglu) {  // row w = gate f, row w + 8 = up f
+                G.out[(size_t)pair[t] * G.out_dim + cons.rb * 8 + warp] = silu_f(s0) * s1;
+              } else {
+                const size_t o0 = (size_t)pair[t] * G.out_dim + r0;
+                float v0 = s0, v1 = s1;
+                if (G.epi == kEpiRelu) { v0 = fmaxf(v0, 0.f); v1 = fmaxf(v1, 0.f); }
+                else if (G.residual) { v0 += G.residual[o0]; if (has1) v1 += G.residual[o0 + 8]; }
+                G.out[o0] = v0;
+                if (has1) G.out[o0 + 8] = v1;
+              }
             }
           }
         }
@@ -290,8 +330,48 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
 #pragma unroll
         for (int t = 0; t < TT; ++t) acc[i][t] = 0.f;
     }
-    cons.next(A, KC);
+    cons.next(A, KC, TT);
   }
+
+  if (A.head.conf == nullptr) return;
+  // ---------------- HEAD: merge warps (warp order), then CTAs (CTA order)
+  const int T = A.g[0].dense_T;
+  if (lane == 0)
+    for (int t = 0; t < TT; ++t) {
+      hred[warp][t][0] = hm[t];
+      hred[warp][t][1] = hs[t];
+      hred[warp][t][2] = __int_as_float(ha[t]);
+    }
+  asm volatile("bar.sync 1, %0;" ::"n"(kSgConsumerWarps * 32));
+  if (tid < T) {
+    float M = -INFINITY, S = 0.f;
+    int Ai = 0x7fffffff;
+    for (int w = 0; w < kSgConsumerWarps; ++w)
+      online_merge2(M, S, Ai, hred[w][tid][0], hred[w][tid][1], __float_as_int(hred[w][tid][2]));
+    float* p = A.head.partials + ((size_t)blockIdx.x * kSgMaxTok + tid) * 3;
+    p[0] = M;
+    p[1] = S;
+    p[2] = __int_as_float(Ai);
+  }
+  __threadfence();
+  asm volatile("bar.sync 1, %0;" ::"n"(kSgConsumerWarps * 32));
+  if (tid == 0) is_last = atomicAdd(A.head.ticket, 1u) == gridDim.x - 1;
+  asm volatile("bar.sync 1, %0;" ::"n"(kSgConsumerWarps * 32));
+  if (!is_last) return;
+  __threadfence();
+  if (tid < T) {
+    float M = -INFINITY, S = 0.f;
+    int Ai = 0x7fffffff;
+    for (unsigned b = 0; b < gridDim.x; ++b) {
+      const volatile float* p = A.head.partials + ((size_t)b * kSgMaxTok + tid) * 3;
+      online_merge2(M, S, Ai, p[0], p[1], __float_as_int(p[2]));
+    }
+    const float conf = 1.0f / S;
+    A.head.conf[tid] = conf;
+    if (A.head.argmax) A.head.argmax[tid] = Ai;
+    if (A.head.fallback) A.head.fallback[tid] = conf <= A.head.gamma ? 1 : 0;
+  }
+  if (tid == 0) *A.head.ticket = 0u;
 }
 
 template <typename W, int TT>
@@ -300,17 +380,17 @@ static int sg_launch(const SgArgs& A, cudaStream_t s) {
   const size_t smem = (size_t)kSgStages * kSgStageBytes;
   if (int st = set_smem_once((const void*)k, smem)) return st;
   int grid = sm_count();
-  if (A.total_units < grid) grid = A.total_units;
+  if (A.head.conf == nullptr && A.total_units < grid) grid = A.total_units;
   if (grid <= 0) return MOBILE_OK;
   k<<<grid, kSgThreads, smem, s>>>(A);
   MOBILE_CHECK_LAUNCH("stream_gemv");
   return MOBILE_OK;
 }
 
-int sg_dispatch(SgArgs& A, int w_dtype, int max_tok, cudaStream_t s) {
+static int sg_dispatch(SgArgs& A, int w_dtype, int max_tok, cudaStream_t s) {
   A.total_units = 0;
   for (int i = 0; i < A.n_groups; ++i) A.total_units += A.g[i].units;
-  if (A.total_units == 0) return MOBILE_OK;
+  if (A.total_units == 0 && A.head.conf == nullptr) return MOBILE_OK;
   const int TT = max_tok <= 1 ? 1 : max_tok <= 2 ? 2 : 4;
   if (w_dtype == MOBILE_BF16) {
     if (TT == 1) return sg_launch<__nv_bfloat16, 1>(A, s);
@@ -326,24 +406,19 @@ int sg_dispatch(SgArgs& A, int w_dtype, int max_tok, cudaStream_t s) {
   return MOBILE_ERR_UNSUPPORTED;
 }
 
-}  // namespace mobile
-
-using namespace mobile;
-
-// Rows per unit: 16 (SwiGLU needs the whole 8+8 group; 16 rows x 4 KB chunk =
-// one 64 KB stage), else the largest power of two <= 16 dividing `rows`.
-static int pick_R(int rows, int epi) {
-  if (epi == kEpiSwiglu) return rows % 16 == 0 ? 16 : -1;
-  int R = 16;
-  while (R > 1 && rows % R) R >>= 1;
-  return R;
-}
-
 static int fill_group(SgGroup& G, const mobile_sg_group* in, int w_dtype) {
   const int V = w_dtype == MOBILE_BF16 ? 8 : 4;
   if (in->K <= 0 || in->rows <= 0 || in->K % V) {
     set_error("stream_gemv: K=%d must be a positive multiple of %d", in->K, V);
     return MOBILE_ERR_UNSUPPORTED;
+  }
+  if (in->epi == kEpiSwiglu && in->rows % kSgTileRows) {
+    set_error("stream_gemv: SwiGLU rows=%d must be a multiple of 16", in->rows);
+    return MOBILE_ERR_UNSUPPORTED;
+  }
+  if (!in->offsets && (in->dense_T < 0 || in->dense_T > 64 * 1024)) {
+    set_error("stream_gemv: bad dense_T=%d", in->dense_T);
+    return MOBILE_ERR_INVALID;
   }
   G.w_base = (const char*)in->w_base;
   G.stride = in->stride;
@@ -354,28 +429,59 @@ static int fill_group(SgGroup& G, const mobile_sg_group* in, int w_dtype) {
   G.pairs = in->pairs;
   G.active = in->active;
   G.dense_T = in->dense_T;
-  G.max_active = in->active ? in->max_active : 1;
+  G.max_active = in->offsets ? in->max_active : 1;
   G.K = in->K;
   G.rows = in->rows;
   G.epi = in->epi;
-  G.R = pick_R(in->rows, in->epi);
-  if (G.R < 1 || in->rows % G.R) {
-    set_error("stream_gemv: rows=%d K=%d epi=%d cannot be tiled", in->rows, in->K, in->epi);
-    return MOBILE_ERR_UNSUPPORTED;
-  }
   G.out_dim = in->epi == kEpiSwiglu ? in->rows / 2 : in->rows;
   G.out = in->out;
   G.residual = in->residual;
-  G.units = G.max_active * (in->rows / G.R);
+  G.units = G.max_active * ((in->rows + kSgTileRows - 1) / kSgTileRows);
   return MOBILE_OK;
 }
+
+}  // namespace mobile
+
+using namespace mobile;
 
 extern "C" int mobile_stream_gemv(const mobile_sg_group* groups, int n_groups, int w_dtype, int max_tokens,
                                   void* stream) {
   if (n_groups < 1 || n_groups > kSgMaxGroups) { set_error("stream_gemv: 1..%d groups", kSgMaxGroups); return MOBILE_ERR_INVALID; }
   SgArgs A{};
   A.n_groups = n_groups;
-  for (int i = 0; i < n_groups; ++i)
+  for (int i = 0; i < n_groups; ++i) {
+    if (groups[i].epi == kEpiHead) { set_error("stream_gemv: use mobile_stream_head for the head"); return MOBILE_ERR_INVALID; }
     if (int st = fill_group(A.g[i], &groups[i], w_dtype)) return st;
+  }
   return sg_dispatch(A, w_dtype, max_tokens, (cudaStream_t)stream);
+}
+
+extern "C" size_t mobile_stream_head_ws_bytes(void) {
+  return 256 + sizeof(float) * 3 * kSgMaxTok * (size_t)sm_count();
+}
+
+extern "C" int mobile_stream_head(const float* x_ln, int T, int d, const void* w_head, int w_dtype, int V,
+                                  float logit_scale, float gamma, float* logits_out, float* conf_out,
+                                  int* argmax_out, uint8_t* fallback_out, void* workspace, void* stream) {
+  if (T < 1 || T > kSgMaxTok || d <= 0 || V <= 0) { set_error("stream_head: bad shape T=%d (1..4)", T); return MOBILE_ERR_INVALID; }
+  SgArgs A{};
+  A.n_groups = 1;
+  mobile_sg_group in{};
+  in.w_base = w_head;
+  in.x = x_ln;
+  in.x_div = 1;
+  in.dense_T = T;
+  in.K = d;
+  in.rows = V;
+  in.out = logits_out;
+  in.epi = kEpiHead;
+  if (int st = fill_group(A.g[0], &in, w_dtype)) return st;
+  A.head.scale = logit_scale;
+  A.head.gamma = gamma;
+  A.head.conf = conf_out;
+  A.head.argmax = argmax_out;
+  A.head.fallback = fallback_out;
+  A.head.ticket = reinterpret_cast<unsigned*>(workspace);
+  A.head.partials = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + 256);
+  return sg_dispatch(A, w_dtype, T, (cudaStream_t)stream);
 }

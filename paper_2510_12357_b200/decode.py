@@ -57,14 +57,16 @@ class MobileGenerator:
         self.k_l = torch.full((1,), s.k_little, dtype=torch.int32, device=dev)
         self.k_b = torch.full((1,), s.k_big, dtype=torch.int32, device=dev)
         self.one = torch.ones(1, dtype=torch.uint8, device=dev)
-        self.ws = dm.head_workspace(1)
+        self.ws = dm.stream_head_ws()
         self.head_out = dict(conf=torch.empty(1, device=dev), argmax=torch.empty(1, device=dev, dtype=torch.int32),
                              fallback=torch.empty(1, device=dev, dtype=torch.uint8))
         self.stats = DecodeStats()
         self.timer = None  # optional kernel timer (bench roofline)
 
     def _head(self, x_last, gamma):
-        return K.head_confidence(x_last, self.dm.dw.head, gamma, self.spec.logit_scale, ws=self.ws, out=self.head_out)
+        import torch.nn.functional as Fn
+        x_ln = Fn.layer_norm(x_last, (self.spec.hidden_dim,), eps=1e-5).contiguous()
+        return K.stream_head(x_ln, self.dm.dw.head, gamma, self.spec.logit_scale, ws=self.ws, out=self.head_out)
 
     def start(self, prompt: list[int]) -> DecodeSession:
         dm, s = self.dm, self.spec

@@ -234,3 +234,25 @@ def memcpy_async(dst: torch.Tensor, src: torch.Tensor, stream=None):
     """Raw cudaMemcpyAsync (graph-capturable) between pinned host and device tensors."""
     n = src.numel() * src.element_size()
     N.check(N.lib.mobile_memcpy_async(N.ptr(dst), N.ptr(src), n, _s(stream)), "memcpy_async")
+
+
+class StreamHeadWorkspace:
+    def __init__(self, device):
+        self.buf = torch.zeros(int(N.lib.mobile_stream_head_ws_bytes()), dtype=torch.uint8, device=device)
+
+
+def stream_head(x_ln, w_head, gamma, logit_scale, *, ws: StreamHeadWorkspace, logits_out=None, out=None,
+                stream=None):
+    """Head + confidence on the bulk-copy engine (x_ln = LN(x), T <= 4 rows)."""
+    _dev(x_ln, w_head)
+    T, d = x_ln.shape
+    V = w_head.shape[0]
+    if out is None:
+        out = dict(conf=torch.empty(T, device=x_ln.device, dtype=torch.float32),
+                   argmax=torch.empty(T, device=x_ln.device, dtype=torch.int32),
+                   fallback=torch.empty(T, device=x_ln.device, dtype=torch.uint8))
+    _count()
+    N.check(N.lib.mobile_stream_head(N.ptr(x_ln), T, d, N.ptr(w_head), dtype_code(w_head), V, float(logit_scale),
+                                     float(gamma), N.ptr(logits_out), N.ptr(out["conf"]), N.ptr(out["argmax"]),
+                                     N.ptr(out["fallback"]), N.ptr(ws.buf), _s(stream)), "stream_head")
+    return out

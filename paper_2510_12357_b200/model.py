@@ -166,6 +166,9 @@ class MoBiLEMoE:
         return sc["x_out"]
 
     def _experts_warp(self, x, layer, sc, k_tok, k_max, loc, timer, ln_out):
+        from .weights import tile_chunk
+        if max(self.I, self.Is, self.d) > tile_chunk(self.dw.elem_bytes):
+            raise N.MobileNativeError("warp FFN kernels read row-major weights: K must fit one tile chunk")
         T = x.shape[0]
         dw, E, d = self.dw, self.E, self.d
         r, p = sc["router"], sc["perm"]
@@ -227,7 +230,8 @@ class DeviceModel:
 
     # ------------------------------------------------------------- pieces
     def _lin(self, h: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
-        """h @ w.T for an out-major weight (N, d)."""
+        """h @ w.T for an out-major (tiled) weight (N, d)."""
+        w = self.dw.plain(w)
         if w.dtype == torch.float32:
             return Fn.linear(h, w)
         return Fn.linear(h.to(w.dtype), w).to(torch.float32)
@@ -247,6 +251,11 @@ class DeviceModel:
         attn = torch.softmax(scores, dim=-1)
         out = (attn @ vh).transpose(0, 1).reshape(n, d)
         return x + self._lin(out, dw.o[layer])
+
+    def stream_head_ws(self) -> K.StreamHeadWorkspace:
+        if getattr(self, "_sh_ws", None) is None:
+            self._sh_ws = K.StreamHeadWorkspace(self.device)
+        return self._sh_ws
 
     def head_workspace(self, T: int) -> K.HeadWorkspace:
         ws = self.head_ws.get(T)
@@ -284,8 +293,8 @@ class DeviceModel:
             sc["router"]["flags"].zero_()
             x = x_new.clone()
         logits = torch.empty(1, s.vocab_size, device=dev, dtype=torch.float32)
-        K.head_confidence(x[-1:].contiguous(), dw.head, 0.0, s.logit_scale, ws=self.head_workspace(1),
-                          logits_out=logits)
+        x_ln = Fn.layer_norm(x[-1:], (s.hidden_dim,), eps=1e-5).contiguous()
+        K.stream_head(x_ln, dw.head, 0.0, s.logit_scale, ws=self.stream_head_ws(), logits_out=logits)
         probs = K.softmax_rows(logits, torch.float64)[0]
         return probs, states, sels, flags
 

@@ -64,7 +64,7 @@ class StepEngine:
         self.ones = torch.ones(B, dtype=torch.uint8, device=dev)
         self.head = {kd: dict(conf=torch.empty(B, dtype=f32, device=dev), argmax=torch.empty(B, dtype=i32, device=dev),
                               fallback=torch.empty(B, dtype=torch.uint8, device=dev)) for kd in KINDS}
-        self.head_ws = K.HeadWorkspace(B, s.vocab_size, dev)
+        self.head_ws = K.StreamHeadWorkspace(dev)
         self.gamma = torch.zeros(1)  # host value baked at capture; see set_gamma
         self._gamma = 0.7
         self.graphs: dict = {}
@@ -100,8 +100,9 @@ class StepEngine:
                                    timer=None if self.use_graphs else self.timer, ln_out=self.ln)
 
     def _head(self, x_last: torch.Tensor, kind: str):
+        """LN(x) is already in self.ln (written by the last layer's combine)."""
         s = self.spec
-        K.head_confidence(x_last, self.dm.dw.head, self._gamma, s.logit_scale, ws=self.head_ws, out=self.head[kind])
+        K.stream_head(self.ln, self.dm.dw.head, self._gamma, s.logit_scale, ws=self.head_ws, out=self.head[kind])
 
     def _offload_loc(self, l: int, kind: str):
         row = 1 if kind == "big" else 0

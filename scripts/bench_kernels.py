@@ -36,6 +36,12 @@ for name, spec in (("qwen", QWEN15_MOE), ("olmoe", OLMOE)):
         scs = [dict(sc) for sc in scs]  # route() returns views of shared scratch: rebuild per layer
         for impl in ("stream", "warp"):
             M.FFN_IMPL = impl
+            try:
+                sc0 = moe.route(x, 0, k_tok, k)
+                moe.experts(x, 0, sc0, k_tok, k)
+            except Exception as exc:  # warp kernels need row-major (untiled) K
+                out[f"{name}_{kname}_{impl}"] = f"n/a: {exc}"
+                continue
             for it in range(3):
                 for l in range(L):
                     sc = moe.route(x, l, k_tok, k)
