@@ -177,6 +177,8 @@ typedef struct {
   float* out;
   const float* residual;
   int epi;
+  int prefetch;  /* 1: weights AND expert lists do not depend on the previous kernel
+                    (dense / shared experts): copies may start before the PDL wait */
 } mobile_sg_group;
 int mobile_stream_gemv(const mobile_sg_group* groups, int n_groups, int w_dtype, int max_tokens,
                        void* stream);
@@ -185,6 +187,16 @@ int mobile_stream_gemv(const mobile_sg_group* groups, int n_groups, int w_dtype,
  * layer-normalised), conf[t] = max softmax, first argmax, fallback =
  * conf <= gamma.  T <= 4.  workspace >= mobile_stream_head_ws_bytes(), zeroed
  * once (the kernel leaves it zeroed). */
+/* Down projection fused with the combine (mobile_combine semantics, run by
+ * the last CTA to finish): groups as mobile_stream_gemv (they write Y /
+ * Y_shared), then x_out = x + sum_j gates*Y (selection order) + shared, and
+ * ln_out = LN(x_out) if non-NULL.  workspace >= mobile_down_combine_ws_bytes(),
+ * zeroed once (left zeroed). */
+size_t mobile_down_combine_ws_bytes(void);
+int mobile_down_combine(const mobile_sg_group* groups, int n_groups, int w_dtype, int max_tokens,
+                        const float* x, const float* Y, const float* gates, const int* k_tok, int T, int k_max,
+                        int d, const float* Y_shared, int n_shared, const float* shared_logits, float* x_out,
+                        float* ln_out, void* workspace, void* stream);
 size_t mobile_stream_head_ws_bytes(void);
 int mobile_stream_head(const float* x_ln, int T, int d, const void* w_head, int w_dtype, int V,
                        float logit_scale, float gamma, float* logits_out, float* conf_out, int* argmax_out,
@@ -291,6 +303,15 @@ int mobile_offload_release(mobile_offload* o, int layer, const int* experts, int
 int mobile_offload_sync(mobile_offload* o);
 int mobile_offload_token_end(mobile_offload* o);
 mobile_cache* mobile_offload_cache(mobile_offload* o);
+/* Drive one whole pass of L+1 captured graph segments (cudaGraphExec_t
+ * handles) with the engine.py:121-169 protocol: planned = 1 replays a known
+ * plan (targets (L, k), issue windows max(0, l - lookahead)); planned = 0 loads
+ * on demand from the per-layer active lists the segments copy into
+ * active_host ((L, E+1) pinned).  Slot tables go to slot_host ((L, E) pinned),
+ * which the segments copy to the device. */
+int mobile_offload_run_pass(mobile_offload* o, const unsigned long long* graph_execs, int L, void* stream,
+                            int planned, const int* active_host, const int* targets, int k, int* slot_host,
+                            const void* slot_dev_row, long long slot_row_bytes, int lookahead, int* fresh_out);
 /* bytes copied H2D so far, transfers issued */
 int mobile_offload_counters(const mobile_offload* o, long long* out2);
 

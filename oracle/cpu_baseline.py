@@ -70,7 +70,8 @@ def oracle_spec_from(ms) -> R.OracleSpec:
                         hidden_dim=ms.hidden_dim, vocab_size=ms.vocab_size, eos_token=ms.eos_token, seed=ms.seed,
                         ffn_dim=ms.ffn, activation=ms.activation, n_shared=ms.n_shared,
                         shared_ffn_dim=ms.shared_ffn, shared_gate=ms.shared_gate, gate_norm=ms.gate_norm,
-                        n_heads=ms.n_heads, logit_scale=ms.logit_scale, embed_scale=ms.embed_scale)
+                        n_heads=ms.n_heads, logit_scale=ms.logit_scale, embed_scale=ms.embed_scale,
+                        pos_encoding=ms.pos_encoding)
 
 
 def time_decode(W: R.OracleWeights, prompt, flags, warmup: int, steps: int, gamma=0.7):

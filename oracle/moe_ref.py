@@ -50,6 +50,7 @@ class OracleSpec:
     n_heads: int = 1
     logit_scale: float = LOGIT_SCALE
     embed_scale: float = 0.0  # 0 -> 1/sqrt(d) as the toy (toymoe.py:109-112)
+    pos_encoding: str = "sinusoidal"  # toymoe.py:135-140 | "none" (extension)
 
     def __post_init__(self):
         if self.k_little == 0:
@@ -407,7 +408,8 @@ class KVDecoder:
         selections_last, new_kv).  Does NOT commit the K/V rows."""
         W, s = self.W, self.W.spec
         n = len(tokens)
-        x = W.embed[np.asarray(tokens)] + positional(n, s.hidden_dim, self.length).astype(W.embed.dtype)
+        pe = positional(n, s.hidden_dim, self.length) if s.pos_encoding != "none" else np.zeros((n, s.hidden_dim))
+        x = W.embed[np.asarray(tokens)] + pe.astype(W.embed.dtype)
         states = np.empty((s.num_layers, s.num_experts))
         sels, new_kv = [], []
         mask = None

@@ -34,7 +34,7 @@ class mobile_sg_group(C.Structure):
     _fields_ = [("w_base", C.c_void_p), ("stride", C.c_longlong), ("slot", C.c_void_p), ("x", C.c_void_p),
                 ("x_div", C.c_int), ("offsets", C.c_void_p), ("pairs", C.c_void_p), ("active", C.c_void_p),
                 ("dense_T", C.c_int), ("max_active", C.c_int), ("K", C.c_int), ("rows", C.c_int),
-                ("out", C.c_void_p), ("residual", C.c_void_p), ("epi", C.c_int)]
+                ("out", C.c_void_p), ("residual", C.c_void_p), ("epi", C.c_int), ("prefetch", C.c_int)]
 
 
 class mobile_channel(C.Structure):
@@ -70,6 +70,8 @@ _SIGS = {
     "mobile_combine": ([P, P, P, P, I32, I32, I32, P, I32, P, P, P, P], I32),
     "mobile_stream_gemv": ([P, I32, I32, I32, P], I32),
     "mobile_stream_head_ws_bytes": ([], SZ),
+    "mobile_down_combine_ws_bytes": ([], SZ),
+    "mobile_down_combine": ([P, I32, I32, I32, P, P, P, P, I32, I32, I32, P, I32, P, P, P, P, P], I32),
     "mobile_stream_head": ([P, I32, I32, P, I32, I32, F, F, P, P, P, P, P, P], I32),
     "mobile_dense_gemv": ([P, I32, I32, I32, P, I32, I32, P, P, P], I32),
     "mobile_attn_decode": ([P, P, P, P, I32, I32, I32, I32, P, P], I32),
@@ -98,6 +100,7 @@ _SIGS = {
     "mobile_offload_token_end": ([P], I32),
     "mobile_offload_cache": ([P], P),
     "mobile_offload_counters": ([P, P], I32),
+    "mobile_offload_run_pass": ([P, P, I32, P, I32, P, P, I32, P, P, I64, I32, P], I32),
 }
 EXPORTED = tuple(_SIGS)
 for _name, (_args, _ret) in _SIGS.items():

@@ -3,6 +3,8 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <unordered_map>
 
@@ -38,6 +40,15 @@ int set_smem_once(const void* func, size_t smem) {
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
   cur = smem;
   return MOBILE_OK;
+}
+
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("MOBILE_PDL");
+    v = (e && std::strcmp(e, "0") == 0) ? 0 : 1;
+  }
+  return v == 1;
 }
 
 }  // namespace mobile

@@ -123,6 +123,8 @@ __global__ void attn_decode_kernel(const float* __restrict__ qkv, float* __restr
                                    int max_len, float* __restrict__ out) {
   extern __shared__ __align__(16) float sc[];  // max_len scores + hd q
   __shared__ float red[32];
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.x / H, hh = blockIdx.x % H;
   const int hd = d / H;
   const int p = pos[b];
@@ -178,6 +180,8 @@ __global__ void embed_kernel(const int* __restrict__ tok, const int* __restrict_
                              const float* __restrict__ embed, const float* __restrict__ pe, int d,
                              float* __restrict__ x, float* __restrict__ ln_out) {
   __shared__ float red[32];
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.x;
   const float* er = embed + (size_t)tok[b] * d;
   const float* pr = pe + (size_t)pos[b] * d;
@@ -211,6 +215,8 @@ __global__ void embed_kernel(const int* __restrict__ tok, const int* __restrict_
 }
 
 __global__ void advance_kernel(int* pos, int B, int* tok, const int* next_tok) {
+  pdl_trigger();
+  pdl_wait();
   const int b = threadIdx.x;
   if (b < B) {
     pos[b] += 1;
@@ -265,22 +271,19 @@ extern "C" int mobile_attn_decode(const float* qkv, float* k_cache, float* v_cac
   const size_t smem = sizeof(float) * ((size_t)max_len + d / H);
   if (smem > 200 * 1024) { set_error("attn_decode: max_len=%d too long", max_len); return MOBILE_ERR_UNSUPPORTED; }
   set_smem_once((const void*)attn_decode_kernel, smem);
-  attn_decode_kernel<<<B * H, 128, smem, (cudaStream_t)stream>>>(qkv, k_cache, v_cache, pos, d, H, max_len, out);
-  MOBILE_CHECK_LAUNCH("attn_decode");
-  return MOBILE_OK;
+  return launch_pdl(attn_decode_kernel, dim3(B * H), dim3(128), smem, (cudaStream_t)stream, 1, "attn_decode", qkv,
+                    k_cache, v_cache, pos, d, H, max_len, out);
 }
 
 extern "C" int mobile_embed(const int* tok, const int* pos, const float* embed, const float* pe, int B, int d,
                             float* x, float* ln_out, void* stream) {
   if (B <= 0 || d <= 0) { set_error("embed: bad shape"); return MOBILE_ERR_INVALID; }
-  embed_kernel<<<B, 256, 0, (cudaStream_t)stream>>>(tok, pos, embed, pe, d, x, ln_out);
-  MOBILE_CHECK_LAUNCH("embed");
-  return MOBILE_OK;
+  return launch_pdl(embed_kernel, dim3(B), dim3(256), 0, (cudaStream_t)stream, 1, "embed", tok, pos, embed, pe, d, x,
+                    ln_out);
 }
 
 extern "C" int mobile_advance(int* pos, int B, int* tok, const int* next_tok, void* stream) {
   if (B <= 0 || B > 1024) { set_error("advance: bad B"); return MOBILE_ERR_INVALID; }
-  advance_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(pos, B, tok, next_tok);
-  MOBILE_CHECK_LAUNCH("advance");
-  return MOBILE_OK;
+  return launch_pdl(advance_kernel, dim3(1), dim3(1024), 0, (cudaStream_t)stream, 1, "advance", pos, B, tok,
+                    next_tok);
 }

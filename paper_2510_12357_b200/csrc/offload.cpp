@@ -14,8 +14,10 @@
 // kernels, and a new copy into the slot waits on it first.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <limits>
+#include <tuple>
 #include <vector>
 
 #include "../../include/mobile.h"
@@ -205,6 +207,73 @@ int mobile_offload_token_end(mobile_offload* o) {
 }
 
 mobile_cache* mobile_offload_cache(mobile_offload* o) { return o->cache; }
+
+// One whole pass of an offloaded decode step, driven from C++ so the per-layer
+// host work is a few microseconds: graph segment l = [experts(l-1), attention
+// + routing(l)], segment L = [experts(L-1), head] (runtime.py captures them).
+// The order of operations is StreamSimulator.run_pass (engine.py:121-169):
+//   planned pass: (1) speculative issue window at the layer boundary
+//                 (engine.py:98-119: stale entries dropped, deferred retried)
+//   both:         (2) attention/routing (segment l) ...
+//   demand pass:  ... host reads layer l's active experts (the only sync)
+//   both:         (3) request + pin, issue misses, (4) compute waits on copies,
+//                 (5) experts run in segment l+1, (6) unpin after it is enqueued
+int mobile_offload_run_pass(mobile_offload* o, const unsigned long long* graph_execs, int L, void* stream,
+                            int planned, const int* active_host, const int* targets, int k, int* slot_host,
+                            const void* slot_dev_row, long long slot_row_bytes, int lookahead, int* fresh_out) {
+  cudaStream_t cs = (cudaStream_t)stream;
+  const int E = o->E;
+  int fresh = 0;
+  // planned pass: entries sorted by (earliest_issue_layer, layer, expert) (policy.py:86-106)
+  std::vector<std::tuple<int, int, int>> waiting;
+  if (planned) {
+    for (int l = 0; l < L; ++l)
+      for (int j = 0; j < k; ++j) waiting.emplace_back(std::max(0, l - lookahead), l, targets[l * k + j]);
+    std::sort(waiting.begin(), waiting.end());
+  }
+  std::vector<int> prev, cur;
+  for (int l = 0; l < L; ++l) {
+    if (planned) {  // (1) issue window
+      std::vector<std::tuple<int, int, int>> kept;
+      size_t i = 0;
+      for (; i < waiting.size(); ++i) {
+        const auto& en = waiting[i];
+        if (std::get<0>(en) > l) break;
+        if (std::get<1>(en) < l) continue;  // stale: its layer already executed
+        int st = 0;
+        const int rc = mobile_offload_prefetch(o, std::get<1>(en), std::get<2>(en), &st);
+        if (rc == MOBILE_ERR_DEFERRED) kept.push_back(en);
+        else if (rc != MOBILE_OK) return rc;
+      }
+      kept.insert(kept.end(), waiting.begin() + i, waiting.end());
+      waiting.swap(kept);
+    }
+    OFF_CUDA(cudaGraphLaunch((cudaGraphExec_t)graph_execs[l], cs), "segment launch");  // (2)
+    if (l > 0) {
+      if (int rc = mobile_offload_release(o, l - 1, prev.data(), (int)prev.size(), stream)) return rc;  // (6)
+    }
+    cur.clear();
+    if (planned) {
+      cur.assign(targets + l * k, targets + (l + 1) * k);
+    } else {  // the layer's selection comes back to the host
+      OFF_CUDA(cudaStreamSynchronize(cs), "routing sync");
+      settle(o);
+      const int* a = active_host + (size_t)l * (E + 1);
+      cur.assign(a + 1, a + 1 + a[0]);
+    }
+    int issued = 0;  // (3) + (4)
+    if (int rc = mobile_offload_require(o, l, cur.data(), (int)cur.size(), stream, slot_host + (size_t)l * E, &issued))
+      return rc;
+    fresh += issued;
+    prev.swap(cur);
+  }
+  OFF_CUDA(cudaGraphLaunch((cudaGraphExec_t)graph_execs[L], cs), "segment launch");  // (5) experts(L-1) + head
+  if (int rc = mobile_offload_release(o, L - 1, prev.data(), (int)prev.size(), stream)) return rc;
+  (void)slot_dev_row;
+  (void)slot_row_bytes;
+  if (fresh_out) *fresh_out = fresh;
+  return MOBILE_OK;
+}
 
 int mobile_offload_counters(const mobile_offload* o, long long* out2) {
   out2[0] = o->bytes;

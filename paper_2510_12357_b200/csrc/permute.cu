@@ -22,6 +22,8 @@ __global__ void __launch_bounds__(kPermThreads) permute_kernel(const int* __rest
   __shared__ int base[kPermMaxE];
   __shared__ int wcnt[kPermWarps][kPermMaxE];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pdl_trigger();
+  pdl_wait();
   const int P = T * k_max;
   for (int e = tid; e < E; e += kPermThreads) cnt[e] = 0;
   for (int i = tid; i < kPermWarps * E; i += kPermThreads) wcnt[i / E][i % E] = 0;
@@ -86,6 +88,8 @@ __global__ void __launch_bounds__(1024) combine_kernel(const float* __restrict__
   __shared__ float red[32];
   __shared__ float sg[16];    // gates (selection order) then shared-expert gates
   const int t = blockIdx.x;
+  pdl_trigger();
+  pdl_wait();
   const int kt = k_tok ? k_tok[t] : k_max;
   if (threadIdx.x < kt) sg[threadIdx.x] = gates[(size_t)t * k_max + threadIdx.x];
   if (threadIdx.x < n_shared)
@@ -142,10 +146,8 @@ extern "C" int mobile_permute(const int* idx, const int* k_tok, int T, int k_max
                               int* sorted_pairs, int* active, void* stream) {
   if (T < 0 || k_max <= 0 || E <= 0) { set_error("permute: bad shape T=%d k=%d E=%d", T, k_max, E); return MOBILE_ERR_INVALID; }
   if (E > kPermMaxE) { set_error("permute: E=%d exceeds %d", E, kPermMaxE); return MOBILE_ERR_UNSUPPORTED; }
-  permute_kernel<<<1, kPermThreads, 0, (cudaStream_t)stream>>>(idx, k_tok, T, k_max, E, offsets,
-                                                              sorted_pairs, active);
-  MOBILE_CHECK_LAUNCH("permute");
-  return MOBILE_OK;
+  return launch_pdl(permute_kernel, dim3(1), dim3(kPermThreads), 0, (cudaStream_t)stream, 1, "permute", idx, k_tok,
+                    T, k_max, E, offsets, sorted_pairs, active);
 }
 
 extern "C" int mobile_combine(const float* x, const float* Y, const float* gates, const int* k_tok,
@@ -155,8 +157,6 @@ extern "C" int mobile_combine(const float* x, const float* Y, const float* gates
   if (T == 0) return MOBILE_OK;
   if (n_shared > 8) { set_error("combine: at most 8 shared experts"); return MOBILE_ERR_UNSUPPORTED; }
   const int threads = d >= 1024 ? 1024 : ((d + 31) / 32) * 32;
-  combine_kernel<<<T, threads, 0, (cudaStream_t)stream>>>(x, Y, gates, k_tok, k_max, d, Y_shared,
-                                                      Y_shared ? n_shared : 0, shared_logits, T, x_out, ln_out);
-  MOBILE_CHECK_LAUNCH("combine");
-  return MOBILE_OK;
+  return launch_pdl(combine_kernel, dim3(T), dim3(threads), 0, (cudaStream_t)stream, 1, "combine", x, Y, gates,
+                    k_tok, k_max, d, Y_shared, Y_shared ? n_shared : 0, shared_logits, T, x_out, ln_out);
 }

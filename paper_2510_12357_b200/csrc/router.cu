@@ -274,6 +274,18 @@ __global__ void __launch_bounds__(kRouterThreads) router_kernel(RouterArgs a) {
   // every CTA of the cluster must have started before DSMEM is touched; the
   // relaxed arrive here overlaps that handshake with the LayerNorm below.
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+  pdl_trigger();
+  {  // the router rows are static: pull this CTA's slice into L2 while the previous kernel drains
+    const int per0 = (Etot + CS - 1) / CS;
+    const int eb = rank * per0, ee = min(Etot, eb + per0);
+    if (threadIdx.x == 0 && ee > eb) {
+      const char* src = reinterpret_cast<const char*>(a.w) + (size_t)eb * a.d * sizeof(W);
+      const unsigned bytes = (unsigned)((size_t)(ee - eb) * a.d * sizeof(W));
+      if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && (bytes & 15) == 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+    }
+  }
+  pdl_wait();  // x is the previous kernel's output
 
   // 1. stage + layer-normalise the token tile
   for (int t = 0; t < rows; ++t) {
@@ -335,21 +347,8 @@ static int launch_router(const RouterArgs& a, cudaStream_t stream) {
   const size_t smem = sizeof(float) * ((size_t)TT * a.d + (size_t)TT * Etot + 64);
   auto kern = router_kernel<W, TT>;
   if (int st = set_smem_once((const void*)kern, smem)) return st;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(cs, (a.T + TT - 1) / TT, 1);
-  cfg.blockDim = dim3(kRouterThreads, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cs;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
-  if (e != cudaSuccess) return cuda_status(e, "router launch");
-  return MOBILE_OK;
+  return launch_pdl(kern, dim3(cs, (a.T + TT - 1) / TT, 1), dim3(kRouterThreads), smem, stream, cs,
+                    "router launch", a);
 }
 
 // ---------------------------------------------------------------- topk rows

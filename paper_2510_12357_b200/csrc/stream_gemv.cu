@@ -3,8 +3,10 @@
 // Every decode-time matrix product on the MoBiLE path is HBM-bound: each
 // weight byte is used by 1-4 tokens.  This kernel streams weights into shared
 // memory with cp.async.bulk (the Blackwell bulk-copy engine; SASS UBLKCP) on a
-// full/empty mbarrier ring of 3 x 64 KB stages per CTA, one CTA per SM, so
-// ~192 KB per SM is in flight with no register cost.
+// full/empty mbarrier ring (3 stages at batch 1, 2 above), one CTA per SM, so
+// ~200 KB per SM is in flight with no register cost.  A stage holds one 64 KB
+// weight tile AND the matching activation slices (bulk-copied too), so the
+// consumers' inner loop reads shared memory only.
 //
 // Weights are stored TILED (see weights.py): a matrix of `rows` x K is cut
 // into tiles of 16 rows x 4 KB of K (2048 bf16 / 1024 f32) laid out
@@ -24,15 +26,14 @@
 //            (toymoe.py:209-210, 273; policy.py:69-79)
 // Work is a list of UNITS = (group, active expert, 16-row block); a launch can
 // carry several groups (routed + shared experts) so one launch covers a
-// layer's whole gate-up (or down) and balances 148 SMs.
+// layer's whole gate-up (or down); each CTA owns a contiguous unit range.
 #include "common.cuh"
 
 namespace mobile {
 
 constexpr int kSgConsumerWarps = 8;
 constexpr int kSgThreads = (kSgConsumerWarps + 1) * 32;  // + 1 producer warp
-constexpr int kSgStages = 3;
-constexpr int kSgStageBytes = 64 * 1024;
+constexpr int kSgWBytes = 64 * 1024;   // weight tile region of a stage
 constexpr int kSgTileRows = 16;
 constexpr int kSgTileRowBytes = 4096;  // K chunk per tile row
 constexpr int kSgMaxGroups = 4;
@@ -57,6 +58,7 @@ struct SgGroup {
   float* out;
   const float* residual;
   int epi;
+  int prefetch;             // weights + expert lists independent of the previous kernel
   int units;                // max_active * ceil(rows / 16)
 };
 
@@ -69,9 +71,23 @@ struct SgHead {             // HEAD epilogue state (one dense group)
   unsigned* ticket;         // left at 0
 };
 
+struct SgCombine {          // fused combine epilogue (last CTA), toymoe.py:204, 207
+  const float* x;           // (T, d) residual in
+  const float* Y;           // (T*k_max, d) routed expert outputs (pair order)
+  const float* gates;       // (T, k_max)
+  const int* k_tok;         // (T,) or NULL
+  const float* Ys;          // (T, S, d) shared outputs or NULL
+  const float* shared_logits;  // (T, S) sigmoid gates or NULL
+  float* x_out;             // (T, d)
+  float* ln_out;            // (T, d) LN(x_out) or NULL
+  unsigned* ticket;         // left at 0
+  int T, d, k_max, n_shared;
+};
+
 struct SgArgs {
   SgGroup g[kSgMaxGroups];
   SgHead head;
+  SgCombine comb;
   int n_groups;
   int total_units;
 };
@@ -82,6 +98,12 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {  // no arrival
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -104,68 +126,130 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// Iterator over this CTA's (unit, token-chunk, k-chunk) items.
+template <int TT>
+struct SgCfg {
+  static constexpr int kStages = TT == 1 ? 3 : 2;
+  static constexpr int kXBytes = TT * 8192;  // TT activation slices of <= 4 KB-of-K (f32: 2048 floats max)
+  static constexpr int kStageBytes = kSgWBytes + kXBytes;
+};
+
+// Iterator over this CTA's (unit, token-chunk, k-chunk) items.  A CTA owns a
+// contiguous range of units, i.e. consecutive row blocks of mostly one expert,
+// so the expert-level lookups (active list, offsets, slot, pair ids: dependent
+// global loads) are cached and re-read only when the expert or token chunk
+// changes -- the producer's issue loop is then pure arithmetic.
+template <int TT>
 struct SgIter {
-  int unit;
+  int unit, unit_end;
   int g, a, rb, rr;  // group, active slot, row block, rows in block
-  int e, p0, n;      // expert, first pair index, #pairs
+  int e, p0, n, slot;
   int tc, kc;
+  int cg, ca, ctc;   // cache keys
+  int pair[TT];
   bool valid;
+  bool static_only;  // before the PDL wait: refuse groups that depend on the previous kernel
+  bool blocked;
 
   __device__ bool decode(const SgArgs& A) {
     int u = unit;
-    for (g = 0; g < A.n_groups; ++g) {
-      if (u < A.g[g].units) break;
-      u -= A.g[g].units;
+    int gg = 0;
+    for (; gg < A.n_groups; ++gg) {
+      if (u < A.g[gg].units) break;
+      u -= A.g[gg].units;
     }
-    if (g >= A.n_groups) return false;
-    const SgGroup& G = A.g[g];
+    if (gg >= A.n_groups) return false;
+    const SgGroup& G = A.g[gg];
+    if (static_only && !G.prefetch) {
+      blocked = true;
+      return true;  // stop here without touching dependent data
+    }
     const int upe = (G.rows + kSgTileRows - 1) / kSgTileRows;
-    a = u / upe;
-    rb = u - a * upe;
+    const int aa = u / upe;
+    rb = u - aa * upe;
     rr = min(kSgTileRows, G.rows - rb * kSgTileRows);
-    if (G.offsets) {
-      if (a >= G.active[0]) return false;
-      e = G.active[1 + a];
-      p0 = G.offsets[e];
-      n = G.offsets[e + 1] - p0;
-    } else {
-      e = 0;
-      p0 = 0;
-      n = G.dense_T;
+    if (gg != cg || aa != ca) {
+      cg = gg;
+      ca = aa;
+      ctc = -1;
+      if (G.offsets) {
+        if (aa >= G.active[0]) { n = 0; e = 0; p0 = 0; slot = 0; }
+        else {
+          e = G.active[1 + aa];
+          p0 = G.offsets[e];
+          n = G.offsets[e + 1] - p0;
+          slot = G.slot ? G.slot[e] : e;
+        }
+      } else {
+        e = 0; p0 = 0; n = G.dense_T; slot = 0;
+      }
     }
+    g = gg;
+    a = aa;
     return n > 0;
   }
-  __device__ void seek(const SgArgs& A) {
-    while (unit < A.total_units && !decode(A)) unit += gridDim.x;
-    valid = unit < A.total_units;
-    tc = kc = 0;
+  __device__ void load_pairs(const SgArgs& A) {
+    if (ctc == tc) return;
+    ctc = tc;
+    const SgGroup& G = A.g[g];
+#pragma unroll
+    for (int t = 0; t < TT; ++t) {
+      const int q = tc * TT + t;
+      pair[t] = q < n ? (G.offsets ? G.pairs[p0 + q] : q) : 0;
+    }
   }
-  __device__ void start(const SgArgs& A) {
-    unit = blockIdx.x;
+  __device__ void seek(const SgArgs& A) {
+    while (unit < unit_end && !decode(A)) ++unit;
+    valid = unit < unit_end && !blocked;
+    tc = kc = 0;
+    if (valid) load_pairs(A);
+  }
+  __device__ void start(const SgArgs& A, bool static_only_ = false) {
+    unit = (int)(((long long)A.total_units * blockIdx.x) / gridDim.x);
+    unit_end = (int)(((long long)A.total_units * (blockIdx.x + 1)) / gridDim.x);
+    cg = ca = ctc = -1;
+    static_only = static_only_;
+    blocked = false;
     seek(A);
   }
-  __device__ void next(const SgArgs& A, int kc_elems, int tt) {
+  __device__ void next(const SgArgs& A, int kc_elems) {
     const SgGroup& G = A.g[g];
     if (++kc * kc_elems < G.K) return;
     kc = 0;
-    if (++tc * tt < n) return;
-    unit += gridDim.x;
+    if (++tc * TT < n) { load_pairs(A); return; }
+    ++unit;
     seek(A);
   }
 };
 
-template <typename W>
-__device__ void sg_issue(const SgArgs& A, const SgIter& it, char* stage, uint64_t* bar) {
+template <typename W, int TT>
+__device__ void sg_issue(const SgArgs& A, const SgIter<TT>& it, char* stage, uint64_t* bar) {
   constexpr int KC = kSgTileRowBytes / sizeof(W);
   const SgGroup& G = A.g[it.g];
-  const int s = G.slot ? G.slot[it.e] : it.e;
+  const int s = it.slot;
   const int k0 = it.kc * KC;
   const int kn = min(KC, G.K - k0);
   const size_t off = (size_t)it.rb * kSgTileRows * G.K + (size_t)k0 * it.rr;  // tiled layout
-  const uint32_t bytes = (uint32_t)(it.rr * kn * sizeof(W));
-  mbar_expect_tx(bar, bytes);
-  bulk_g2s(stage, G.w_base + (long long)s * G.stride + off * sizeof(W), bytes, bar);
+  const uint32_t wbytes = (uint32_t)(it.rr * kn * sizeof(W));
+  const int nt = min(TT, it.n - it.tc * TT);
+  const uint32_t xbytes = (uint32_t)(kn * sizeof(float));
+  mbar_expect_tx(bar, wbytes + nt * xbytes);
+  bulk_g2s(stage, G.w_base + (long long)s * G.stride + off * sizeof(W), wbytes, bar);
+  for (int t = 0; t < nt; ++t)  // activation slices x[row, k0:k0+kn]
+    bulk_g2s(stage + kSgWBytes + (size_t)t * xbytes, G.x + (size_t)(it.pair[t] / G.x_div) * G.K + k0, xbytes, bar);
+}
+
+// L2 prefetch of an item's weight tile (no shared memory cost): the producer
+// runs this kSgL2Ahead items ahead of its bulk copies so that, under a loaded
+// memory system, most bulk copies hit L2 instead of waiting on DRAM.
+constexpr int kSgL2Ahead = 0;  // measured: L2 prefetch did not help (kept for experiments)
+template <typename W, int TT>
+__device__ void sg_prefetch(const SgArgs& A, const SgIter<TT>& it) {
+  constexpr int KC = kSgTileRowBytes / sizeof(W);
+  const SgGroup& G = A.g[it.g];
+  const int k0 = it.kc * KC;
+  const int kn = min(KC, G.K - k0);
+  const size_t off = (size_t)it.rb * kSgTileRows * G.K + (size_t)k0 * it.rr;
+  bulk_prefetch_l2(G.w_base + (long long)it.slot * G.stride + off * sizeof(W), (uint32_t)(it.rr * kn * sizeof(W)));
 }
 
 __device__ __forceinline__ void online_add(float& m, float& s, int& arg, float l, int idx) {
@@ -185,6 +269,8 @@ __device__ __forceinline__ void online_merge2(float& M, float& S, int& A_, float
 
 template <typename W, int TT>
 __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid_constant__ SgArgs A) {
+  constexpr int kSgStages = SgCfg<TT>::kStages;
+  constexpr int kSgStageBytes = SgCfg<TT>::kStageBytes;
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) uint64_t full[kSgStages];
   __shared__ __align__(8) uint64_t empty[kSgStages];
@@ -203,29 +289,71 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
   }
   __syncthreads();
 
+  pdl_trigger();
   if (warp == kSgConsumerWarps) {
     // ---------------- producer: one lane streams every item of this CTA
     if (lane == 0) {
-      SgIter prod;
+      // phase A (overlaps the previous kernel's tail): weight tiles of static
+      // groups (dense / shared experts) for the first stages
+      int npre = 0;
+      {
+        SgIter<TT> pre;
+        pre.start(A, /*static_only=*/true);
+        while (npre < kSgStages && pre.valid) {
+          const SgGroup& G = A.g[pre.g];
+          const int k0 = pre.kc * KC, kn = min(KC, G.K - k0);
+          const size_t off = (size_t)pre.rb * kSgTileRows * G.K + (size_t)k0 * pre.rr;
+          const uint32_t wbytes = (uint32_t)(pre.rr * kn * sizeof(W));
+          mbar_expect_tx_only(&full[npre], wbytes);
+          bulk_g2s(smem + (size_t)npre * kSgStageBytes, G.w_base + (long long)pre.slot * G.stride + off * sizeof(W),
+                   wbytes, &full[npre]);
+          ++npre;
+          pre.next(A, KC);
+        }
+      }
+      pdl_wait();  // activations / routing of the previous kernel are now visible
+      SgIter<TT> prod;
       prod.start(A);
+      SgIter<TT> pf = prod;  // L2-prefetch cursor, kSgStages + kSgL2Ahead items ahead
+      for (int j = 0; j < kSgStages && pf.valid; ++j) pf.next(A, KC);
+      for (int j = 0; j < kSgL2Ahead && pf.valid; ++j) {
+        sg_prefetch<W, TT>(A, pf);
+        pf.next(A, KC);
+      }
       int stage = 0;
       uint32_t empty_phase = 0;
       for (int i = 0; prod.valid; ++i) {
-        if (i >= kSgStages) {
-          mbar_wait(&empty[stage], (empty_phase >> stage) & 1u);
-          empty_phase ^= 1u << stage;
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (kSgL2Ahead > 0 && i >= kSgStages && pf.valid) {
+          sg_prefetch<W, TT>(A, pf);
+          pf.next(A, KC);
         }
-        sg_issue<W>(A, prod, smem + (size_t)stage * kSgStageBytes, &full[stage]);
-        prod.next(A, KC, TT);
+        if (i < npre) {  // weights already in flight: add the activation slices
+          const SgGroup& G = A.g[prod.g];
+          const int k0 = prod.kc * KC, kn = min(KC, G.K - k0);
+          const int nt = min(TT, prod.n - prod.tc * TT);
+          const uint32_t xbytes = (uint32_t)(kn * sizeof(float));
+          mbar_expect_tx(&full[stage], nt * xbytes);
+          for (int t = 0; t < nt; ++t)
+            bulk_g2s(smem + (size_t)stage * kSgStageBytes + kSgWBytes + (size_t)t * xbytes,
+                     G.x + (size_t)(prod.pair[t] / G.x_div) * G.K + k0, xbytes, &full[stage]);
+        } else {
+          if (i >= kSgStages) {
+            mbar_wait(&empty[stage], (empty_phase >> stage) & 1u);
+            empty_phase ^= 1u << stage;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          }
+          sg_issue<W, TT>(A, prod, smem + (size_t)stage * kSgStageBytes, &full[stage]);
+        }
+        prod.next(A, KC);
         stage = stage + 1 == kSgStages ? 0 : stage + 1;
       }
     }
     return;
   }
 
+  pdl_wait();
   // ---------------- consumers: warp w owns rows {w, w + 8} of each tile
-  SgIter cons;
+  SgIter<TT> cons;
   cons.start(A);
   uint32_t full_phase = 0;
   int stage = 0;
@@ -247,45 +375,39 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
     const bool has0 = warp < cons.rr, has1 = warp + 8 < cons.rr;
     int pair[TT];
 #pragma unroll
-    for (int t = 0; t < TT; ++t)
-      pair[t] = t < nt ? (G.offsets ? G.pairs[cons.p0 + cons.tc * TT + t] : cons.tc * TT + t) : 0;
+    for (int t = 0; t < TT; ++t) pair[t] = cons.pair[t];
     mbar_wait(&full[stage], (full_phase >> stage) & 1u);
     full_phase ^= 1u << stage;
     if (has0) {
-      const W* row0 = reinterpret_cast<const W*>(smem + (size_t)stage * kSgStageBytes) + (size_t)warp * kn;
+      const char* st = smem + (size_t)stage * kSgStageBytes;
+      const W* row0 = reinterpret_cast<const W*>(st) + (size_t)warp * kn;
       const W* row1 = row0 + (size_t)8 * kn;
+      const float* xs = reinterpret_cast<const float*>(st + kSgWBytes);
       const int nvec = kn / V;
+#pragma unroll 4
       for (int vi = lane; vi < nvec; vi += 32) {
-        float xv[TT][V];
+        float f0[V], f1[V];
+        WVec<W>::widen(*reinterpret_cast<const uint4*>(row0 + vi * V), f0);
+        if (has1) WVec<W>::widen(*reinterpret_cast<const uint4*>(row1 + vi * V), f1);
 #pragma unroll
         for (int t = 0; t < TT; ++t) {
           if (t < nt) {
-            const float4* xp = reinterpret_cast<const float4*>(G.x + (size_t)(pair[t] / G.x_div) * G.K + k0 + vi * V);
+            const float4* xp = reinterpret_cast<const float4*>(xs + (size_t)t * kn + vi * V);
 #pragma unroll
             for (int q = 0; q < V / 4; ++q) {
-              const float4 f = __ldg(xp + q);
-              xv[t][4 * q] = f.x; xv[t][4 * q + 1] = f.y; xv[t][4 * q + 2] = f.z; xv[t][4 * q + 3] = f.w;
+              const float4 xq = xp[q];
+              acc[0][t] = fmaf(f0[4 * q], xq.x, acc[0][t]);
+              acc[0][t] = fmaf(f0[4 * q + 1], xq.y, acc[0][t]);
+              acc[0][t] = fmaf(f0[4 * q + 2], xq.z, acc[0][t]);
+              acc[0][t] = fmaf(f0[4 * q + 3], xq.w, acc[0][t]);
+              if (has1) {
+                acc[1][t] = fmaf(f1[4 * q], xq.x, acc[1][t]);
+                acc[1][t] = fmaf(f1[4 * q + 1], xq.y, acc[1][t]);
+                acc[1][t] = fmaf(f1[4 * q + 2], xq.z, acc[1][t]);
+                acc[1][t] = fmaf(f1[4 * q + 3], xq.w, acc[1][t]);
+              }
             }
-          } else {
-#pragma unroll
-            for (int q = 0; q < V; ++q) xv[t][q] = 0.f;
           }
-        }
-        {
-          float f[V];
-          WVec<W>::widen(*reinterpret_cast<const uint4*>(row0 + vi * V), f);
-#pragma unroll
-          for (int t = 0; t < TT; ++t)
-#pragma unroll
-            for (int q = 0; q < V; ++q) acc[0][t] = fmaf(f[q], xv[t][q], acc[0][t]);
-        }
-        if (has1) {
-          float f[V];
-          WVec<W>::widen(*reinterpret_cast<const uint4*>(row1 + vi * V), f);
-#pragma unroll
-          for (int t = 0; t < TT; ++t)
-#pragma unroll
-            for (int q = 0; q < V; ++q) acc[1][t] = fmaf(f[q], xv[t][q], acc[1][t]);
         }
       }
     }
@@ -330,9 +452,64 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
 #pragma unroll
         for (int t = 0; t < TT; ++t) acc[i][t] = 0.f;
     }
-    cons.next(A, KC, TT);
+    cons.next(A, KC);
   }
 
+  if (A.comb.x_out != nullptr) {
+    // ---------------- fused combine: the last CTA to finish mixes the expert
+    // outputs in selection order, adds the shared experts and the residual,
+    // and writes LN(x_out) for the next layer (one launch less per layer)
+    __threadfence();
+    asm volatile("bar.sync 1, %0;" ::"n"(kSgConsumerWarps * 32));
+    if (tid == 0) is_last = atomicAdd(A.comb.ticket, 1u) == gridDim.x - 1;
+    asm volatile("bar.sync 1, %0;" ::"n"(kSgConsumerWarps * 32));
+    if (!is_last) return;
+    __threadfence();
+    const SgCombine& Cb = A.comb;
+    float* red = &hred[0][0][0];  // 8 warps x 2 floats of scratch
+    for (int t = 0; t < Cb.T; ++t) {
+      const int kt = Cb.k_tok ? Cb.k_tok[t] : Cb.k_max;
+      float sum = 0.f;
+      for (int i = tid; i < Cb.d; i += kSgConsumerWarps * 32) {
+        float m = 0.f;
+        for (int j = 0; j < kt; ++j)
+          m = fmaf(Cb.gates[(size_t)t * Cb.k_max + j], __ldcg(Cb.Y + ((size_t)t * Cb.k_max + j) * Cb.d + i), m);
+        for (int sh = 0; sh < Cb.n_shared; ++sh) {
+          float ys = __ldcg(Cb.Ys + ((size_t)t * Cb.n_shared + sh) * Cb.d + i);
+          if (Cb.shared_logits) ys = sigmoid_f(Cb.shared_logits[(size_t)t * Cb.n_shared + sh]) * ys;
+          m += ys;
+        }
+        const float v = Cb.x[(size_t)t * Cb.d + i] + m;
+        Cb.x_out[(size_t)t * Cb.d + i] = v;
+        sum += v;
+      }
+      if (Cb.ln_out) {
+        sum = warp_sum(sum);
+        if (lane == 0) red[warp] = sum;
+        asm volatile("bar.sync 1, %0;" ::"n"(kSgConsumerWarps * 32));
+        float mean = 0.f;
+        for (int w = 0; w < kSgConsumerWarps; ++w) mean += red[w];
+        mean /= (float)Cb.d;
+        float q = 0.f;
+        for (int i = tid; i < Cb.d; i += kSgConsumerWarps * 32) {
+          const float c = Cb.x_out[(size_t)t * Cb.d + i] - mean;
+          q += c * c;
+        }
+        q = warp_sum(q);
+        asm volatile("bar.sync 1, %0;" ::"n"(kSgConsumerWarps * 32));
+        if (lane == 0) red[warp] = q;
+        asm volatile("bar.sync 1, %0;" ::"n"(kSgConsumerWarps * 32));
+        float var = 0.f;
+        for (int w = 0; w < kSgConsumerWarps; ++w) var += red[w];
+        const float inv = 1.0f / sqrtf(var / (float)Cb.d + 1e-5f);
+        for (int i = tid; i < Cb.d; i += kSgConsumerWarps * 32)
+          Cb.ln_out[(size_t)t * Cb.d + i] = (Cb.x_out[(size_t)t * Cb.d + i] - mean) * inv;
+        asm volatile("bar.sync 1, %0;" ::"n"(kSgConsumerWarps * 32));
+      }
+    }
+    if (tid == 0) *Cb.ticket = 0u;
+    return;
+  }
   if (A.head.conf == nullptr) return;
   // ---------------- HEAD: merge warps (warp order), then CTAs (CTA order)
   const int T = A.g[0].dense_T;
@@ -377,20 +554,18 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
 template <typename W, int TT>
 static int sg_launch(const SgArgs& A, cudaStream_t s) {
   auto k = stream_gemv_kernel<W, TT>;
-  const size_t smem = (size_t)kSgStages * kSgStageBytes;
+  const size_t smem = (size_t)SgCfg<TT>::kStages * SgCfg<TT>::kStageBytes;
   if (int st = set_smem_once((const void*)k, smem)) return st;
   int grid = sm_count();
-  if (A.head.conf == nullptr && A.total_units < grid) grid = A.total_units;
+  if (A.head.conf == nullptr && A.comb.x_out == nullptr && A.total_units < grid) grid = A.total_units;
   if (grid <= 0) return MOBILE_OK;
-  k<<<grid, kSgThreads, smem, s>>>(A);
-  MOBILE_CHECK_LAUNCH("stream_gemv");
-  return MOBILE_OK;
+  return launch_pdl(k, dim3(grid), dim3(kSgThreads), smem, s, 1, "stream_gemv", A);
 }
 
 static int sg_dispatch(SgArgs& A, int w_dtype, int max_tok, cudaStream_t s) {
   A.total_units = 0;
   for (int i = 0; i < A.n_groups; ++i) A.total_units += A.g[i].units;
-  if (A.total_units == 0 && A.head.conf == nullptr) return MOBILE_OK;
+  if (A.total_units == 0 && A.head.conf == nullptr && A.comb.x_out == nullptr) return MOBILE_OK;
   const int TT = max_tok <= 1 ? 1 : max_tok <= 2 ? 2 : 4;
   if (w_dtype == MOBILE_BF16) {
     if (TT == 1) return sg_launch<__nv_bfloat16, 1>(A, s);
@@ -436,6 +611,7 @@ static int fill_group(SgGroup& G, const mobile_sg_group* in, int w_dtype) {
   G.out_dim = in->epi == kEpiSwiglu ? in->rows / 2 : in->rows;
   G.out = in->out;
   G.residual = in->residual;
+  G.prefetch = in->prefetch;
   G.units = G.max_active * ((in->rows + kSgTileRows - 1) / kSgTileRows);
   return MOBILE_OK;
 }
@@ -475,6 +651,7 @@ extern "C" int mobile_stream_head(const float* x_ln, int T, int d, const void* w
   in.rows = V;
   in.out = logits_out;
   in.epi = kEpiHead;
+  in.prefetch = 1;
   if (int st = fill_group(A.g[0], &in, w_dtype)) return st;
   A.head.scale = logit_scale;
   A.head.gamma = gamma;
@@ -484,4 +661,24 @@ extern "C" int mobile_stream_head(const float* x_ln, int T, int d, const void* w
   A.head.ticket = reinterpret_cast<unsigned*>(workspace);
   A.head.partials = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + 256);
   return sg_dispatch(A, w_dtype, T, (cudaStream_t)stream);
+}
+
+extern "C" size_t mobile_down_combine_ws_bytes(void) { return 256; }
+
+extern "C" int mobile_down_combine(const mobile_sg_group* groups, int n_groups, int w_dtype, int max_tokens,
+                                   const float* x, const float* Y, const float* gates, const int* k_tok, int T,
+                                   int k_max, int d, const float* Y_shared, int n_shared,
+                                   const float* shared_logits, float* x_out, float* ln_out, void* workspace,
+                                   void* stream) {
+  if (n_groups < 1 || n_groups > kSgMaxGroups || T < 1 || d <= 0 || n_shared < 0 || !x_out) {
+    set_error("down_combine: bad arguments");
+    return MOBILE_ERR_INVALID;
+  }
+  SgArgs A{};
+  A.n_groups = n_groups;
+  for (int i = 0; i < n_groups; ++i)
+    if (int st = fill_group(A.g[i], &groups[i], w_dtype)) return st;
+  A.comb = SgCombine{x, Y, gates, k_tok, Y_shared, shared_logits, x_out, ln_out,
+                     reinterpret_cast<unsigned*>(workspace), T, d, k_max, Y_shared ? n_shared : 0};
+  return sg_dispatch(A, w_dtype, max_tokens, (cudaStream_t)stream);
 }

@@ -175,10 +175,14 @@ EPI_STORE, EPI_RELU, EPI_SWIGLU = 0, 1, 2
 
 
 def sg_group(*, w_base: int, K: int, rows: int, x, out, epi=EPI_STORE, stride=0, slot=None, x_div=1,
-             offsets=None, pairs=None, active=None, max_active=1, dense_T=0, residual=None):
+             offsets=None, pairs=None, active=None, max_active=1, dense_T=0, residual=None, prefetch=None):
+    """`prefetch` (default: dense groups) marks groups whose weights and expert
+    lists are static, so their copies may start before the PDL wait."""
+    if prefetch is None:
+        prefetch = offsets is None
     return N.mobile_sg_group(w_base, int(stride), N.ptr(slot), N.ptr(x), int(x_div), N.ptr(offsets), N.ptr(pairs),
                              N.ptr(active), int(dense_T), int(max_active), int(K), int(rows), N.ptr(out),
-                             N.ptr(residual), int(epi))
+                             N.ptr(residual), int(epi), int(bool(prefetch)))
 
 
 def stream_gemv(groups, w_dtype: int, max_tokens: int, stream=None):
@@ -256,3 +260,16 @@ def stream_head(x_ln, w_head, gamma, logit_scale, *, ws: StreamHeadWorkspace, lo
                                      float(gamma), N.ptr(logits_out), N.ptr(out["conf"]), N.ptr(out["argmax"]),
                                      N.ptr(out["fallback"]), N.ptr(ws.buf), _s(stream)), "stream_head")
     return out
+
+
+def down_combine(groups, w_dtype, max_tokens, x, Y, gates, k_tok, Y_shared, n_shared, shared_logits, x_out,
+                 ln_out, ws, stream=None):
+    """Down-projection launch whose last CTA also runs the combine (+LN)."""
+    arr = (N.mobile_sg_group * len(groups))(*groups)
+    T, d = x.shape
+    _count()
+    N.check(N.lib.mobile_down_combine(arr, len(groups), w_dtype, int(max_tokens), N.ptr(x), N.ptr(Y), N.ptr(gates),
+                                      N.ptr(k_tok), T, gates.shape[1], d, N.ptr(Y_shared), int(n_shared),
+                                      N.ptr(shared_logits), N.ptr(x_out), N.ptr(ln_out), N.ptr(ws), _s(stream)),
+            "down_combine")
+    return x_out

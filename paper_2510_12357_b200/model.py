@@ -36,6 +36,9 @@ _ACT = {"relu": N.ACT_RELU, "swiglu": N.ACT_SWIGLU}
 # expert FFN implementation: "stream" (bulk-copy TMA streaming, default) or
 # "warp" (register-streaming warp kernels); both are libmobile sm_100a kernels
 FFN_IMPL = os.environ.get("MOBILE_FFN", "stream")
+# fuse the combine into the down launch (last-CTA epilogue); measured slower
+# than the separate 1024-thread combine kernel at batch 1, so off by default
+FUSE_COMBINE = os.environ.get("MOBILE_FUSE_COMBINE", "0") == "1"
 _GATE = {"selected_softmax": N.GATE_SELECTED_SOFTMAX, "softmax_all": N.GATE_SOFTMAX_ALL}
 
 
@@ -45,6 +48,13 @@ def positional(n: int, d: int, start: int, device) -> torch.Tensor:
     dim = torch.arange(d, device=device, dtype=torch.float64)[None, :]
     angle = pos / torch.pow(torch.tensor(10000.0, dtype=torch.float64, device=device), (2 * (dim // 2)) / d)
     return torch.where(dim.long() % 2 == 0, torch.sin(angle), torch.cos(angle)).to(torch.float32)
+
+
+def pos_rows(spec: ModelSpec, n: int, start: int, device) -> torch.Tensor:
+    """Positional rows added to the embeddings (zeros for pos_encoding="none")."""
+    if spec.pos_encoding == "none":
+        return torch.zeros(n, spec.hidden_dim, device=device, dtype=torch.float32)
+    return positional(n, spec.hidden_dim, start, device)
 
 
 class ExpertLocation:
@@ -67,6 +77,8 @@ class MoBiLEMoE:
         self.act = _ACT[s.activation]
         self.gate_norm = _GATE[s.gate_norm]
         self._scratch: dict = {}
+        # ticket word of the fused down+combine launch (zeroed once, left zeroed)
+        self.comb_ws = torch.zeros(int(N.lib.mobile_down_combine_ws_bytes()), dtype=torch.uint8, device=dw.device)
 
     def resident(self, layer: int) -> ExpertLocation:
         dw = self.dw
@@ -148,21 +160,27 @@ class MoBiLEMoE:
         if self.S:
             base, sb = dw.shared[layer].data_ptr(), dw.shared_bytes
             rows13s = 2 * self.Is if self.act == N.ACT_SWIGLU else self.Is
-            g_up.append(K.sg_group(w_base=base, stride=sb, K=d, rows=rows13s, x=r["h2"], x_div=self.S,
-                                   offsets=sc["s_offsets"], pairs=sc["s_pairs"], active=sc["s_active"],
-                                   max_active=self.S, out=sc["Us"], epi=act_epi))
-            g_dn.append(K.sg_group(w_base=base + dw.s_w13_elems * dw.elem_bytes, stride=sb, K=self.Is, rows=d,
-                                   x=sc["Us"], offsets=sc["s_offsets"], pairs=sc["s_pairs"], active=sc["s_active"],
-                                   max_active=self.S, out=sc["Ys"]))
+            # shared experts first: their weights and (constant) pair lists are
+            # static, so their copies start before the PDL wait on the router
+            g_up.insert(0, K.sg_group(w_base=base, stride=sb, K=d, rows=rows13s, x=r["h2"], x_div=self.S,
+                                      offsets=sc["s_offsets"], pairs=sc["s_pairs"], active=sc["s_active"],
+                                      max_active=self.S, out=sc["Us"], epi=act_epi, prefetch=True))
+            g_dn.insert(0, K.sg_group(w_base=base + dw.s_w13_elems * dw.elem_bytes, stride=sb, K=self.Is, rows=d,
+                                      x=sc["Us"], offsets=sc["s_offsets"], pairs=sc["s_pairs"],
+                                      active=sc["s_active"], max_active=self.S, out=sc["Ys"], prefetch=True))
             Ys = sc["Ys"]
         if timer is not None:
             timer.start()
         K.stream_gemv(g_up, self.wcode, T)
         if timer is not None:
             timer.stop(("gate_up", T, k_max))
-        K.stream_gemv(g_dn, self.wcode, T)
         shared_logits = r["extra"] if dw.n_gate_rows else None
-        K.combine(x, sc["Y"], r["gates"], k_tok, Ys, self.S, shared_logits, x_out=sc["x_out"], ln_out=ln_out)
+        if FUSE_COMBINE and T <= 4:  # the down launch's last CTA runs the combine (+ LN for the next layer)
+            K.down_combine(g_dn, self.wcode, T, x, sc["Y"], r["gates"], k_tok, Ys, self.S, shared_logits,
+                           sc["x_out"], ln_out, self.comb_ws)
+        else:
+            K.stream_gemv(g_dn, self.wcode, T)
+            K.combine(x, sc["Y"], r["gates"], k_tok, Ys, self.S, shared_logits, x_out=sc["x_out"], ln_out=ln_out)
         return sc["x_out"]
 
     def _experts_warp(self, x, layer, sc, k_tok, k_max, loc, timer, ln_out):
@@ -271,7 +289,7 @@ class DeviceModel:
         dev = self.device
         n = len(tokens)
         tok = torch.as_tensor(np.asarray(tokens, dtype=np.int64)).to(dev)
-        x = dw.embed[tok] + positional(n, s.hidden_dim, 0, dev)
+        x = dw.embed[tok] + pos_rows(s, n, 0, dev)
         k_tok = torch.full((n,), k, dtype=torch.int32, device=dev)
         replay = mask = None
         if replay_states is not None:
@@ -350,7 +368,7 @@ class DecodeSession:
         dw, dev = m.dw, m.device
         Bn, n = tokens.shape
         pos = self.pos
-        x = dw.embed[tokens.reshape(-1)] + positional(n, s.hidden_dim, pos, dev).repeat(Bn, 1)
+        x = dw.embed[tokens.reshape(-1)] + pos_rows(s, n, pos, dev).repeat(Bn, 1)
         T = Bn * n
         states = torch.empty(s.num_layers, Bn, s.num_experts, device=dev, dtype=torch.float32)
         idx = torch.empty(s.num_layers, Bn, k_max, device=dev, dtype=torch.int32)

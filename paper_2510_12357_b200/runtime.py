@@ -30,7 +30,7 @@ import torch
 
 from . import _native as N
 from . import kernels as K
-from .model import DecodeSession, DeviceModel, positional
+from .model import DecodeSession, DeviceModel, pos_rows
 from .policy import plan_from_targets
 
 KINDS = ("little", "big", "full")
@@ -48,7 +48,7 @@ class StepEngine:
         L, E, d, B = s.num_layers, s.num_experts, s.hidden_dim, batch
         self.sess = DecodeSession(dm, batch, max_len)
         f32, i32 = torch.float32, torch.int32
-        self.pe = positional(max_len, d, 0, dev).contiguous()
+        self.pe = pos_rows(s, max_len, 0, dev).contiguous()
         self.tok = torch.zeros(B, dtype=i32, device=dev)
         self.pos = torch.zeros(B, dtype=i32, device=dev)
         self.tok_host = torch.zeros(B, dtype=i32, pin_memory=True)
@@ -178,7 +178,11 @@ class StepEngine:
         self._launch(self.run[kind])
 
     def pass_offload(self, kind: str):
-        """Drive the L+1 segments with the engine.py:121-169 protocol."""
+        """Drive the L+1 segments with the engine.py:121-169 protocol: in C++
+        (mobile_offload_run_pass) when the segments are captured graphs, else
+        from Python (eager mode, used for per-kernel instrumentation)."""
+        if self.use_graphs:
+            return self._pass_offload_native(kind)
         rt, L = self.rt, self.spec.num_layers
         segs = self.run[kind]
         row = 1 if kind == "big" else 0
@@ -219,6 +223,29 @@ class StepEngine:
             prev = experts
         self._launch(segs[L])  # (5) experts(L-1) + head
         self._release(L - 1, prev)
+
+    def _pass_offload_native(self, kind: str):
+        rt, s = self.rt, self.spec
+        L = s.num_layers
+        if not hasattr(self, "_execs"):
+            self._execs = {kd: (C.c_ulonglong * (L + 1))(*[self.graphs[(kd, l)].raw_cuda_graph_exec()
+                                                            for l in range(L + 1)]) for kd in KINDS}
+        row = 1 if kind == "big" else 0
+        planned = kind == "big"
+        targets = None
+        k = 0
+        if planned:
+            with torch.cuda.stream(self.stream):
+                idx, _ = K.topk_rows(self.states["little"][:, 0].contiguous(), s.k_big)
+                flat = idx.cpu().reshape(-1).tolist()  # one D2H for the whole planned pass
+            k = s.k_big
+            targets = (C.c_int * len(flat))(*flat)
+        fresh = C.c_int()
+        N.check(N.lib.mobile_offload_run_pass(
+            rt.h, self._execs[kind], L, self.stream.cuda_stream, int(planned),
+            None if planned else self.active_host.data_ptr(), targets, k, rt.slot_host[row].data_ptr(),
+            None, 0, rt.lookahead, C.byref(fresh)), "offload run_pass")
+        rt.fresh += fresh.value
 
     def _require(self, l, experts, row):
         rt = self.rt

@@ -73,3 +73,5 @@ def selections_agree(got, want, logits, tol=2e-5):
             return False, near
         near += 1
     return True, near
+
+QWEN_MINI_NOPE = dict(QWEN_MINI, embed_scale=1.0, pos_encoding="none", seed=9)
