@@ -149,9 +149,8 @@ int mobile_expert_down(const float* U, const int* offsets, const int* sorted_pai
 /* ---- bulk-copy streaming GEMV (decode engine) -----------------------------
  * One launch computes several groups of weight-row dot products, streaming
  * weights through shared memory with cp.async.bulk on an mbarrier ring.
- * Weights must be in the TILED layout: tiles of 16 rows x 4 KB of K
- * (2048 bf16 / 1024 f32 elements), contiguous in (row block, K chunk) order;
- * for K <= the chunk this is plain row-major (see weights.py tile_rows).
+ * Weights are row-major (out-major); rows are streamed in tiles of 16 rows x
+ * 4 KB of K (one contiguous copy when the row fits, else one copy per row).
  * Group semantics (per pair p of expert e, see mobile_expert_gate_up):
  *   epi 0 STORE : out[p, r] = (residual[p, r] +) x[p / x_div] . W_e[r]
  *   epi 1 RELU  : out[p, r] = max(x[p / x_div] . W_e[r], 0)
@@ -201,6 +200,28 @@ size_t mobile_stream_head_ws_bytes(void);
 int mobile_stream_head(const float* x_ln, int T, int d, const void* w_head, int w_dtype, int V,
                        float logit_scale, float gamma, float* logits_out, float* conf_out, int* argmax_out,
                        uint8_t* fallback_out, void* workspace, void* stream);
+
+/* ---- grouped expert GEMM on tcgen05 (prefill / batched) -------------------
+ * D_e = A_e . B_e^T, bf16 x bf16 -> f32 accumulate in TMEM, TMA-fed
+ * (SWIZZLE_128B, 4-stage mbarrier ring), one 128 x 128 tile per CTA.
+ *   A  (rows_a, K) bf16 row-major: expert-sorted activations; expert e owns
+ *      rows offsets[e]..offsets[e+1] (active = [n, ids]); with offsets NULL,
+ *      "dense" mode: each of dense_experts B experts sees rows 0..dense_rows.
+ *   B  expert weights (N, K) bf16 row-major at B_base + slot[e]*b_expert_stride
+ *      (n_slots experts addressable; slot NULL = identity).
+ *   epi 0: out_f32[row_to_pair[r] * ldo + e*out_expert_stride + n] = D (f32)
+ *   epi 1: SwiGLU on 16-column groups [8 gate | 8 up] -> bf16
+ *          out_bf16[r * ldo + e*out_expert_stride + f]
+ *   epi 2: bf16 store of D.
+ * K % 64 == 0, N % 128 == 0; max_tiles bounds the number of 128x128 tiles
+ * (surplus CTAs exit); the tile list is derived on the device. */
+int mobile_grouped_gemm(const void* A, int rows_a, int K, const void* B_base, long long b_expert_stride,
+                        int n_slots, int N, const int* offsets, const int* active, const int* slot, int max_tiles,
+                        int dense_rows, int dense_experts, int epi, float* out_f32, void* out_bf16, int ldo,
+                        int out_expert_stride, const int* row_to_pair, void* stream);
+/* X[r, :] = bf16(src[pairs[r] / div, :]) (pairs NULL: row r) -- the expert-
+ * sorted activation matrix for mobile_grouped_gemm. */
+int mobile_gather_bf16(const float* src, const int* pairs, int div, int P, int d, void* X, void* stream);
 
 /* ---- combine -------------------------------------------------------------
  * toymoe.py:192, 204, 207:  moe = sum_j gates[t,j] * Y[t*k_max + j] (selection

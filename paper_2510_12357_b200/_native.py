@@ -68,6 +68,8 @@ _SIGS = {
     "mobile_expert_gate_up": ([P, P, P, P, I32, I32, I32, I32, I32, P, I64, P, I32, I32, P, P], I32),
     "mobile_expert_down": ([P, P, P, P, I32, I32, I32, I32, P, I64, P, I32, P, P], I32),
     "mobile_combine": ([P, P, P, P, I32, I32, I32, P, I32, P, P, P, P], I32),
+    "mobile_grouped_gemm": ([P, I32, I32, P, I64, I32, I32, P, P, P, I32, I32, I32, I32, P, P, I32, I32, P, P], I32),
+    "mobile_gather_bf16": ([P, P, I32, I32, I32, P, P], I32),
     "mobile_stream_gemv": ([P, I32, I32, I32, P], I32),
     "mobile_stream_head_ws_bytes": ([], SZ),
     "mobile_down_combine_ws_bytes": ([], SZ),

@@ -1,0 +1,305 @@
+// Grouped expert GEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA)
+// for prefill / batched decode, where experts see many tokens and the expert
+// FFN becomes a dense contraction (SURVEY.md §2.3 `grouped_ffn_sm100`).
+//
+//   D_e[m, n] = sum_k A[row(e, m), k] * B_e[n, k]        (bf16 x bf16 -> f32)
+//
+// A is the expert-sorted (permuted) activation matrix (P x K bf16, rows of
+// expert e contiguous at offsets[e]..offsets[e+1]); B_e are the expert's
+// weight rows (out-major, K-major), addressed through a 3-D TMA map
+// (K, N, slot).  One CTA computes one 128 x 128 output tile:
+//   warp 0      TMA producer: A and B K-blocks of 64 (128 B, SWIZZLE_128B)
+//               into a 4-stage smem ring (full/empty mbarriers)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//               (4 x K=16 MMAs per stage, tcgen05.commit frees the stage)
+//   warps 2-5   epilogue: tcgen05.ld of the 128 x 128 f32 accumulator
+//               (warp w reads TMEM lanes 32*(w%4)..), then
+//                 SWIGLU: 16-column groups [8 gate | 8 up] -> silu(g)*u, bf16
+//                 STORE : f32, row scattered to its pair id (combine input)
+// Tiles are enumerated on the device from the expert offsets, so no host sync
+// is needed between routing and the GEMM; surplus CTAs exit.
+#include "common.cuh"
+#include "umma.cuh"
+
+namespace mobile {
+
+constexpr int kGgBM = 128, kGgBN = 128, kGgBK = 64;
+constexpr int kGgStages = 4;
+constexpr int kGgThreads = 192;
+constexpr int kGgABytes = kGgBM * kGgBK * 2;  // 16 KB
+constexpr int kGgBBytes = kGgBN * kGgBK * 2;  // 16 KB
+constexpr int kGgStageBytes = kGgABytes + kGgBBytes;
+
+enum GgEpi { kGgStoreF32Scatter = 0, kGgSwigluBf16 = 1, kGgStoreBf16 = 2 };
+
+struct GgArgs {
+  CUtensorMap tma_a;       // (K, rows_a)      box (64, 128)
+  CUtensorMap tma_b;       // (K, N, slots)    box (64, 128, 1)
+  const int* offsets;      // (E+1) row offsets of A per expert; NULL = dense
+  const int* active;       // [n, ids] (NULL = dense)
+  const int* slot;         // expert -> B slot (NULL = identity / dense expert index)
+  const int* row_to_pair;  // permuted row -> output row for STORE scatter (NULL = same row)
+  int dense_rows;          // dense: A rows (all experts see rows 0..dense_rows)
+  int dense_experts;       // dense: number of B experts (each gets all rows)
+  int K, N;
+  int epi;
+  float* out_f32;          // STORE: out_f32[(row_to_pair[r]) * ldo + n]
+  __nv_bfloat16* out_bf16; // SWIGLU / STORE bf16: out[r * ldo + col]
+  int ldo;
+  int out_expert_stride;   // dense experts: column offset of expert e in the output (elements)
+};
+
+struct GgTile {
+  int e, row0, nrows, n0, bslot;
+  bool valid;
+};
+
+// tile id -> (expert, m-tile, n-tile): experts in active order, m-tiles of an
+// expert consecutive, n fastest within an m-tile (consecutive CTAs share A).
+__device__ GgTile gg_tile(const GgArgs& a, int tile) {
+  GgTile t{};
+  const int nt = a.N / kGgBN;
+  if (!a.offsets) {
+    const int mt = (a.dense_rows + kGgBM - 1) / kGgBM;
+    const int per = mt * nt;
+    const int e = tile / per;
+    if (e >= a.dense_experts) return t;
+    const int r = tile - e * per;
+    t.e = e;
+    t.row0 = (r / nt) * kGgBM;
+    t.nrows = min(kGgBM, a.dense_rows - t.row0);
+    t.n0 = (r % nt) * kGgBN;
+    t.bslot = a.slot ? a.slot[e] : e;
+    t.valid = true;
+    return t;
+  }
+  const int na = a.active[0];
+  int base = 0;
+  for (int i = 0; i < na; ++i) {
+    const int e = a.active[1 + i];
+    const int off = a.offsets[e], n = a.offsets[e + 1] - off;
+    const int mt = (n + kGgBM - 1) / kGgBM;
+    if (tile < base + mt * nt) {
+      const int r = tile - base;
+      t.e = e;
+      t.row0 = off + (r / nt) * kGgBM;
+      t.nrows = min(kGgBM, off + n - t.row0);
+      t.n0 = (r % nt) * kGgBN;
+      t.bslot = a.slot ? a.slot[e] : e;
+      t.valid = true;
+      return t;
+    }
+    base += mt * nt;
+  }
+  return t;
+}
+
+__global__ void __launch_bounds__(kGgThreads, 1) grouped_gemm_kernel(const __grid_constant__ GgArgs a) {
+  extern __shared__ __align__(1024) uint8_t gsm[];
+  __shared__ __align__(8) uint64_t full[kGgStages], empty[kGgStages], done;
+  __shared__ uint32_t tmem_base;
+  __shared__ GgTile tile_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // 1024-byte aligned stage buffers (SWIZZLE_128B atoms)
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm) + 1023) & ~uintptr_t(1023));
+
+  if (tid == 0) {
+    umma::prefetch_tmap(&a.tma_a);
+    umma::prefetch_tmap(&a.tma_b);
+    for (int s = 0; s < kGgStages; ++s) {
+      umma::mbar_init(&full[s], 1);
+      umma::mbar_init(&empty[s], 1);
+    }
+    umma::mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) umma::tmem_alloc(&tmem_base, kGgBN);  // 128 f32 columns
+  pdl_trigger();
+  pdl_wait();
+  if (tid == 0) tile_s = gg_tile(a, blockIdx.x);
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const GgTile T = tile_s;
+  const uint32_t tmem = tmem_base;
+  const int nk = a.K / kGgBK;
+
+  if (T.valid) {
+    if (warp == 0 && lane == 0) {
+      // ---------------- TMA producer
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % kGgStages;
+        if (kb >= kGgStages) umma::mbar_wait(&empty[s], ((kb / kGgStages) - 1) & 1);
+        uint8_t* sa = base + (size_t)s * kGgStageBytes;
+        umma::mbar_expect_tx(&full[s], kGgStageBytes);
+        umma::tma_load_2d(sa, &a.tma_a, kb * kGgBK, T.row0, &full[s]);
+        umma::tma_load_3d(sa + kGgABytes, &a.tma_b, kb * kGgBK, T.n0, T.bslot, &full[s]);
+      }
+    } else if (warp == 1 && lane == 0) {
+      // ---------------- MMA issuer (one thread for the whole CTA)
+      constexpr uint32_t idesc = umma::idesc_bf16_f32(kGgBM, kGgBN);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % kGgStages;
+        umma::mbar_wait(&full[s], (kb / kGgStages) & 1);
+        umma::fence_after();
+        const uint8_t* sa = base + (size_t)s * kGgStageBytes;
+        const uint8_t* sb = sa + kGgABytes;
+#pragma unroll
+        for (int k = 0; k < kGgBK / 16; ++k) {
+          // advance the start address by 16 elements (32 B) inside the 128 B swizzle atom
+          umma::mma_bf16(tmem, umma::sdesc_sw128(sa + k * 32), umma::sdesc_sw128(sb + k * 32), idesc,
+                         (kb | k) != 0);
+        }
+        umma::mma_commit(&empty[s]);  // stage free once these MMAs have read it
+      }
+      umma::mma_commit(&done);  // accumulator complete
+    } else if (warp >= 2) {
+      // ---------------- epilogue: TMEM -> registers -> global
+      umma::mbar_wait(&done, 0);
+      umma::fence_after();
+      const int q = warp & 3;               // TMEM lane quarter this warp may read
+      const int r = q * 32 + lane;          // tile row = TMEM lane
+      const bool live = r < T.nrows;
+      const int row = T.row0 + r;           // row of A (permuted / dense)
+#pragma unroll 1
+      for (int c = 0; c < kGgBN / 16; ++c) {
+        float v[16];
+        umma::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 16), v);
+        if (!live) continue;
+        const int n = T.n0 + c * 16;
+        if (a.epi == kGgSwigluBf16) {
+          const int f0 = (n / 16) * 8;      // 8 features: cols 0-7 gate, 8-15 up
+          __nv_bfloat16* o = a.out_bf16 + (size_t)row * a.ldo + (size_t)T.e * a.out_expert_stride + f0;
+          uint4 pk;
+          uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float h0 = silu_f(v[2 * j]) * v[8 + 2 * j];
+            const float h1 = silu_f(v[2 * j + 1]) * v[8 + 2 * j + 1];
+            const __nv_bfloat162 b2 = __floats2bfloat162_rn(h0, h1);
+            pw[j] = *reinterpret_cast<const uint32_t*>(&b2);
+          }
+          *reinterpret_cast<uint4*>(o) = pk;
+        } else if (a.epi == kGgStoreF32Scatter) {
+          const int orow = a.row_to_pair ? a.row_to_pair[row] : row;
+          float* o = a.out_f32 + (size_t)orow * a.ldo + (size_t)T.e * a.out_expert_stride + n;
+#pragma unroll
+          for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        } else {
+          __nv_bfloat16* o = a.out_bf16 + (size_t)row * a.ldo + (size_t)T.e * a.out_expert_stride + n;
+#pragma unroll
+          for (int j = 0; j < 16; j += 2) {
+            const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[j], v[j + 1]);
+            *reinterpret_cast<__nv_bfloat162*>(o + j) = b2;
+          }
+        }
+      }
+    }
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    umma::fence_after();
+    umma::tmem_dealloc(tmem, kGgBN);
+  }
+}
+
+// activation gather: X[r, :] = bf16(src[row_to_src(r), :])
+__global__ void gather_bf16_kernel(const float* __restrict__ src, const int* __restrict__ pairs, int div, int P,
+                                   int d, __nv_bfloat16* __restrict__ X) {
+  pdl_trigger();
+  pdl_wait();
+  const int r = blockIdx.x;
+  if (r >= P) return;
+  const int srow = pairs ? pairs[r] / div : r;
+  const float* s = src + (size_t)srow * d;
+  __nv_bfloat16* o = X + (size_t)r * d;
+  for (int i = threadIdx.x * 2; i < d; i += blockDim.x * 2)
+    *reinterpret_cast<__nv_bfloat162*>(o + i) = __floats2bfloat162_rn(s[i], s[i + 1]);
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+static int make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                    const cuuint32_t* box) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) { set_error("cuTensorMapEncodeTiled unavailable"); return MOBILE_ERR_CUDA; }
+  const cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed (%d)", (int)r); return MOBILE_ERR_CUDA; }
+  return MOBILE_OK;
+}
+
+}  // namespace mobile
+
+using namespace mobile;
+
+extern "C" int mobile_grouped_gemm(const void* A, int rows_a, int K, const void* B_base, long long b_expert_stride,
+                                   int n_slots, int N, const int* offsets, const int* active, const int* slot,
+                                   int max_tiles, int dense_rows, int dense_experts, int epi, float* out_f32,
+                                   void* out_bf16, int ldo, int out_expert_stride, const int* row_to_pair,
+                                   void* stream) {
+  if (K <= 0 || K % kGgBK || N <= 0 || N % kGgBN || rows_a <= 0 || n_slots <= 0) {
+    set_error("grouped_gemm: K=%d must be a multiple of 64 and N=%d of 128", K, N);
+    return MOBILE_ERR_UNSUPPORTED;
+  }
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B_base) & 15) || (b_expert_stride & 15)) {
+    set_error("grouped_gemm: operands must be 16-byte aligned");
+    return MOBILE_ERR_INVALID;
+  }
+  GgArgs a{};
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows_a};
+    const cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+    const cuuint32_t box[2] = {kGgBK, kGgBM};
+    if (int st = make_map(&a.tma_a, A, 2, dims, strides, box)) return st;
+  }
+  {
+    const cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)N, (cuuint64_t)n_slots};
+    const cuuint64_t strides[2] = {(cuuint64_t)K * 2, (cuuint64_t)b_expert_stride};
+    const cuuint32_t box[3] = {kGgBK, kGgBN, 1};
+    if (int st = make_map(&a.tma_b, B_base, 3, dims, strides, box)) return st;
+  }
+  a.offsets = offsets;
+  a.active = active;
+  a.slot = slot;
+  a.row_to_pair = row_to_pair;
+  a.dense_rows = dense_rows;
+  a.dense_experts = dense_experts;
+  a.K = K;
+  a.N = N;
+  a.epi = epi;
+  a.out_f32 = out_f32;
+  a.out_bf16 = reinterpret_cast<__nv_bfloat16*>(out_bf16);
+  a.ldo = ldo;
+  a.out_expert_stride = out_expert_stride;
+  if (max_tiles <= 0) return MOBILE_OK;
+  const size_t smem = (size_t)kGgStages * kGgStageBytes + 1024;
+  if (int st = set_smem_once((const void*)grouped_gemm_kernel, smem)) return st;
+  return launch_pdl(grouped_gemm_kernel, dim3(max_tiles), dim3(kGgThreads), smem, (cudaStream_t)stream, 1,
+                    "grouped_gemm", a);
+}
+
+extern "C" int mobile_gather_bf16(const float* src, const int* pairs, int div, int P, int d, void* X, void* stream) {
+  if (P <= 0) return MOBILE_OK;
+  if (d % 2) { set_error("gather: d must be even"); return MOBILE_ERR_UNSUPPORTED; }
+  return launch_pdl(gather_bf16_kernel, dim3(P), dim3(256), 0, (cudaStream_t)stream, 1, "gather_bf16", src, pairs,
+                    div > 0 ? div : 1, P, d, reinterpret_cast<__nv_bfloat16*>(X));
+}

@@ -8,11 +8,9 @@
 // weight tile AND the matching activation slices (bulk-copied too), so the
 // consumers' inner loop reads shared memory only.
 //
-// Weights are stored TILED (see weights.py): a matrix of `rows` x K is cut
-// into tiles of 16 rows x 4 KB of K (2048 bf16 / 1024 f32) laid out
-// contiguously in (row block, K chunk) order -- for K <= the chunk this is
-// plain row-major.  One tile = one 64 KB bulk copy = one pipeline item, so the
-// copy engine sees a few large requests instead of many row-sized ones.
+// Weights are row-major.  A pipeline item is a tile of 16 rows x 4 KB of K
+// (2048 bf16 / 1024 f32): when a whole row fits the chunk the tile is one
+// contiguous bulk copy of up to 64 KB, otherwise 16 row copies.
 //
 // Warp 8 is the producer (one lane issues copies); warps 0-7 consume: warp w
 // owns rows {w, w+8} of every 16-row tile, so each output is one warp's
@@ -228,12 +226,17 @@ __device__ void sg_issue(const SgArgs& A, const SgIter<TT>& it, char* stage, uin
   const int s = it.slot;
   const int k0 = it.kc * KC;
   const int kn = min(KC, G.K - k0);
-  const size_t off = (size_t)it.rb * kSgTileRows * G.K + (size_t)k0 * it.rr;  // tiled layout
+  const char* rows = G.w_base + (long long)s * G.stride + (size_t)it.rb * kSgTileRows * G.K * sizeof(W);
   const uint32_t wbytes = (uint32_t)(it.rr * kn * sizeof(W));
   const int nt = min(TT, it.n - it.tc * TT);
   const uint32_t xbytes = (uint32_t)(kn * sizeof(float));
   mbar_expect_tx(bar, wbytes + nt * xbytes);
-  bulk_g2s(stage, G.w_base + (long long)s * G.stride + off * sizeof(W), wbytes, bar);
+  if (kn == G.K) {  // whole rows: one contiguous copy
+    bulk_g2s(stage, rows, wbytes, bar);
+  } else {
+    const uint32_t rb = (uint32_t)(kn * sizeof(W));
+    for (int r = 0; r < it.rr; ++r) bulk_g2s(stage + (size_t)r * rb, rows + ((size_t)r * G.K + k0) * sizeof(W), rb, bar);
+  }
   for (int t = 0; t < nt; ++t)  // activation slices x[row, k0:k0+kn]
     bulk_g2s(stage + kSgWBytes + (size_t)t * xbytes, G.x + (size_t)(it.pair[t] / G.x_div) * G.K + k0, xbytes, bar);
 }
@@ -248,8 +251,8 @@ __device__ void sg_prefetch(const SgArgs& A, const SgIter<TT>& it) {
   const SgGroup& G = A.g[it.g];
   const int k0 = it.kc * KC;
   const int kn = min(KC, G.K - k0);
-  const size_t off = (size_t)it.rb * kSgTileRows * G.K + (size_t)k0 * it.rr;
-  bulk_prefetch_l2(G.w_base + (long long)it.slot * G.stride + off * sizeof(W), (uint32_t)(it.rr * kn * sizeof(W)));
+  const char* rows = G.w_base + (long long)it.slot * G.stride + (size_t)it.rb * kSgTileRows * G.K * sizeof(W);
+  if (kn == G.K) bulk_prefetch_l2(rows, (uint32_t)(it.rr * kn * sizeof(W)));
 }
 
 __device__ __forceinline__ void online_add(float& m, float& s, int& arg, float l, int idx) {
@@ -302,11 +305,17 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
         while (npre < kSgStages && pre.valid) {
           const SgGroup& G = A.g[pre.g];
           const int k0 = pre.kc * KC, kn = min(KC, G.K - k0);
-          const size_t off = (size_t)pre.rb * kSgTileRows * G.K + (size_t)k0 * pre.rr;
+          const char* rows = G.w_base + (long long)pre.slot * G.stride + (size_t)pre.rb * kSgTileRows * G.K * sizeof(W);
           const uint32_t wbytes = (uint32_t)(pre.rr * kn * sizeof(W));
           mbar_expect_tx_only(&full[npre], wbytes);
-          bulk_g2s(smem + (size_t)npre * kSgStageBytes, G.w_base + (long long)pre.slot * G.stride + off * sizeof(W),
-                   wbytes, &full[npre]);
+          char* st = smem + (size_t)npre * kSgStageBytes;
+          if (kn == G.K) {
+            bulk_g2s(st, rows, wbytes, &full[npre]);
+          } else {
+            const uint32_t rbytes = (uint32_t)(kn * sizeof(W));
+            for (int r = 0; r < pre.rr; ++r)
+              bulk_g2s(st + (size_t)r * rbytes, rows + ((size_t)r * G.K + k0) * sizeof(W), rbytes, &full[npre]);
+          }
           ++npre;
           pre.next(A, KC);
         }

@@ -273,3 +273,30 @@ def down_combine(groups, w_dtype, max_tokens, x, Y, gates, k_tok, Y_shared, n_sh
                                       N.ptr(shared_logits), N.ptr(x_out), N.ptr(ln_out), N.ptr(ws), _s(stream)),
             "down_combine")
     return x_out
+
+
+GG_STORE_F32, GG_SWIGLU_BF16, GG_STORE_BF16 = 0, 1, 2
+
+
+def _gg_call(A, K, B_base, b_expert_stride, n_slots, n_cols, offsets, active, slot, max_tiles, dense_rows,
+             dense_experts, epi, out_f32, out_bf16, ldo, out_expert_stride, row_to_pair, stream):
+    N.check(N.lib.mobile_grouped_gemm(
+        N.ptr(A), A.shape[0], int(K), int(B_base), int(b_expert_stride), int(n_slots), int(n_cols), N.ptr(offsets),
+        N.ptr(active), N.ptr(slot), int(max_tiles), int(dense_rows), int(dense_experts), int(epi), N.ptr(out_f32),
+        N.ptr(out_bf16), int(ldo), int(out_expert_stride), N.ptr(row_to_pair), _s(stream)), "grouped_gemm")
+
+
+def grouped_gemm(A, K, B_base: int, b_expert_stride: int, n_slots: int, N_: int, *, offsets=None, active=None,
+                 slot=None, max_tiles: int, dense_rows=0, dense_experts=0, epi=GG_STORE_F32, out_f32=None,
+                 out_bf16=None, ldo=0, out_expert_stride=0, row_to_pair=None, stream=None):
+    """tcgen05 grouped GEMM (mobile_grouped_gemm)."""
+    _count()
+    _gg_call(A, K, B_base, b_expert_stride, n_slots, N_, offsets, active, slot, max_tiles, dense_rows, dense_experts,
+             epi, out_f32, out_bf16, ldo, out_expert_stride, row_to_pair, stream)
+
+
+def gather_bf16(src, pairs, div, P, X, stream=None):
+    _count()
+    N.check(N.lib.mobile_gather_bf16(N.ptr(src), N.ptr(pairs), int(div), int(P), src.shape[1], N.ptr(X), _s(stream)),
+            "gather_bf16")
+    return X

@@ -184,9 +184,6 @@ class MoBiLEMoE:
         return sc["x_out"]
 
     def _experts_warp(self, x, layer, sc, k_tok, k_max, loc, timer, ln_out):
-        from .weights import tile_chunk
-        if max(self.I, self.Is, self.d) > tile_chunk(self.dw.elem_bytes):
-            raise N.MobileNativeError("warp FFN kernels read row-major weights: K must fit one tile chunk")
         T = x.shape[0]
         dw, E, d = self.dw, self.E, self.d
         r, p = sc["router"], sc["perm"]

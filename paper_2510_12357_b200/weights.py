@@ -8,12 +8,11 @@ unchanged.  Large shapes (d=2048...) are generated directly on the device in
 device layout (same distribution, torch RNG) because a host fp64 draw of 14 B
 parameters is neither needed nor feasible.
 
-Device layout (all "out-major": rows = output features over the input dim),
-and TILED for the bulk-copy streaming engine (csrc/stream_gemv.cu): a
-(rows x K) matrix is stored as tiles of 16 rows x 4 KB of K (2048 bf16 /
-1024 f32 elements), contiguous in (row block, K chunk) order, so every
-pipeline item is one contiguous 64 KB copy.  For K <= that chunk (every
-d=2048 bf16 matrix except the 5632-wide shared W2) tiled == row-major.
+Device layout (all "out-major": rows = output features over the input dim,
+row-major), shared by the bulk-copy streaming engine (decode; a 16-row tile
+is one contiguous copy whenever the row fits a 4 KB K chunk, else 16 row
+copies) and the tcgen05 grouped GEMM (prefill; 2-D/3-D TMA maps over the
+same rows).
   router   (L, E + S_gate, d)   rows E.. = Qwen-style sigmoid shared-gate rows
   experts  (L, E, P)            packed per expert: W13 then W2, where
            W13 = (2I, d) SwiGLU gate/up rows interleaved in groups of 8+8
@@ -102,54 +101,8 @@ def init_host_weights(spec: ModelSpec) -> HostWeights:
     return hw
 
 
-TILE_ROWS = 16
-TILE_ROW_BYTES = 4096
-
-
-def tile_chunk(elem_size: int) -> int:
-    return TILE_ROW_BYTES // elem_size
-
-
-def tile_rows(m: torch.Tensor) -> torch.Tensor:
-    """(..., N, K) -> (..., N*K) in the tiled layout (identity when K <= chunk)."""
-    *lead, N, K = m.shape
-    KC = tile_chunk(m.element_size())
-    if K <= KC:
-        return m.reshape(*lead, N * K)
-    chunks = [(k0, min(KC, K - k0)) for k0 in range(0, K, KC)]
-    nfull = N // TILE_ROWS
-    tail = N - nfull * TILE_ROWS
-    parts = []
-    if nfull:
-        mf = m[..., :nfull * TILE_ROWS, :].reshape(*lead, nfull, TILE_ROWS, K)
-        blocks = torch.cat([mf[..., k0:k0 + kn].reshape(*lead, nfull, TILE_ROWS * kn) for k0, kn in chunks], dim=-1)
-        parts.append(blocks.reshape(*lead, nfull * TILE_ROWS * K))
-    if tail:
-        mt = m[..., nfull * TILE_ROWS:, :]
-        parts.append(torch.cat([mt[..., k0:k0 + kn].reshape(*lead, tail * kn) for k0, kn in chunks], dim=-1))
-    return torch.cat(parts, dim=-1)
-
-
-def untile_rows(flat: torch.Tensor, N: int, K: int) -> torch.Tensor:
-    """Inverse of tile_rows for one matrix: (N*K,) -> (N, K)."""
-    KC = tile_chunk(flat.element_size())
-    if K <= KC:
-        return flat.reshape(N, K)
-    out = torch.empty(N, K, dtype=flat.dtype, device=flat.device)
-    pos = 0
-    for r0 in range(0, N, TILE_ROWS):
-        rr = min(TILE_ROWS, N - r0)
-        for k0 in range(0, K, KC):
-            kn = min(KC, K - k0)
-            out[r0:r0 + rr, k0:k0 + kn] = flat[pos:pos + rr * kn].reshape(rr, kn)
-            pos += rr * kn
-    return out
-
-
 def pack_experts(w_in: torch.Tensor, w_up: torch.Tensor | None, w_out: torch.Tensor) -> torch.Tensor:
-    """(..., d, I), (..., d, I), (..., I, d) reference layout -> (..., P) packed tiled layout.
-
-    Convert to the storage dtype BEFORE packing: the tile chunk depends on it."""
+    """(..., d, I), (..., d, I), (..., I, d) reference layout -> (..., P) packed device layout."""
     lead = w_in.shape[:-2]
     d, I = w_in.shape[-2], w_in.shape[-1]
     w1t = w_in.transpose(-1, -2)  # (..., I, d)
@@ -162,7 +115,7 @@ def pack_experts(w_in: torch.Tensor, w_up: torch.Tensor | None, w_out: torch.Ten
     else:
         w13 = w1t
     w2t = w_out.transpose(-1, -2)  # (..., d, I)
-    return torch.cat([tile_rows(w13.contiguous()), tile_rows(w2t.contiguous())], dim=-1).contiguous()
+    return torch.cat([w13.contiguous().reshape(*lead, -1), w2t.contiguous().reshape(*lead, -1)], dim=-1).contiguous()
 
 
 class DeviceWeights:
@@ -201,9 +154,8 @@ class DeviceWeights:
 
         dw.embed = T(hw.embed, torch.float32)
         tr = lambda a: np.transpose(a, (0, 2, 1))  # noqa: E731  (L, in, out) -> (L, out, in)
-        dw.qkv = tile_rows(T(np.concatenate([tr(hw.attn_q), tr(hw.attn_k), tr(hw.attn_v)], axis=1))).reshape(
-            spec.num_layers, 3 * spec.hidden_dim, spec.hidden_dim)
-        dw.o = tile_rows(T(tr(hw.attn_o))).reshape(spec.num_layers, spec.hidden_dim, spec.hidden_dim)
+        dw.qkv = T(np.concatenate([tr(hw.attn_q), tr(hw.attn_k), tr(hw.attn_v)], axis=1))
+        dw.o = T(tr(hw.attn_o))
         rt = np.transpose(hw.router, (0, 2, 1))  # (L, E, d)
         if dw.n_gate_rows:
             rt = np.concatenate([rt, np.transpose(hw.shared_gate_w, (0, 2, 1))], axis=1)
@@ -217,15 +169,12 @@ class DeviceWeights:
         if spec.n_shared:
             sp = pack_experts(tt(hw.shared_in), tt(hw.shared_up), tt(hw.shared_out))
             dw.shared = sp.to(device=dev, dtype=wt)
-        dw.head = tile_rows(T(np.ascontiguousarray(hw.head.T))).reshape(spec.vocab_size, spec.hidden_dim)
+        dw.head = T(np.ascontiguousarray(hw.head.T))
         return dw
 
     def plain(self, w: torch.Tensor) -> torch.Tensor:
-        """Row-major view of a tiled (N, K) matrix (identity when K <= chunk)."""
-        N, K = w.shape
-        if K <= tile_chunk(w.element_size()):
-            return w
-        return untile_rows(w.reshape(-1), N, K)
+        """Row-major (N, K) view of a weight (the device layout is row-major)."""
+        return w
 
     @classmethod
     def random(cls, spec: ModelSpec, device, seed: int = 0, experts_on_device=True) -> "DeviceWeights":

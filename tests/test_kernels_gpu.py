@@ -237,9 +237,8 @@ def test_stream_gemv_dense(dev, wdt, T, K_, N_):
         w = round_bf16(w)
     x = rng.normal(size=(T, K_)).astype(np.float32)
     res = rng.normal(size=(T, N_)).astype(np.float32)
-    from paper_2510_12357_b200.weights import tile_rows
     tdt = torch.bfloat16 if wdt == "bfloat16" else torch.float32
-    wt = tile_rows(torch.tensor(w, device=dev, dtype=tdt))  # tiled layout (identity for K <= chunk)
+    wt = torch.tensor(w, device=dev, dtype=tdt)
     out = torch.empty(T, N_, device=dev)
     xt, rt = torch.tensor(x, device=dev), torch.tensor(res, device=dev)
     K.stream_gemv([K.sg_group(w_base=wt.data_ptr(), K=K_, rows=N_, x=xt, dense_T=T, out=out, residual=rt)],
@@ -276,7 +275,6 @@ def test_router_fused_permute(dev, T, k):
 def test_stream_head(dev, wdt, T, d, V):
     """Head + confidence on the bulk-copy engine vs the oracle (toymoe.py:209-210, policy.py:69-79)."""
     from paper_2510_12357_b200 import kernels as K
-    from paper_2510_12357_b200.weights import tile_rows
     rng = np.random.default_rng(d + V + T)
     head = rng.uniform(-1, 1, size=(d, V)) / np.sqrt(d)
     if wdt == "bfloat16":
@@ -284,7 +282,7 @@ def test_stream_head(dev, wdt, T, d, V):
     x = rng.normal(size=(T, d))
     xln = R.layer_norm(x).astype(np.float32)
     tdt = torch.bfloat16 if wdt == "bfloat16" else torch.float32
-    wt = tile_rows(torch.tensor(head.T.copy(), device=dev, dtype=tdt)).reshape(V, d)
+    wt = torch.tensor(head.T.copy(), device=dev, dtype=tdt)
     ws = K.StreamHeadWorkspace(dev)
     logits = torch.empty(T, V, device=dev)
     for gamma in (0.0, 0.3, 1.0):
@@ -298,6 +296,6 @@ def test_stream_head(dev, wdt, T, d, V):
             assert bool(out["fallback"][t].item()) == (out["conf"][t].item() <= gamma)
     # ties: identical rows -> first index wins
     w2 = torch.zeros(V, d, device=dev, dtype=tdt)
-    out = K.stream_head(torch.tensor(xln, device=dev), tile_rows(w2).reshape(V, d), 0.5, 24.0, ws=ws)
+    out = K.stream_head(torch.tensor(xln, device=dev), w2, 0.5, 24.0, ws=ws)
     assert out["argmax"].tolist() == [0] * T
     assert abs(out["conf"][0].item() - 1.0 / V) < 1e-6

@@ -72,22 +72,3 @@ def test_on_demand_plan():
     assert plan.targets[0] == [ExpertId(0, 1)]
     with pytest.raises(ValueError, match="layer 1"):
         on_demand_selection([[ExpertId(0, 0)], []])
-
-
-
-def test_tile_untile_roundtrip():
-    """Tiled weight layout (16 rows x 4 KB chunks) round-trips; identity for short K."""
-    import torch
-    from paper_2510_12357_b200.weights import tile_rows, untile_rows
-    for dt in (torch.float32, torch.bfloat16):
-        for N, K in ((48, 64), (37, 5632), (2048, 1408), (16, 4096), (33, 2049 * 4)):
-            m = torch.arange(N * K, dtype=torch.float32).reshape(N, K).to(dt)
-            t = tile_rows(m)
-            assert t.numel() == N * K
-            assert torch.equal(untile_rows(t, N, K), m)
-            KC = 4096 // m.element_size()
-            if K <= KC:
-                assert torch.equal(t, m.reshape(-1))
-            else:  # first tile = rows 0..15 x first chunk, contiguous
-                rr = min(16, N)
-                assert torch.equal(t[:rr * KC].reshape(rr, KC), m[:rr, :KC])
