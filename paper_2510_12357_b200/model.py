@@ -39,6 +39,8 @@ FFN_IMPL = os.environ.get("MOBILE_FFN", "stream")
 # fuse the combine into the down launch (last-CTA epilogue); measured slower
 # than the separate 1024-thread combine kernel at batch 1, so off by default
 FUSE_COMBINE = os.environ.get("MOBILE_FUSE_COMBINE", "0") == "1"
+# prefill / batched (T > TC_MIN_TOKENS): grouped expert GEMM on tcgen05 tensor cores
+TC_MIN_TOKENS = int(os.environ.get("MOBILE_TC_MIN_TOKENS", "5"))
 _GATE = {"selected_softmax": N.GATE_SELECTED_SOFTMAX, "softmax_all": N.GATE_SOFTMAX_ALL}
 
 
@@ -58,10 +60,12 @@ def pos_rows(spec: ModelSpec, n: int, start: int, device) -> torch.Tensor:
 
 
 class ExpertLocation:
-    """Where a layer's routed experts live: resident tensor or cache slot pool."""
+    """Where a layer's routed experts live: resident tensor or cache slot pool
+    (`n_slots` = experts addressable from the base, for TMA maps)."""
 
-    def __init__(self, w13_base: int, w2_base: int, stride: int, slot: torch.Tensor | None):
+    def __init__(self, w13_base: int, w2_base: int, stride: int, slot: torch.Tensor | None, n_slots: int = 0):
         self.w13_base, self.w2_base, self.stride, self.slot = w13_base, w2_base, stride, slot
+        self.n_slots = n_slots
 
 
 class MoBiLEMoE:
@@ -83,7 +87,7 @@ class MoBiLEMoE:
     def resident(self, layer: int) -> ExpertLocation:
         dw = self.dw
         base = dw.experts[layer].data_ptr()
-        return ExpertLocation(base, base + dw.w13_elems * dw.elem_bytes, dw.expert_bytes, None)
+        return ExpertLocation(base, base + dw.w13_elems * dw.elem_bytes, dw.expert_bytes, None, self.E)
 
     def scratch(self, T: int, k_max: int) -> dict:
         key = (T, k_max)
@@ -98,7 +102,7 @@ class MoBiLEMoE:
                         extra=torch.empty(T, ne, device=dev, dtype=f32), idx=torch.empty(T, k_max, device=dev, dtype=i32),
                         gates=torch.empty(T, k_max, device=dev, dtype=f32), flags=torch.zeros(1, device=dev, dtype=i32)),
             perm=dict(offsets=torch.empty(E + 1, device=dev, dtype=i32),
-                      sorted_pairs=torch.empty(T * k_max, device=dev, dtype=i32),
+                      sorted_pairs=torch.zeros(T * k_max, device=dev, dtype=i32),  # tail stays a valid index
                       active=torch.empty(E + 1, device=dev, dtype=i32)),
             U=torch.empty(T * k_max, self.I, device=dev, dtype=f32),
             Y=torch.empty(T * k_max, d, device=dev, dtype=f32),
@@ -148,6 +152,8 @@ class MoBiLEMoE:
         max_active = min(E, T * k_max)
         if FFN_IMPL == "warp":
             return self._experts_warp(x, layer, sc, k_tok, k_max, loc, timer, ln_out)
+        if T >= TC_MIN_TOKENS and self.tc_ok and FFN_IMPL != "stream_only":
+            return self._experts_tc(x, layer, sc, k_tok, k_max, loc, ln_out)
         act_epi = K.EPI_SWIGLU if self.act == N.ACT_SWIGLU else K.EPI_RELU
         rows13 = 2 * self.I if self.act == N.ACT_SWIGLU else self.I
         g_up = [K.sg_group(w_base=loc.w13_base, stride=loc.stride, slot=loc.slot, K=d, rows=rows13, x=r["h2"],
@@ -181,6 +187,61 @@ class MoBiLEMoE:
         else:
             K.stream_gemv(g_dn, self.wcode, T)
             K.combine(x, sc["Y"], r["gates"], k_tok, Ys, self.S, shared_logits, x_out=sc["x_out"], ln_out=ln_out)
+        return sc["x_out"]
+
+    @property
+    def tc_ok(self) -> bool:
+        """Shapes/dtype the tcgen05 grouped GEMM supports (bf16, K % 64, N % 128)."""
+        d, I, Is = self.d, self.I, self.Is
+        return (self.dw.wdtype == torch.bfloat16 and self.act == N.ACT_SWIGLU and d % 128 == 0
+                and I % 64 == 0 and (2 * I) % 128 == 0 and (not self.S or (Is % 64 == 0 and (2 * Is) % 128 == 0)))
+
+    def _tc_scratch(self, sc: dict, T: int, k_max: int) -> dict:
+        tc = sc.get("tc")
+        if tc is None:
+            dev, d = self.dw.device, self.d
+            P = T * k_max
+            bf = torch.bfloat16
+            tc = dict(X=torch.empty(P, d, device=dev, dtype=bf), U=torch.empty(P, self.I, device=dev, dtype=bf))
+            if self.S:
+                tc["Xs"] = torch.empty(T, d, device=dev, dtype=bf)
+                tc["Us"] = torch.empty(T, self.Is, device=dev, dtype=bf)
+                tc["s_rows"] = [(torch.arange(T, device=dev, dtype=torch.int32) * self.S + s).contiguous()
+                                for s in range(self.S)]
+            sc["tc"] = tc
+            self._scratch[(T, k_max)]["tc"] = tc
+        return tc
+
+    def _experts_tc(self, x, layer, sc, k_tok, k_max, loc, ln_out):
+        """Prefill / batched experts: gather -> tcgen05 gate-up (SwiGLU) -> tcgen05 down (scatter to pairs)."""
+        T = x.shape[0]
+        dw, E, d, I = self.dw, self.E, self.d, self.I
+        r, p = sc["router"], sc["perm"]
+        tc = self._tc_scratch(sc, T, k_max)
+        P = T * k_max
+        bound = (P + 127) // 128 + min(E, P)
+        n_slots = loc.n_slots or E
+        K.gather_bf16(r["h2"], p["sorted_pairs"], k_max, P, tc["X"])
+        K.grouped_gemm(tc["X"], d, loc.w13_base, loc.stride, n_slots, 2 * I, offsets=p["offsets"], active=p["active"],
+                       slot=loc.slot, max_tiles=bound * (2 * I // 128), epi=K.GG_SWIGLU_BF16, out_bf16=tc["U"], ldo=I)
+        K.grouped_gemm(tc["U"], I, loc.w2_base, loc.stride, n_slots, d, offsets=p["offsets"], active=p["active"],
+                       slot=loc.slot, max_tiles=bound * (d // 128), epi=K.GG_STORE_F32, out_f32=sc["Y"], ldo=d,
+                       row_to_pair=p["sorted_pairs"])
+        Ys = None
+        if self.S:
+            Is = self.Is
+            K.gather_bf16(r["h2"], None, 1, T, tc["Xs"])
+            mt = (T + 127) // 128
+            for s_ in range(self.S):
+                base = dw.shared[layer, s_].data_ptr()
+                K.grouped_gemm(tc["Xs"], d, base, dw.shared_bytes, 1, 2 * Is, max_tiles=mt * (2 * Is // 128),
+                               dense_rows=T, dense_experts=1, epi=K.GG_SWIGLU_BF16, out_bf16=tc["Us"], ldo=Is)
+                K.grouped_gemm(tc["Us"], Is, base + dw.s_w13_elems * dw.elem_bytes, dw.shared_bytes, 1, d,
+                               max_tiles=mt * (d // 128), dense_rows=T, dense_experts=1, epi=K.GG_STORE_F32,
+                               out_f32=sc["Ys"], ldo=d, row_to_pair=tc["s_rows"][s_])
+            Ys = sc["Ys"]
+        shared_logits = r["extra"] if dw.n_gate_rows else None
+        K.combine(x, sc["Y"], r["gates"], k_tok, Ys, self.S, shared_logits, x_out=sc["x_out"], ln_out=ln_out)
         return sc["x_out"]
 
     def _experts_warp(self, x, layer, sc, k_tok, k_max, loc, timer, ln_out):

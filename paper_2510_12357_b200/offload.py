@@ -70,7 +70,7 @@ class OffloadRuntime:
     # ------------------------------------------------------------- runtime ops
     def _location(self, layer: int, row: int) -> ExpertLocation:
         base = self.pool.data_ptr()
-        return ExpertLocation(base, base + self.w13_bytes, self.dw.expert_bytes, self.slot_dev[row, layer])
+        return ExpertLocation(base, base + self.w13_bytes, self.dw.expert_bytes, self.slot_dev[row, layer], self.slots)
 
     def _require(self, layer: int, experts: list[int], row: int) -> ExpertLocation:
         arr = (C.c_int * len(experts))(*experts)

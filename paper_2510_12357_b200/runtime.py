@@ -104,7 +104,7 @@ class StepEngine:
         s = self.spec
         K.stream_head(self.ln, self.dm.dw.head, self._gamma, s.logit_scale, ws=self.head_ws, out=self.head[kind])
 
-    def _offload_loc(self, l: int, kind: str):
+    def _offload_loc(self, l: int, kind: str):  # noqa: D401
         row = 1 if kind == "big" else 0
         return self.rt._location(l, row), row
 
