@@ -36,9 +36,6 @@ _ACT = {"relu": N.ACT_RELU, "swiglu": N.ACT_SWIGLU}
 # expert FFN implementation: "stream" (bulk-copy TMA streaming, default) or
 # "warp" (register-streaming warp kernels); both are libmobile sm_100a kernels
 FFN_IMPL = os.environ.get("MOBILE_FFN", "stream")
-# fuse the combine into the down launch (last-CTA epilogue); measured slower
-# than the separate 1024-thread combine kernel at batch 1, so off by default
-FUSE_COMBINE = os.environ.get("MOBILE_FUSE_COMBINE", "0") == "1"
 # prefill / batched (T > TC_MIN_TOKENS): grouped expert GEMM on tcgen05 tensor cores
 TC_MIN_TOKENS = int(os.environ.get("MOBILE_TC_MIN_TOKENS", "5"))
 _GATE = {"selected_softmax": N.GATE_SELECTED_SOFTMAX, "softmax_all": N.GATE_SOFTMAX_ALL}
@@ -142,52 +139,54 @@ class MoBiLEMoE:
                 loc: ExpertLocation | None = None, timer=None, ln_out=None) -> torch.Tensor:
         """Grouped expert FFN + shared experts + combine/residual (toymoe.py:202-207).
 
-        Default path: two bulk-copy streaming launches (gate-up of routed +
-        shared experts, then down of both) and the combine.  FFN_IMPL="warp"
-        selects the register-streaming warp kernels (mobile_expert_gate_up/down)."""
+        Decode (T < TC_MIN_TOKENS): bulk-copy streaming GEMV launches (gate-up
+        of routed + shared experts in one launch, then down of both) and the
+        combine.  Prefill / batched: the tcgen05 grouped GEMM.
+        FFN_IMPL="warp" selects the register-streaming warp kernels."""
         T = x.shape[0]
-        dw, E, d = self.dw, self.E, self.d
-        r, p = sc["router"], sc["perm"]
         loc = loc if loc is not None else self.resident(layer)
-        max_active = min(E, T * k_max)
         if FFN_IMPL == "warp":
             return self._experts_warp(x, layer, sc, k_tok, k_max, loc, timer, ln_out)
+        r = sc["router"]
         if T >= TC_MIN_TOKENS and self.tc_ok and FFN_IMPL != "stream_only":
-            return self._experts_tc(x, layer, sc, k_tok, k_max, loc, ln_out)
+            self._routed_tc(r["h2"], sc["perm"], T, k_max, loc, sc)
+            Ys = self._shared_tc(r["h2"], layer, T, sc) if self.S else None
+        else:
+            self._stream_ffn(r["h2"], sc["perm"], layer, T, k_max, loc, sc, timer)
+            Ys = sc["Ys"] if self.S else None
+        shared_logits = r["extra"] if self.dw.n_gate_rows else None
+        K.combine(x, sc["Y"], r["gates"], k_tok, Ys, self.S, shared_logits, x_out=sc["x_out"], ln_out=ln_out)
+        return sc["x_out"]
+
+    def _stream_ffn(self, h2, p, layer, T, k_max, loc, sc, timer=None, shared=True):
+        """Decode FFN on the bulk-copy engine: writes sc["Y"] (and sc["Ys"])."""
+        dw, E, d = self.dw, self.E, self.d
+        max_active = min(E, T * k_max)
         act_epi = K.EPI_SWIGLU if self.act == N.ACT_SWIGLU else K.EPI_RELU
         rows13 = 2 * self.I if self.act == N.ACT_SWIGLU else self.I
-        g_up = [K.sg_group(w_base=loc.w13_base, stride=loc.stride, slot=loc.slot, K=d, rows=rows13, x=r["h2"],
+        g_up = [K.sg_group(w_base=loc.w13_base, stride=loc.stride, slot=loc.slot, K=d, rows=rows13, x=h2,
                            x_div=k_max, offsets=p["offsets"], pairs=p["sorted_pairs"], active=p["active"],
                            max_active=max_active, out=sc["U"], epi=act_epi)]
         g_dn = [K.sg_group(w_base=loc.w2_base, stride=loc.stride, slot=loc.slot, K=self.I, rows=d, x=sc["U"],
                            offsets=p["offsets"], pairs=p["sorted_pairs"], active=p["active"],
                            max_active=max_active, out=sc["Y"])]
-        Ys = None
-        if self.S:
+        if self.S and shared:
             base, sb = dw.shared[layer].data_ptr(), dw.shared_bytes
             rows13s = 2 * self.Is if self.act == N.ACT_SWIGLU else self.Is
             # shared experts first: their weights and (constant) pair lists are
             # static, so their copies start before the PDL wait on the router
-            g_up.insert(0, K.sg_group(w_base=base, stride=sb, K=d, rows=rows13s, x=r["h2"], x_div=self.S,
+            g_up.insert(0, K.sg_group(w_base=base, stride=sb, K=d, rows=rows13s, x=h2, x_div=self.S,
                                       offsets=sc["s_offsets"], pairs=sc["s_pairs"], active=sc["s_active"],
                                       max_active=self.S, out=sc["Us"], epi=act_epi, prefetch=True))
             g_dn.insert(0, K.sg_group(w_base=base + dw.s_w13_elems * dw.elem_bytes, stride=sb, K=self.Is, rows=d,
                                       x=sc["Us"], offsets=sc["s_offsets"], pairs=sc["s_pairs"],
                                       active=sc["s_active"], max_active=self.S, out=sc["Ys"], prefetch=True))
-            Ys = sc["Ys"]
         if timer is not None:
             timer.start()
         K.stream_gemv(g_up, self.wcode, T)
         if timer is not None:
             timer.stop(("gate_up", T, k_max))
-        shared_logits = r["extra"] if dw.n_gate_rows else None
-        if FUSE_COMBINE and T <= 4:  # the down launch's last CTA runs the combine (+ LN for the next layer)
-            K.down_combine(g_dn, self.wcode, T, x, sc["Y"], r["gates"], k_tok, Ys, self.S, shared_logits,
-                           sc["x_out"], ln_out, self.comb_ws)
-        else:
-            K.stream_gemv(g_dn, self.wcode, T)
-            K.combine(x, sc["Y"], r["gates"], k_tok, Ys, self.S, shared_logits, x_out=sc["x_out"], ln_out=ln_out)
-        return sc["x_out"]
+        K.stream_gemv(g_dn, self.wcode, T)
 
     @property
     def tc_ok(self) -> bool:
@@ -197,7 +196,8 @@ class MoBiLEMoE:
                 and I % 64 == 0 and (2 * I) % 128 == 0 and (not self.S or (Is % 64 == 0 and (2 * Is) % 128 == 0)))
 
     def _tc_scratch(self, sc: dict, T: int, k_max: int) -> dict:
-        tc = sc.get("tc")
+        key = (T, k_max)
+        tc = self._scratch[key].get("tc")
         if tc is None:
             dev, d = self.dw.device, self.d
             P = T * k_max
@@ -208,41 +208,70 @@ class MoBiLEMoE:
                 tc["Us"] = torch.empty(T, self.Is, device=dev, dtype=bf)
                 tc["s_rows"] = [(torch.arange(T, device=dev, dtype=torch.int32) * self.S + s).contiguous()
                                 for s in range(self.S)]
-            sc["tc"] = tc
-            self._scratch[(T, k_max)]["tc"] = tc
+            self._scratch[key]["tc"] = tc
         return tc
 
-    def _experts_tc(self, x, layer, sc, k_tok, k_max, loc, ln_out):
-        """Prefill / batched experts: gather -> tcgen05 gate-up (SwiGLU) -> tcgen05 down (scatter to pairs)."""
-        T = x.shape[0]
-        dw, E, d, I = self.dw, self.E, self.d, self.I
-        r, p = sc["router"], sc["perm"]
+    def _routed_tc(self, h2, p, T, k_max, loc, sc):
+        """Routed experts on tcgen05: gather -> gate-up (SwiGLU) -> down (scatter to pairs) into sc["Y"]."""
+        E, d, I = self.E, self.d, self.I
         tc = self._tc_scratch(sc, T, k_max)
         P = T * k_max
         bound = (P + 127) // 128 + min(E, P)
         n_slots = loc.n_slots or E
-        K.gather_bf16(r["h2"], p["sorted_pairs"], k_max, P, tc["X"])
+        K.gather_bf16(h2, p["sorted_pairs"], k_max, P, tc["X"])
         K.grouped_gemm(tc["X"], d, loc.w13_base, loc.stride, n_slots, 2 * I, offsets=p["offsets"], active=p["active"],
                        slot=loc.slot, max_tiles=bound * (2 * I // 128), epi=K.GG_SWIGLU_BF16, out_bf16=tc["U"], ldo=I)
         K.grouped_gemm(tc["U"], I, loc.w2_base, loc.stride, n_slots, d, offsets=p["offsets"], active=p["active"],
                        slot=loc.slot, max_tiles=bound * (d // 128), epi=K.GG_STORE_F32, out_f32=sc["Y"], ldo=d,
                        row_to_pair=p["sorted_pairs"])
-        Ys = None
-        if self.S:
-            Is = self.Is
-            K.gather_bf16(r["h2"], None, 1, T, tc["Xs"])
-            mt = (T + 127) // 128
-            for s_ in range(self.S):
-                base = dw.shared[layer, s_].data_ptr()
-                K.grouped_gemm(tc["Xs"], d, base, dw.shared_bytes, 1, 2 * Is, max_tiles=mt * (2 * Is // 128),
-                               dense_rows=T, dense_experts=1, epi=K.GG_SWIGLU_BF16, out_bf16=tc["Us"], ldo=Is)
-                K.grouped_gemm(tc["Us"], Is, base + dw.s_w13_elems * dw.elem_bytes, dw.shared_bytes, 1, d,
-                               max_tiles=mt * (d // 128), dense_rows=T, dense_experts=1, epi=K.GG_STORE_F32,
-                               out_f32=sc["Ys"], ldo=d, row_to_pair=tc["s_rows"][s_])
-            Ys = sc["Ys"]
-        shared_logits = r["extra"] if dw.n_gate_rows else None
-        K.combine(x, sc["Y"], r["gates"], k_tok, Ys, self.S, shared_logits, x_out=sc["x_out"], ln_out=ln_out)
-        return sc["x_out"]
+
+    def _shared_tc(self, h2, layer, T, sc):
+        """Shared experts on tcgen05 (dense groups) into sc["Ys"] (T, S, d)."""
+        dw, d, Is = self.dw, self.d, self.Is
+        tc = self._tc_scratch(sc, T, sc["perm"]["sorted_pairs"].numel() // max(T, 1))
+        K.gather_bf16(h2, None, 1, T, tc["Xs"])
+        mt = (T + 127) // 128
+        for s_ in range(self.S):
+            base = dw.shared[layer, s_].data_ptr()
+            K.grouped_gemm(tc["Xs"], d, base, dw.shared_bytes, 1, 2 * Is, max_tiles=mt * (2 * Is // 128),
+                           dense_rows=T, dense_experts=1, epi=K.GG_SWIGLU_BF16, out_bf16=tc["Us"], ldo=Is)
+            K.grouped_gemm(tc["Us"], Is, base + dw.s_w13_elems * dw.elem_bytes, dw.shared_bytes, 1, d,
+                           max_tiles=mt * (d // 128), dense_rows=T, dense_experts=1, epi=K.GG_STORE_F32,
+                           out_f32=sc["Ys"], ldo=d, row_to_pair=tc["s_rows"][s_])
+        return sc["Ys"]
+
+    # ---- expert-parallel helpers (ep.py) ----
+    def rows_ffn(self, layer: int, rows: torch.Tensor, ids: torch.Tensor) -> torch.Tensor:
+        """Routed-expert FFN of R independent rows, row i through local expert ids[i] (k = 1)."""
+        R = rows.shape[0]
+        k_tok = torch.ones(R, dtype=torch.int32, device=rows.device)
+        sc = self.scratch(R, 1)
+        p = K.permute(ids.view(R, 1), k_tok, self.E, out=sc["perm"])
+        loc = self.resident(layer)
+        if R >= TC_MIN_TOKENS and self.tc_ok:
+            self._routed_tc(rows, p, R, 1, loc, sc)
+        else:
+            self._stream_ffn(rows, p, layer, R, 1, loc, sc, shared=False)
+        return sc["Y"][:R].clone()
+
+    def shared_rows(self, layer: int, h2: torch.Tensor, sc: dict) -> torch.Tensor:
+        """Shared-expert outputs (T, S, d) for the tokens of a routed scratch."""
+        T = h2.shape[0]
+        k_max = sc["perm"]["sorted_pairs"].numel() // max(T, 1)
+        if T >= TC_MIN_TOKENS and self.tc_ok:
+            return self._shared_tc(h2, layer, T, sc)
+        dw, d = self.dw, self.d
+        act_epi = K.EPI_SWIGLU if self.act == N.ACT_SWIGLU else K.EPI_RELU
+        base, sb = dw.shared[layer].data_ptr(), dw.shared_bytes
+        rows13s = 2 * self.Is if self.act == N.ACT_SWIGLU else self.Is
+        K.stream_gemv([K.sg_group(w_base=base, stride=sb, K=d, rows=rows13s, x=h2, x_div=self.S,
+                                  offsets=sc["s_offsets"], pairs=sc["s_pairs"], active=sc["s_active"],
+                                  max_active=self.S, out=sc["Us"], epi=act_epi, prefetch=True)], self.wcode, T)
+        K.stream_gemv([K.sg_group(w_base=base + dw.s_w13_elems * dw.elem_bytes, stride=sb, K=self.Is, rows=d,
+                                  x=sc["Us"], offsets=sc["s_offsets"], pairs=sc["s_pairs"], active=sc["s_active"],
+                                  max_active=self.S, out=sc["Ys"], prefetch=True)], self.wcode, T)
+        del k_max
+        return sc["Ys"]
 
     def _experts_warp(self, x, layer, sc, k_tok, k_max, loc, timer, ln_out):
         T = x.shape[0]

@@ -172,6 +172,17 @@ class DeviceWeights:
         dw.head = T(np.ascontiguousarray(hw.head.T))
         return dw
 
+    def shard_experts(self, lo: int, hi: int) -> "DeviceWeights":
+        """This rank's view for expert parallelism: routed experts [lo, hi),
+        everything else (router, shared experts, attention, head) shared."""
+        from dataclasses import replace
+        sub = DeviceWeights(replace(self.spec, num_experts=hi - lo, k_big=min(self.spec.k_big, hi - lo),
+                                    k_little=min(self.spec.k_little, hi - lo)), self.device, True)
+        for name in ("embed", "qkv", "o", "router", "shared", "head"):
+            setattr(sub, name, getattr(self, name))
+        sub.experts = self.experts[:, lo:hi]
+        return sub
+
     def plain(self, w: torch.Tensor) -> torch.Tensor:
         """Row-major (N, K) view of a weight (the device layout is row-major)."""
         return w
