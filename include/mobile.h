@@ -336,6 +336,66 @@ int mobile_offload_run_pass(mobile_offload* o, const unsigned long long* graph_e
 /* bytes copied H2D so far, transfers issued */
 int mobile_offload_counters(const mobile_offload* o, long long* out2);
 
+
+/* ---- persistent decode pass (decode_pass.cu) -------------------------------
+ * One launch runs a whole MoBiLE decode pass of B <= 4 sequences at one new
+ * position each -- embed, per layer [LN + qkv, KV-cache attention, o +
+ * residual, LN + router GEMV (+ shared-gate rows) + shared gate-up, stable
+ * top-k / replay / gate softmax + permute, routed gate-up, shared and routed
+ * down, weighted combine + residual], head + confidence -- i.e. one pass of
+ * toymoe.little_forward / big_forward / full_forward (toymoe.py:143-236) with
+ * a KV cache, on 148 persistent CTAs separated by grid barriers.  With
+ * `offload` set the pass is cut into L+1 segments after each layer's routing
+ * (the active expert list is published to active_out[l] for the host cache,
+ * engine.py:121-169), routed experts are read through slot_table (L, E).
+ * All pointers are device memory owned by the caller; the handle owns only
+ * its program and a small workspace.  `replay` (L, B, E) non-NULL = big pass
+ * (selection from the replayed logits, toymoe.py:194-200). */
+typedef struct mobile_dp_model {
+  int B, L, d, H, V, E, k, n_shared, n_gate, ffn, shared_ffn, activation, gate_norm, reuse_gates;
+  int w_dtype, max_len, offload;
+  float logit_scale, gamma;
+  /* weights (out-major, row-major rows) */
+  const void* qkv;            /* (L, 3d, d) */
+  const void* o;              /* (L, d, d) */
+  const void* router;         /* (L, E + n_gate, d) */
+  const void* shared;         /* (L, S, shared_stride bytes) packed [W13 | W2] */
+  long long shared_stride, shared_w2_offset;
+  const void* experts;        /* resident (L, E, expert_stride) or the offload slot pool */
+  long long expert_layer_stride, expert_stride, expert_w2_offset;
+  const int* slot_table;      /* (L, E) slot of each expert (offload) or NULL */
+  const void* head;           /* (V, d) */
+  const float* embed;         /* (V, d) f32 */
+  const float* pe;            /* (max_len, d) f32 positional rows */
+  /* state */
+  const int* tok;             /* (B,) input token */
+  const int* pos;             /* (B,) position */
+  float *kc, *vc;             /* (L, B, max_len, d) */
+  float *x, *xa, *q, *att;    /* (B, d) */
+  float *U, *Us, *Y, *Ys;     /* (B*k, ffn), (B*S, shared_ffn), (B*k, d), (B*S, d) */
+  float* states;              /* (L, B, E) router logits of this pass */
+  float* extra;               /* (L, B, max(n_gate,1)) shared-gate logits */
+  const float* replay;        /* (L, B, E) or NULL */
+  int* idx_out;               /* (L, B, k) selections */
+  float* gates_out;           /* (L, B, k) */
+  int* active_out;            /* (L, E + 1) [n, expert ids...] or NULL */
+  float* head_logits;         /* (B, V) or NULL */
+  float* conf;                /* (B,) max softmax prob */
+  int* argmax;                /* (B,) */
+  uint8_t* fallback;          /* (B,) conf <= gamma (policy.py:69-79) */
+  int* flags;                 /* |= 1 non-finite router logits, 4/8 watchdog */
+} mobile_dp_model;
+typedef struct mobile_dp mobile_dp;
+int mobile_dp_create(const mobile_dp_model* m, mobile_dp** out);
+void mobile_dp_destroy(mobile_dp* p);
+int mobile_dp_num_segments(const mobile_dp* p);
+int mobile_dp_info(const mobile_dp* p, int* out4); /* phases, stages, smem bytes, grid */
+/* optional device buffer (phases x grid x 3 u64): per phase and CTA the
+ * globaltimer at [barrier passed, inputs ready, work done]; NULL = off */
+int mobile_dp_set_trace(mobile_dp* p, unsigned long long* trace);
+/* segment = -1: the whole pass; else offload segment 0..L */
+int mobile_dp_launch(mobile_dp* p, int segment, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

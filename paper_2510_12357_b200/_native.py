@@ -41,6 +41,23 @@ class mobile_channel(C.Structure):
     _fields_ = [("t_xfer", C.c_double), ("busy_until", C.c_double), ("transfers_issued", C.c_longlong)]
 
 
+class mobile_dp_model(C.Structure):
+    """include/mobile.h mobile_dp_model (persistent decode pass)."""
+    _fields_ = [(n, C.c_int) for n in ("B", "L", "d", "H", "V", "E", "k", "n_shared", "n_gate", "ffn", "shared_ffn",
+                                       "activation", "gate_norm", "reuse_gates", "w_dtype", "max_len", "offload")] + [
+        ("logit_scale", C.c_float), ("gamma", C.c_float),
+        ("qkv", C.c_void_p), ("o", C.c_void_p), ("router", C.c_void_p), ("shared", C.c_void_p),
+        ("shared_stride", C.c_longlong), ("shared_w2_offset", C.c_longlong), ("experts", C.c_void_p),
+        ("expert_layer_stride", C.c_longlong), ("expert_stride", C.c_longlong), ("expert_w2_offset", C.c_longlong),
+        ("slot_table", C.c_void_p), ("head", C.c_void_p), ("embed", C.c_void_p), ("pe", C.c_void_p),
+        ("tok", C.c_void_p), ("pos", C.c_void_p), ("kc", C.c_void_p), ("vc", C.c_void_p),
+        ("x", C.c_void_p), ("xa", C.c_void_p), ("q", C.c_void_p), ("att", C.c_void_p),
+        ("U", C.c_void_p), ("Us", C.c_void_p), ("Y", C.c_void_p), ("Ys", C.c_void_p),
+        ("states", C.c_void_p), ("extra", C.c_void_p), ("replay", C.c_void_p), ("idx_out", C.c_void_p),
+        ("gates_out", C.c_void_p), ("active_out", C.c_void_p), ("head_logits", C.c_void_p), ("conf", C.c_void_p),
+        ("argmax", C.c_void_p), ("fallback", C.c_void_p), ("flags", C.c_void_p)]
+
+
 def _load():
     if not LIB_PATH.exists():
         raise ImportError(
@@ -103,6 +120,12 @@ _SIGS = {
     "mobile_offload_cache": ([P], P),
     "mobile_offload_counters": ([P, P], I32),
     "mobile_offload_run_pass": ([P, P, I32, P, I32, P, P, I32, P, P, I64, I32, P], I32),
+    "mobile_dp_create": ([P, P], I32),
+    "mobile_dp_destroy": ([P], None),
+    "mobile_dp_num_segments": ([P], I32),
+    "mobile_dp_info": ([P, P], I32),
+    "mobile_dp_launch": ([P, I32, P], I32),
+    "mobile_dp_set_trace": ([P, P], I32),
 }
 EXPORTED = tuple(_SIGS)
 for _name, (_args, _ret) in _SIGS.items():

@@ -1,0 +1,1328 @@
+// Persistent decode-pass kernel: one launch runs a whole MoBiLE decode pass
+// (or one offload segment of it) for B <= 4 sequences.
+//
+// Why: at batch 1 every decode matrix is HBM-streamed exactly once and is
+// small (8-70 MB, 1-10 us at roofline), so a kernel-per-op step loses most of
+// its time to launch ramp, pipeline fill and drain (measured: an isolated
+// 8 MB GEMV reaches 32% of HBM, 70 MB 57%, 2 GB 80%).  Here 148 CTAs (one per
+// SM) live for the whole pass; a producer warp per CTA streams every weight
+// tile the CTA will ever consume through one cp.async.bulk / mbarrier ring,
+// running ACROSS phase boundaries: weights of static matrices (attention
+// projections, router, shared experts, head) are in flight while the previous
+// phase is still computing, so the HBM stream does not drain at every op.
+// Phases are separated by grid barriers (an arrival counter in global
+// memory); only the data a phase produces (activations, routing) waits.
+//
+// A pass is a PROGRAM of phases: per layer (toymoe.py:171-207 with a KV cache)
+//   qkv     GEMV  x = LN(x_l) [embed (layer 0) / combine of layer l-1 fused
+//                 into the input build]; epilogue writes q and the new K/V rows
+//   attn    single-query attention, position-split, last-arriver merge
+//   o       GEMV  x = att, + residual -> xa
+//   router  GEMV  x = LN(xa): router logits (+ sigmoid shared-gate rows)
+//                 + shared-expert gate-up (SwiGLU)             (toymoe.py:188-190)
+//   [publish]     offload only: CTA 0 writes the layer's active expert list
+//   gu      routed gate-up (x = LN(xa)) + shared down; every CTA derives the
+//           selection itself from the logits: stable top-k / replay / gate
+//           softmax (toymoe.py:193-201) and the stable (expert, pair) permute
+//   down    routed down -> Y; the weighted combine + residual + LN is fused
+//           into the next layer's input build (toymoe.py:204, 207)
+// then the head (toymoe.py:209-210, 273; policy.py:69-79) with an online
+// max / sum-exp / first-argmax merge.  The program is a handful of per-layer
+// phase TEMPLATES held in the kernel's constant-bank parameter; a phase is
+// (template, layer) and every per-layer pointer is base + layer * stride, so
+// no descriptor is ever fetched from global memory.  Offloaded passes run the
+// same program in L+1 launches cut before each layer's routed experts
+// (engine.py:121-169: the host issues the copies in between).
+//
+// Consumer arithmetic: warp w owns a 256-element K slice of every row of a
+// 16-row weight tile (each weight and activation byte leaves shared memory
+// once); rows are reduced over lanes by a fixed butterfly and over warps in
+// warp order -- fixed-order fp32, no float atomics, deterministic and
+// independent of the grid size.
+#include "common.cuh"
+
+namespace mobile {
+namespace dp {
+
+constexpr int kCW = 8;                      // consumer warps
+constexpr int kThreads = (kCW + 1) * 32;    // + 1 producer warp
+constexpr int kTileRows = 16;
+constexpr int kChunk = 4096;                // bytes of K per tile row
+constexpr int kWBytes = kTileRows * kChunk; // 64 KB weight tile per stage
+constexpr int kMaxB = 4;
+constexpr int kMaxPairs = 32;
+constexpr int kMaxG = 3;
+constexpr int kMaxE = 256;
+constexpr int kMaxStages = 4;
+constexpr int kMaxGate = 4;                 // shared experts (and sigmoid gates) per layer
+constexpr int kMaxTmpl = 9;
+
+enum GroupKind { GK_DENSE = 0, GK_SHARED = 1, GK_ROUTED = 2 };
+enum Epi { EP_STORE = 0, EP_RELU = 1, EP_SWIGLU = 2, EP_QKV = 3, EP_LOGITS = 4, EP_HEAD = 5 };
+enum XKind { XK_NONE = 0, XK_LN = 1, XK_PLAIN = 2, XK_COMBINE_LN = 3, XK_EMBED_LN = 4 };
+enum PhaseType { PT_GEMV = 0, PT_ATTN = 1, PT_PUBLISH = 2 };
+
+struct Group {
+  const char* w;        // layer-0 matrix (dense) / expert 0 (shared, resident routed) / slot 0 (offload)
+  long long w_l;        // bytes per layer
+  long long stride;     // bytes between experts
+  const int* slot;      // routed: slot table (NULL = identity)
+  float* out;
+  long long out_l;      // floats per layer
+  float* out2;          // EP_LOGITS: rows >= split (shared-gate logits)
+  long long out2_l;
+  const float* resid;   // EP_STORE: residual added (same indexing as out)
+  const float* xg;      // staged activations: row (pair) r at xg + r * K
+  int slot_l;           // ints per layer
+  int K, rows, kind, epi, n_exp, xstage, units, out_ld, split;
+};
+
+struct Tmpl {
+  int type, n_groups, xkind, xkind0, keep_x, end_bar, units, has_routed;
+  const float* xsrc;    // XK_LN / XK_PLAIN source; XK_COMBINE_LN residual (xa)
+  float* xdst;          // XK_COMBINE_LN / XK_EMBED_LN: where CTA 0 writes the new residual
+  Group g[kMaxG];
+};
+
+struct Plan {
+  Tmpl t[kMaxTmpl];     // [0, ppl): one layer's phases; [ppl]: head
+  int ppl, L, n_phases, bpl, upl, router_j;
+  int B, d, H, E, k, S, n_gate, gate_norm, reuse_gates, max_len, V, nc_max, TT;
+  float logit_scale, gamma;
+  const int* tok;
+  const int* pos;
+  const float* embed;
+  const float* pe;
+  float* kc;
+  float* vc;
+  float* q;
+  float* att;
+  float* Y;
+  float* Ys;
+  float* states;        // (L, B, E) own router logits
+  float* extra;         // (L, B, n_gate)
+  const float* replay;  // (L, B, E) or NULL
+  int* idx_out;         // (L, B, k)
+  float* gates_out;     // (L, B, k)
+  int* active_out;      // (L, E + 1) or NULL
+  float* head_logits;   // (B, V) or NULL
+  float* conf;
+  int* argmax;
+  uint8_t* fallback;
+  unsigned* sync;       // [0] barrier, [1] exit, [2] head ticket, [64 + b*H + h] attention tickets
+  float* attn_part;
+  float* head_part;
+  int* flags;
+  unsigned long long* trace;  // optional: per (phase, CTA) [barrier passed, inputs ready, work done] ns
+};
+
+struct Route {          // one layer's selection + permute, in shared memory
+  int n_active;
+  short act_e[kMaxPairs], act_p0[kMaxPairs], act_n[kMaxPairs];
+  short pairs[kMaxPairs];
+  short idx[kMaxPairs];
+  float gates[kMaxPairs];
+};
+
+struct StageMeta {      // written by the weight cursor, read by the activation cursor
+  const float* xrow[kMaxB];
+  int nt, xbytes, needx;
+  unsigned tgt;         // barrier count the activations wait for
+};
+
+// ------------------------------------------------------------------ primitives
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_tx_only(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok) : "r"(su32(b)), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
+          su32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, %0;" ::"n"(kCW * 32) : "memory"); }
+
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Sum of 16 per-lane row partials over the 32 lanes of a warp: recursive
+// halving (16 + 8 + 4 + 2 + 1 shuffles); lanes 2i and 2i+1 end with row i.
+template <int TT>
+__device__ __forceinline__ float reduce_rows16(float (&a)[16][TT], int t, int lane) {
+  float v[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = a[r][t];
+#pragma unroll
+  for (int h = 8, off = 16; h >= 1; h >>= 1, off >>= 1) {
+    const bool hi = (lane & off) != 0;
+#pragma unroll
+    for (int r = 0; r < h; ++r) {
+      const float send = hi ? v[r] : v[r + h];
+      const float keep = hi ? v[r + h] : v[r];
+      v[r] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+constexpr unsigned long long kWatchdogNs = 4000000000ull;  // 4 s: a stuck pass traps instead of hanging
+
+// ------------------------------------------------------------------ program
+// phase p -> (template j, layer l); the head is the last phase
+__device__ __forceinline__ void phase_jl(const Plan& P, int p, int& j, int& l) {
+  if (p == P.n_phases - 1) { j = P.ppl; l = P.L; }
+  else { l = p / P.ppl; j = p - l * P.ppl; }
+}
+// end barriers in phases [0, p]
+__device__ __forceinline__ int bar_cum(const Plan& P, int p) {
+  if (p < 0) return 0;
+  int j, l;
+  phase_jl(P, p, j, l);
+  int n = l * P.bpl;
+  if (j < P.ppl)
+    for (int i = 0; i <= j; ++i) n += P.t[i].end_bar;
+  return n;
+}
+// the latest phase before p with an end barrier (-1: none)
+__device__ __forceinline__ int dep_of(const Plan& P, int p) {
+  for (int q = p - 1; q >= 0; --q) {
+    int j, l;
+    phase_jl(P, q, j, l);
+    if (P.t[j].end_bar) return q;
+  }
+  return -1;
+}
+// barrier count (x grid) after which phase q's outputs are visible, within a launch from `first`
+__device__ __forceinline__ unsigned bar_target(const Plan& P, int q, int first) {
+  if (q < first) return 0u;
+  return (unsigned)(bar_cum(P, q) - bar_cum(P, first - 1)) * gridDim.x;
+}
+__device__ __forceinline__ int rot_of(const Plan& P, int j, int l) {
+  long long c = (long long)l * P.upl;
+  if (j < P.ppl)
+    for (int i = 0; i < j; ++i) c += P.t[i].units;
+  return (int)(c % gridDim.x);
+}
+__device__ __forceinline__ Group grp(const Plan& P, int j, int g, int l) {
+  Group G = P.t[j].g[g];
+  G.w += (long long)l * G.w_l;
+  if (G.slot) G.slot += (size_t)l * G.slot_l;
+  if (G.out) G.out += (size_t)l * G.out_l;
+  if (G.out2) G.out2 += (size_t)l * G.out2_l;
+  return G;
+}
+
+__device__ void spin_until(const Plan& P, unsigned target) {
+  if (target == 0u) return;
+  if (ld_relaxed(P.sync) < target) {
+    const unsigned long long t0 = gtimer();
+    while (ld_relaxed(P.sync) < target) {
+      if (gtimer() - t0 > kWatchdogNs) {
+        atomicOr(P.flags, 4);
+        __trap();
+      }
+    }
+  }
+  fence_acq_rel();
+}
+
+// ------------------------------------------------------------------ routing
+// One warp: stable top-k (toymoe.py:80-88 key order: value desc, index asc,
+// -0.0 == +0.0), replay (toymoe.py:194-200), gate softmax in selection order
+// (toymoe.py:201) or HF softmax-over-all, then the deterministic permute of
+// the B*k (token, slot) pairs sorted by (expert, pair) (permute.cu contract).
+__device__ void compute_route(const Plan& P, int l, Route& R, bool publish) {
+  const int lane = threadIdx.x & 31;
+  const int E = P.E, k = P.k, B = P.B;
+  constexpr int kPer = kMaxE / 32;
+  bool bad = false;
+  for (int b = 0; b < B; ++b) {
+    const float* own = P.states + ((size_t)l * B + b) * E;
+    const float* rep = P.replay ? P.replay + ((size_t)l * B + b) * E : nullptr;
+    const float* sel_src = rep ? rep : own;
+    const float* gate_src = (rep && P.reuse_gates) ? rep : own;
+    unsigned long long key[kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int e = lane + 32 * i;
+      if (e < E) {
+        const float v = __ldcg(sel_src + e);
+        bad |= !isfinite(v);
+        key[i] = topk_key(v, e);
+      } else {
+        key[i] = 0ull;
+      }
+    }
+    int sel_local = -1;
+    for (int j = 0; j < k; ++j) {
+      unsigned long long best = 0ull;
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) best = key[i] > best ? key[i] : best;
+      best = warp_max_u64(best);
+      const int e = topk_key_index(best);
+#pragma unroll
+      for (int i = 0; i < kPer; ++i)
+        if (key[i] == best) key[i] = 0ull;
+      if (lane == j) sel_local = e;
+    }
+    if (lane < k) R.idx[b * k + lane] = sel_local;
+    if (P.gate_norm == MOBILE_GATE_SELECTED_SOFTMAX) {
+      const float gl = lane < k ? __ldcg(gate_src + sel_local) : -INFINITY;
+      const float m = warp_max(gl);
+      const float ex = lane < k ? expf(gl - m) : 0.f;
+      float s = 0.f;
+      for (int j = 0; j < k; ++j) s += __shfl_sync(0xffffffffu, ex, j);
+      if (lane < k) R.gates[b * k + lane] = ex / s;
+    } else {
+      float m = -INFINITY;
+      for (int e = lane; e < E; e += 32) m = fmaxf(m, __ldcg(gate_src + e));
+      m = warp_max(m);
+      float z = 0.f;
+      for (int e = lane; e < E; e += 32) z += expf(__ldcg(gate_src + e) - m);
+      z = warp_sum(z);
+      if (lane < k) R.gates[b * k + lane] = expf(__ldcg(gate_src + sel_local) - m) / z;
+    }
+  }
+  __syncwarp();
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(P.flags, 1);
+  // permute: bitonic sort of (expert << 6 | pair) over <= 32 pairs
+  const int NP = B * k;
+  int key = 0x7fffffff;
+  if (lane < NP) key = (R.idx[lane] << 6) | lane;
+#pragma unroll
+  for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      const int other = __shfl_xor_sync(0xffffffffu, key, j);
+      const bool up = (lane & kk) == 0, lower = (lane & j) == 0;
+      key = (lower == up) ? min(key, other) : max(key, other);
+    }
+  }
+  const bool valid = lane < NP;
+  const int e_me = valid ? (key >> 6) : 0x7fffffff;
+  if (valid) R.pairs[lane] = key & 63;
+  const int e_prev = __shfl_up_sync(0xffffffffu, e_me, 1);
+  const bool first = valid && (lane == 0 || e_prev != e_me);
+  const unsigned fm = __ballot_sync(0xffffffffu, first);
+  const int nact = __popc(fm);
+  if (first) {
+    const int a = __popc(fm & ((1u << lane) - 1u));
+    R.act_e[a] = e_me;
+    R.act_p0[a] = lane;
+    const unsigned after = fm & ~((2u << lane) - 1u);  // next first-lane above me
+    const int end = after ? __ffs(after) - 1 : NP;
+    R.act_n[a] = end - lane;
+  }
+  if (lane == 0) R.n_active = nact;
+  __syncwarp();
+  if (publish) {
+    for (int i = lane; i < NP; i += 32) {
+      P.idx_out[(size_t)l * NP + i] = R.idx[i];
+      P.gates_out[(size_t)l * NP + i] = R.gates[i];
+    }
+    if (P.active_out) {
+      int* a = P.active_out + (size_t)l * (E + 1);
+      if (lane == 0) a[0] = nact;
+      if (lane < nact) a[1 + lane] = R.act_e[lane];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ work items
+// Units of a GEMV phase: (group, expert slot a, 16-row block).  CTA c owns the
+// units u with (u + rot) % G == c; an item is (unit, K chunk).
+struct Item {           // everything the producer and the consumers need about one unit
+  int g, a, rb, rr, nkc, n;
+  int K, rows, epi, xstage, out_ld, split;
+  const char* wrow;     // first byte of the tile's rows (chunk 0)
+  const float* xg;
+  float* out;
+  float* out2;
+  const float* resid;
+  int pr[kMaxB];        // output pair index per token slot
+  int tb[kMaxB];        // token per slot
+};
+
+// decode unit u of (template j, layer l); false = no work (inactive routed slot)
+template <typename W>
+__device__ bool decode_unit(const Plan& P, int j, int l, int u, const Route& R, Item& it) {
+  const Tmpl& T = P.t[j];
+  int uu = u, g = 0;
+  for (; g < T.n_groups - 1; ++g) {
+    if (uu < T.g[g].units) break;
+    uu -= T.g[g].units;
+  }
+  const Group G = grp(P, j, g, l);
+  const int upe = (G.rows + kTileRows - 1) / kTileRows;
+  const int a = uu / upe;
+  it.g = g;
+  it.a = a;
+  it.rb = uu - a * upe;
+  it.rr = min(kTileRows, G.rows - it.rb * kTileRows);
+  it.nkc = (G.K * (int)sizeof(W) + kChunk - 1) / kChunk;
+  const char* base;
+  if (G.kind == GK_ROUTED) {
+    if (a >= R.n_active) return false;
+    const int e = R.act_e[a];
+    const int s = G.slot ? G.slot[e] : e;
+    base = G.w + (long long)s * G.stride;
+    it.n = R.act_n[a];
+#pragma unroll
+    for (int t = 0; t < kMaxB; ++t) {
+      const int q = t < it.n ? R.pairs[R.act_p0[a] + t] : 0;
+      it.pr[t] = q;
+      it.tb[t] = q / P.k;
+    }
+  } else if (G.kind == GK_SHARED) {
+    base = G.w + (long long)a * G.stride;
+    it.n = P.B;
+#pragma unroll
+    for (int t = 0; t < kMaxB; ++t) { it.pr[t] = t * P.S + a; it.tb[t] = t; }
+  } else {
+    base = G.w;
+    it.n = P.B;
+#pragma unroll
+    for (int t = 0; t < kMaxB; ++t) { it.pr[t] = t; it.tb[t] = t; }
+  }
+  it.wrow = base + (size_t)it.rb * kTileRows * G.K * sizeof(W);
+  it.K = G.K; it.rows = G.rows; it.epi = G.epi; it.xstage = G.xstage; it.out_ld = G.out_ld; it.split = G.split;
+  it.xg = G.xg; it.out = G.out; it.out2 = G.out2; it.resid = G.resid;
+  return true;
+}
+__device__ __forceinline__ int group_of_unit(const Tmpl& T, int u) {
+  int g = 0;
+  for (; g < T.n_groups - 1; ++g) {
+    if (u < T.g[g].units) break;
+    u -= T.g[g].units;
+  }
+  return g;
+}
+
+// ------------------------------------------------------------------ x loads
+// Consumers build the phase's activation rows in shared memory (xbuf, B x K).
+__device__ void block_ln_rows(float* x, int B, int d, float* red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int b = 0; b < B; ++b) {
+    float* row = x + (size_t)b * d;
+    float s = 0.f;
+    for (int i = tid; i < d; i += kCW * 32) s += row[i];
+    s = warp_sum(s);
+    if (lane == 0) red[warp] = s;
+    cbar();
+    float mean = 0.f;
+    for (int w = 0; w < kCW; ++w) mean += red[w];
+    mean /= (float)d;
+    cbar();
+    float q = 0.f;
+    for (int i = tid; i < d; i += kCW * 32) {
+      const float c = row[i] - mean;
+      q += c * c;
+    }
+    q = warp_sum(q);
+    if (lane == 0) red[warp] = q;
+    cbar();
+    float var = 0.f;
+    for (int w = 0; w < kCW; ++w) var += red[w];
+    const float inv = 1.0f / sqrtf(var / (float)d + 1e-5f);
+    for (int i = tid; i < d; i += kCW * 32) row[i] = (row[i] - mean) * inv;
+    cbar();
+  }
+}
+
+__device__ void load_x(const Plan& P, int xkind, const float* xsrc, float* xdst, int combine_layer, float* xbuf, float* red,
+                       const Route& R, const int* spos) {
+  const int tid = threadIdx.x, B = P.B, d = P.d, nv = d / 4;
+  const bool writer = blockIdx.x == 0;
+  float4* xb4 = reinterpret_cast<float4*>(xbuf);
+  if (xkind == XK_LN || xkind == XK_PLAIN) {
+    const float4* src = reinterpret_cast<const float4*>(xsrc);
+    float4 v[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = tid + c * kCW * 32;
+      if (i < B * nv) v[c] = __ldcg(src + i);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = tid + c * kCW * 32;
+      if (i < B * nv) xb4[i] = v[c];
+    }
+    for (int i = tid + 4 * kCW * 32; i < B * nv; i += kCW * 32) xb4[i] = __ldcg(src + i);
+    cbar();
+    if (xkind == XK_LN) block_ln_rows(xbuf, B, d, red);
+  } else if (xkind == XK_EMBED_LN) {  // x = embed[tok] + pe[pos]   (toymoe.py:172)
+    for (int b = 0; b < B; ++b) {
+      const float4* er = reinterpret_cast<const float4*>(P.embed + (size_t)P.tok[b] * d);
+      const float4* pr = reinterpret_cast<const float4*>(P.pe + (size_t)spos[b] * d);
+      float4* xd = reinterpret_cast<float4*>(xdst + (size_t)b * d);
+      for (int i = tid; i < nv; i += kCW * 32) {
+        const float4 e = er[i], q = pr[i];
+        const float4 v = make_float4(e.x + q.x, e.y + q.y, e.z + q.z, e.w + q.w);
+        xb4[(size_t)b * nv + i] = v;
+        if (writer) xd[i] = v;
+      }
+    }
+    cbar();
+    block_ln_rows(xbuf, B, d, red);
+  } else if (xkind == XK_COMBINE_LN) {
+    // x_out = xa + sum_j g_j Y_j (selection order) + sum_s sigma_s Ys_s   (toymoe.py:204, 207)
+    // Every source row of a chunk is loaded before any arithmetic (one L2 round trip per chunk).
+    const int l = combine_layer, k = P.k, S = P.S;
+    __shared__ float sg[kMaxB][kMaxGate];
+    if (tid < B * S) {
+      const int b = tid / S, s = tid - b * S;
+      sg[b][s] = P.n_gate ? sigmoid_f(__ldcg(P.extra + ((size_t)l * B + b) * P.n_gate + s)) : 1.0f;
+    }
+    cbar();
+    const float4* Y4 = reinterpret_cast<const float4*>(P.Y);
+    const float4* Ys4 = reinterpret_cast<const float4*>(P.Ys);
+    const float4* X4 = reinterpret_cast<const float4*>(xsrc);
+    float4* xd = reinterpret_cast<float4*>(xdst);
+    for (int b = 0; b < B; ++b) {
+      for (int i = tid; i < nv; i += kCW * 32) {
+        float4 yv[8], ys[kMaxGate];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < k) yv[j] = __ldcg(Y4 + ((size_t)b * k + j) * nv + i);
+#pragma unroll
+        for (int s2 = 0; s2 < kMaxGate; ++s2)
+          if (s2 < S) ys[s2] = __ldcg(Ys4 + ((size_t)b * S + s2) * nv + i);
+        const float4 xv = __ldcg(X4 + (size_t)b * nv + i);
+        float m[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (j < k) {
+            const float g = R.gates[b * k + j];
+            m[0] = fmaf(g, yv[j].x, m[0]); m[1] = fmaf(g, yv[j].y, m[1]);
+            m[2] = fmaf(g, yv[j].z, m[2]); m[3] = fmaf(g, yv[j].w, m[3]);
+          }
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < kMaxGate; ++s2) {
+          if (s2 < S) {
+            const float g = sg[b][s2];
+            m[0] += g * ys[s2].x; m[1] += g * ys[s2].y; m[2] += g * ys[s2].z; m[3] += g * ys[s2].w;
+          }
+        }
+        const float4 v = make_float4(xv.x + m[0], xv.y + m[1], xv.z + m[2], xv.w + m[3]);
+        xb4[(size_t)b * nv + i] = v;
+        if (writer) xd[(size_t)b * nv + i] = v;
+      }
+    }
+    cbar();
+    block_ln_rows(xbuf, B, d, red);
+  }
+}
+
+// ------------------------------------------------------------------ attention
+// Single-query attention over the KV cache (toymoe.py:178-186 at one
+// position).  Items (b, h, chunk) are spread over the grid; each CTA's warps
+// run an online softmax over interleaved positions, merge in warp order, and
+// write a partial; the last chunk of a head to finish merges the partials in
+// chunk order (ticket) into att.
+template <int PER>
+__device__ void attn_item(const Plan& P, int l, int b, int h, int c, int nc, int ctx, float* scratch,
+                          bool& last_s) {
+  constexpr int NB = PER <= 2 ? 8 : PER == 4 ? 6 : 3;  // positions in flight per warp
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int H = P.H, d = P.d, hd = PER * 32, B = P.B;
+  const float scale = 1.0f / sqrtf((float)hd);
+  const int p0 = (int)((long long)ctx * c / nc), p1 = (int)((long long)ctx * (c + 1) / nc);
+  float qv[PER], o[PER];
+  const float* qrow = P.q + (size_t)b * d + h * hd;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) { qv[j] = __ldcg(qrow + lane + 32 * j); o[j] = 0.f; }
+  float m = -INFINITY, s = 0.f;
+  const size_t cache0 = ((size_t)l * B + b) * P.max_len;
+  for (int base = p0 + warp; base < p1; base += kCW * NB) {
+    float kv[NB][PER], vv[NB][PER];
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      const int p = base + kCW * n;
+      const bool ok = p < p1;
+      const float* kr = P.kc + (cache0 + (ok ? p : p0)) * d + h * hd;
+      const float* vr = P.vc + (cache0 + (ok ? p : p0)) * d + h * hd;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        kv[n][j] = ok ? __ldcg(kr + lane + 32 * j) : 0.f;
+        vv[n][j] = ok ? __ldcg(vr + lane + 32 * j) : 0.f;
+      }
+    }
+    float sc[NB];
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      float dot = 0.f;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) dot = fmaf(qv[j], kv[n][j], dot);
+      sc[n] = dot;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+      for (int n = 0; n < NB; ++n) sc[n] += __shfl_xor_sync(0xffffffffu, sc[n], off);
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      if (base + kCW * n >= p1) break;
+      const float v = sc[n] * scale;
+      const float mn = fmaxf(m, v);
+      const float a = expf(m - mn), e = expf(v - mn);
+      s = s * a + e;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) o[j] = o[j] * a + e * vv[n][j];
+      m = mn;
+    }
+  }
+  // warp partials -> smem, merged in warp order by warp 0
+  float* wp = scratch + (size_t)warp * (hd + 2);
+  if (lane == 0) { wp[0] = m; wp[1] = s; }
+#pragma unroll
+  for (int j = 0; j < PER; ++j) wp[2 + lane + 32 * j] = o[j];
+  cbar();
+  if (warp == 0) {
+    float* part = P.attn_part + ((size_t)(b * H + h) * P.nc_max + c) * (hd + 2);
+    float M = -INFINITY;
+    for (int w = 0; w < kCW; ++w) M = fmaxf(M, scratch[(size_t)w * (hd + 2)]);
+    float Ssum = 0.f, acc[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) acc[j] = 0.f;
+    for (int w = 0; w < kCW; ++w) {
+      const float* q = scratch + (size_t)w * (hd + 2);
+      if (q[1] == 0.f) continue;
+      const float f = expf(q[0] - M);
+      Ssum += q[1] * f;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) acc[j] += q[2 + lane + 32 * j] * f;
+    }
+    if (lane == 0) { part[0] = M; part[1] = Ssum; }
+#pragma unroll
+    for (int j = 0; j < PER; ++j) part[2 + lane + 32 * j] = acc[j];
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) last_s = atomicAdd(P.sync + 64 + b * H + h, 1u) == (unsigned)(nc - 1);
+    __syncwarp();
+    if (last_s) {  // last chunk of this head: merge the partials in chunk order
+      __threadfence();
+      const float* base = P.attn_part + (size_t)(b * H + h) * P.nc_max * (hd + 2);
+      float mm[16], ss[16];
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) {
+        mm[cc] = cc < nc ? __ldcg(base + (size_t)cc * (hd + 2)) : -INFINITY;
+        ss[cc] = cc < nc ? __ldcg(base + (size_t)cc * (hd + 2) + 1) : 0.f;
+      }
+      float MM = -INFINITY;
+      for (int cc = 0; cc < nc; ++cc) MM = fmaxf(MM, cc < 16 ? mm[cc] : __ldcg(base + (size_t)cc * (hd + 2)));
+      float SS = 0.f;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) acc[j] = 0.f;
+      for (int cc = 0; cc < nc; ++cc) {
+        const float* q = base + (size_t)cc * (hd + 2);
+        const float sq = cc < 16 ? ss[cc] : __ldcg(q + 1);
+        if (sq == 0.f) continue;
+        const float f = expf((cc < 16 ? mm[cc] : __ldcg(q)) - MM);
+        SS += sq * f;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) acc[j] += __ldcg(q + 2 + lane + 32 * j) * f;
+      }
+      const float inv = 1.0f / SS;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) P.att[(size_t)b * d + h * hd + lane + 32 * j] = acc[j] * inv;
+      if (lane == 0) P.sync[64 + b * H + h] = 0u;
+    }
+  }
+  cbar();
+}
+
+// Single-query attention over the KV cache (toymoe.py:178-186 at one
+// position).  Items (b, h, chunk) are spread over the grid; each warp keeps
+// NB positions of K/V in flight, runs an online softmax over them, the warps
+// merge in warp order and write a partial; the last chunk of a head to finish
+// merges the partials in chunk order (ticket) into att.
+__device__ void attn_phase(const Plan& P, int layer, float* scratch, int rot, const int* spos) {
+  const int B = P.B, H = P.H, hd = P.d / H;
+  const int G = gridDim.x;
+  __shared__ bool last_s;
+  int ctx_max = 1;
+  for (int b = 0; b < B; ++b) ctx_max = max(ctx_max, spos[b] + 1);
+  const int nc = max(1, min(min(G / (B * H), P.nc_max), (ctx_max + 7) / 8));
+  for (int i = ((int)blockIdx.x - rot % G + G) % G; i < B * H * nc; i += G) {
+    const int b = i / (H * nc), r = i - b * H * nc;
+    const int h = r / nc, c = r - h * nc;
+    const int ctx = spos[b] + 1;
+    switch (hd / 32) {
+      case 1: attn_item<1>(P, layer, b, h, c, nc, ctx, scratch, last_s); break;
+      case 2: attn_item<2>(P, layer, b, h, c, nc, ctx, scratch, last_s); break;
+      case 4: attn_item<4>(P, layer, b, h, c, nc, ctx, scratch, last_s); break;
+      default: attn_item<8>(P, layer, b, h, c, nc, ctx, scratch, last_s); break;
+    }
+  }
+}
+
+__device__ __forceinline__ void online_add(float& m, float& s, int& arg, float l, int idx) {
+  if (l > m) {
+    s = s * expf(m - l) + 1.0f;
+    m = l;
+    arg = idx;
+  } else {
+    s += expf(l - m);
+  }
+}
+__device__ __forceinline__ void online_merge(float& M, float& S, int& A, float m, float s, int a) {
+  if (s == 0.f) return;
+  if (m > M) { S = S * expf(M - m) + s; M = m; A = a; }
+  else { S += s * expf(m - M); if (m == M && a < A) A = a; }
+}
+
+// ------------------------------------------------------------------ the kernel
+template <typename W, int TT>
+__global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_constant__ Plan P, int first,
+                                                                   int last, int nst, int stage_bytes,
+                                                                   int xbuf_off) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) uint64_t full[kMaxStages];
+  __shared__ __align__(8) uint64_t empty[kMaxStages];
+  __shared__ StageMeta meta[kMaxStages];
+  __shared__ Route rt_c, rt_p;
+  __shared__ int spos[kMaxB];
+  __shared__ __align__(16) float red2[kCW * kTileRows * TT];  // cross-warp row sums / LN / head merge
+  __shared__ bool is_last;
+  float* red = red2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int V = WVec<W>::N;
+  constexpr int KC = kChunk / (int)sizeof(W);
+  const int G = gridDim.x;
+  float* xbuf = reinterpret_cast<float*>(smem + xbuf_off);
+
+  if (tid == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < P.B) spos[tid] = P.pos[tid];
+  __syncthreads();
+
+  if (warp == kCW) {
+    // ================================================================ producer
+    // Weight cursor (W): issues the weight tile of every item into the ring as
+    // soon as a stage is free and the tile's address is known (static
+    // matrices: always; routed experts: once the layer's selection is).
+    // Activation cursor (X): issues the staged activation slices of items
+    // whose inputs come from the previous phase, once its barrier completed.
+    int wp = first, wu = 0, wkc = 0, wj = 0, wl = 0;
+    unsigned wtgt = 0;            // barrier count after which this phase's activations exist
+    Item wit;
+    int rt_layer = -1;
+    auto seek = [&](bool fresh) -> int {  // 0 = ok, 1 = done, 2 = blocked on routing (warp-uniform)
+      while (wp < last) {
+        phase_jl(P, wp, wj, wl);
+        const Tmpl& T = P.t[wj];
+        if (T.type != PT_GEMV) { ++wp; fresh = true; continue; }
+        if (fresh) {
+          wu = (blockIdx.x - rot_of(P, wj, wl) + G) % G;
+          wkc = 0;
+          const int dq = dep_of(P, wp);
+          wtgt = dq >= 0 ? bar_target(P, dq, first) : 0u;
+          fresh = false;
+        }
+        while (wu < T.units) {
+          const int g = group_of_unit(T, wu);
+          if (T.g[g].kind == GK_ROUTED && rt_layer != wl) {
+            unsigned ok = 1;
+            if (lane == 0 && !P.replay) {
+              const unsigned tgt = bar_target(P, wl * P.ppl + P.router_j, first);
+              ok = (tgt == 0u || ld_relaxed(P.sync) >= tgt) ? 1u : 0u;
+            }
+            ok = __shfl_sync(0xffffffffu, ok, 0);
+            if (!ok) return 2;
+            fence_acq_rel();
+            compute_route(P, wl, rt_p, false);
+            rt_layer = wl;
+          }
+          if (decode_unit<W>(P, wj, wl, wu, rt_p, wit)) return 0;
+          wu += G;
+        }
+        ++wp;
+        fresh = true;
+      }
+      return 1;
+    };
+    int st = seek(true);
+    uint32_t iw = 0, ix = 0;      // items issued (weights) / completed (activations)
+    unsigned long long t0 = 0;
+    unsigned seen = 0;            // last observed barrier counter
+    while (true) {
+      bool progress = false;
+      if (st == 2) st = seek(false);
+      // ---- weight cursor
+      if (st == 0 && iw < ix + (uint32_t)nst) {
+        const int s = (int)(iw % (uint32_t)nst);
+        bool free_ = true;
+        if (iw >= (uint32_t)nst) {
+          unsigned ok = 0;
+          if (lane == 0) ok = mbar_test(&empty[s], ((iw / nst) - 1) & 1u) ? 1u : 0u;
+          free_ = __shfl_sync(0xffffffffu, ok, 0) != 0;
+        }
+        if (free_) {
+          const Item& Gr = wit;
+          const int k0 = wkc * KC, kn = min(KC, Gr.K - k0);
+          const uint32_t wbytes = (uint32_t)(wit.rr * kn * sizeof(W));
+          char* stg = smem + (size_t)s * stage_bytes;
+          if (lane == 0) {
+            if (iw >= (uint32_t)nst) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            StageMeta& mt = meta[s];
+            mt.needx = Gr.xstage;
+            if (Gr.xstage) {
+              mt.nt = wit.n;
+              mt.xbytes = kn * (int)sizeof(float);
+              mt.tgt = wtgt;
+              for (int t = 0; t < kMaxB; ++t) mt.xrow[t] = Gr.xg + (size_t)wit.pr[t] * Gr.K + k0;
+              mbar_tx_only(&full[s], wbytes);
+            } else {
+              mbar_arrive_tx(&full[s], wbytes);
+            }
+            if (kn == Gr.K) {
+              bulk_g2s(stg, wit.wrow, wbytes, &full[s]);
+            } else {
+              const uint32_t rb = (uint32_t)(kn * sizeof(W));
+              for (int r = 0; r < wit.rr; ++r)
+                bulk_g2s(stg + (size_t)r * rb, wit.wrow + ((size_t)r * Gr.K + k0) * sizeof(W), rb, &full[s]);
+            }
+          }
+          ++iw;
+          progress = true;
+          if (++wkc >= wit.nkc) {
+            wkc = 0;
+            wu += G;
+            st = seek(false);
+          }
+        }
+      }
+      // ---- activation cursor
+      __syncwarp();
+      if (ix < iw) {
+        const int s = (int)(ix % (uint32_t)nst);
+        const StageMeta& mt = meta[s];
+        if (!mt.needx) {
+          ++ix;
+          progress = true;
+        } else {
+          const unsigned tgt = mt.tgt;
+          unsigned ok = 0;
+          if (lane == 0) {
+            if (seen < tgt) seen = ld_relaxed(P.sync);
+            ok = seen >= tgt ? 1u : 0u;
+          }
+          if (__shfl_sync(0xffffffffu, ok, 0)) {
+            if (lane == 0) {
+              fence_acq_rel();
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+              char* stg = smem + (size_t)s * stage_bytes + kWBytes;
+              mbar_arrive_tx(&full[s], (uint32_t)(mt.nt * mt.xbytes));
+              for (int t = 0; t < mt.nt; ++t)
+                bulk_g2s(stg + (size_t)t * mt.xbytes, mt.xrow[t], (uint32_t)mt.xbytes, &full[s]);
+            }
+            ++ix;
+            progress = true;
+          }
+        }
+      }
+      if (st == 1 && ix == iw) break;
+      if (!progress) {
+        if (t0 == 0) t0 = gtimer();
+        else if (gtimer() - t0 > kWatchdogNs) {
+          if (lane == 0) atomicOr(P.flags, 8);
+          __trap();
+        }
+        __nanosleep(20);
+      } else {
+        t0 = 0;
+      }
+    }
+    return;
+  }
+
+  // ================================================================== consumers
+  uint32_t ic = 0;  // items consumed
+  float hm = -INFINITY, hs = 0.f;  // head: online (max, sum-exp, first argmax) of this thread's row
+  int ha = 0x7fffffff;
+  int rtc_layer = -1;
+  constexpr int SL = KC / kCW;  // K elements of a chunk owned by one warp (= 32 lanes x V)
+  for (int p = first; p < last; ++p) {
+    int j, l;
+    phase_jl(P, p, j, l);
+    const Tmpl& T = P.t[j];
+    // ---- wait for the phase's inputs
+    if (tid == 0) {
+      const int dep = dep_of(P, p);
+      if (dep >= first) spin_until(P, bar_target(P, dep, first));
+    }
+    cbar();
+    unsigned long long* tr = P.trace ? P.trace + ((size_t)(p - first) * G + blockIdx.x) * 3 : nullptr;
+    if (tr && tid == 0) tr[0] = gtimer();
+    const int rot = rot_of(P, j, l);
+    if (T.type == PT_PUBLISH) {
+      if (blockIdx.x == 0 && warp == 0) compute_route(P, l, rt_c, true);
+    } else if (T.type == PT_ATTN) {
+      attn_phase(P, l, xbuf, rot, spos);
+    } else {
+      if (T.has_routed && rtc_layer != l) {
+        if (warp == 0) compute_route(P, l, rt_c, blockIdx.x == 0);
+        rtc_layer = l;
+      }
+      const int xk = l == 0 ? T.xkind0 : T.xkind;
+      if (xk != XK_NONE && (!T.keep_x || p == first)) load_x(P, xk, T.xsrc, T.xdst, l - 1, xbuf, red, rt_c, spos);
+      cbar();
+      if (tr && tid == 0) tr[1] = gtimer();
+      const bool head_phase = T.g[0].epi == EP_HEAD;
+      if (head_phase) { hm = -INFINITY; hs = 0.f; ha = 0x7fffffff; }
+      Item it;
+      for (int u = (blockIdx.x - rot + G) % G; u < T.units; u += G) {
+        if (!decode_unit<W>(P, j, l, u, rt_c, it)) continue;
+        const Item& Gr = it;
+        const int nt = it.n, rr = it.rr;
+        // warp w owns K elements [w*SL, (w+1)*SL) of every row of the tile
+        float acc[kTileRows][TT];
+#pragma unroll
+        for (int r = 0; r < kTileRows; ++r)
+#pragma unroll
+          for (int t = 0; t < TT; ++t) acc[r][t] = 0.f;
+        for (int kc = 0; kc < it.nkc; ++kc, ++ic) {
+          const int s = (int)(ic % (uint32_t)nst);
+          const int k0 = kc * KC, kn = min(KC, Gr.K - k0);
+          const int e0 = warp * SL + lane * V;
+          mbar_wait(&full[s], (ic / nst) & 1u);
+          if (e0 < kn) {
+            const char* stg = smem + (size_t)s * stage_bytes;
+            float xv[TT][V];
+#pragma unroll
+            for (int t = 0; t < TT; ++t) {
+              if (t < nt) {
+                const float* xr = Gr.xstage ? reinterpret_cast<const float*>(stg + kWBytes) + (size_t)t * kn + e0
+                                            : xbuf + (size_t)it.tb[t < kMaxB ? t : 0] * Gr.K + k0 + e0;
+#pragma unroll
+                for (int qq = 0; qq < V / 4; ++qq) {
+                  const float4 x4 = reinterpret_cast<const float4*>(xr)[qq];
+                  xv[t][4 * qq] = x4.x; xv[t][4 * qq + 1] = x4.y; xv[t][4 * qq + 2] = x4.z; xv[t][4 * qq + 3] = x4.w;
+                }
+              }
+            }
+            const W* wb = reinterpret_cast<const W*>(stg) + e0;
+#pragma unroll
+            for (int r = 0; r < kTileRows; ++r) {
+              if (r < rr) {
+                float f[V];
+                WVec<W>::widen(*reinterpret_cast<const uint4*>(wb + (size_t)r * kn), f);
+#pragma unroll
+                for (int t = 0; t < TT; ++t)
+                  if (t < nt)
+#pragma unroll
+                    for (int q = 0; q < V; ++q) acc[r][t] = fmaf(f[q], xv[t][q], acc[r][t]);
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        // ---- reduce: 16 rows over 32 lanes (butterfly), then over warps in order
+        float rs[TT];
+#pragma unroll
+        for (int t = 0; t < TT; ++t) rs[t] = reduce_rows16<TT>(acc, t, lane);
+        cbar();  // the previous unit's epilogue has read red2
+        if ((lane & 1) == 0)
+#pragma unroll
+          for (int t = 0; t < TT; ++t) red2[(warp * kTileRows + ((lane >> 1) & 15)) * TT + t] = rs[t];
+        cbar();
+        if (tid < kTileRows * TT) {
+          const int t = tid >> 4, i = tid & 15;
+          if (t < nt && i < rr) {
+            float v = 0.f;
+            for (int w = 0; w < kCW; ++w) v += red2[(w * kTileRows + i) * TT + t];
+            const int r0 = it.rb * kTileRows + i;
+            const int pr = it.pr[t], tb = it.tb[t];
+            if (Gr.epi == EP_HEAD) {
+              const float lg = v * P.logit_scale;
+              if (P.head_logits) P.head_logits[(size_t)tb * P.V + r0] = lg;
+              online_add(hm, hs, ha, lg, r0);
+            } else if (Gr.epi == EP_SWIGLU) {  // tile rows [8 gate | 8 up]
+              if (i < 8) {
+                float u2 = 0.f;
+                for (int w = 0; w < kCW; ++w) u2 += red2[(w * kTileRows + i + 8) * TT + t];
+                Gr.out[(size_t)pr * Gr.out_ld + it.rb * 8 + i] = silu_f(v) * u2;
+              }
+            } else if (Gr.epi == EP_QKV) {
+              const int d = P.d;
+              if (r0 < d) P.q[(size_t)tb * d + r0] = v;
+              else {
+                float* cache = r0 < 2 * d ? P.kc : P.vc;
+                const int c = r0 < 2 * d ? r0 - d : r0 - 2 * d;
+                cache[(((size_t)l * P.B + tb) * P.max_len + spos[tb]) * d + c] = v;
+              }
+            } else if (Gr.epi == EP_LOGITS) {
+              if (r0 < Gr.split) Gr.out[(size_t)tb * Gr.out_ld + r0] = v;
+              else Gr.out2[(size_t)tb * (Gr.rows - Gr.split) + (r0 - Gr.split)] = v;
+            } else {
+              const size_t o0 = (size_t)pr * Gr.out_ld + r0;
+              if (Gr.epi == EP_RELU) v = fmaxf(v, 0.f);
+              else if (Gr.resid) v += __ldcg(Gr.resid + o0);
+              Gr.out[o0] = v;
+            }
+          }
+        }
+      }
+      if (head_phase) {
+        // merge the 16 row-threads of each token (row order), then CTAs (CTA order) in the last CTA
+        cbar();
+        if (tid < kTileRows * TT) {
+          red2[tid * 3] = hm;
+          red2[tid * 3 + 1] = hs;
+          red2[tid * 3 + 2] = __int_as_float(ha);
+        }
+        cbar();
+        if (tid < P.B) {
+          float M = -INFINITY, S = 0.f;
+          int A = 0x7fffffff;
+          for (int i = 0; i < kTileRows; ++i) {
+            const float* q = red2 + (tid * kTileRows + i) * 3;
+            online_merge(M, S, A, q[0], q[1], __float_as_int(q[2]));
+          }
+          float* hp = P.head_part + ((size_t)blockIdx.x * kMaxB + tid) * 3;
+          hp[0] = M; hp[1] = S; hp[2] = __int_as_float(A);
+        }
+        __threadfence();
+        cbar();
+        if (tid == 0) is_last = atomicAdd(P.sync + 2, 1u) == gridDim.x - 1;
+        cbar();
+        if (is_last) {
+          __threadfence();
+          if (tid < P.B) {
+            float M = -INFINITY, S = 0.f;
+            int A = 0x7fffffff;
+            for (unsigned b = 0; b < gridDim.x; ++b) {
+              const float* hp = P.head_part + ((size_t)b * kMaxB + tid) * 3;
+              online_merge(M, S, A, __ldcg(hp), __ldcg(hp + 1), __float_as_int(__ldcg(hp + 2)));
+            }
+            const float conf = 1.0f / S;
+            P.conf[tid] = conf;
+            if (P.argmax) P.argmax[tid] = A;
+            if (P.fallback) P.fallback[tid] = conf <= P.gamma ? 1 : 0;
+          }
+          if (tid == 0) P.sync[2] = 0u;
+        }
+      }
+    }
+    // ---- end of phase: grid barrier arrival
+    cbar();
+    if (tr && tid == 0) tr[2] = gtimer();
+    if (T.end_bar && tid == 0) red_release_add(P.sync, 1u);
+  }
+  // exit ticket: the last CTA out resets the barrier for the next launch
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(P.sync + 1, 1u) == gridDim.x - 1) {
+      P.sync[0] = 0u;
+      P.sync[1] = 0u;
+      __threadfence();
+    }
+  }
+}
+
+}  // namespace dp
+}  // namespace mobile
+
+// ====================================================================== host
+#include <algorithm>
+#include <vector>
+
+using namespace mobile;
+using namespace mobile::dp;
+
+struct mobile_dp {
+  Plan plan{};
+  std::vector<int> seg_first;  // offload: first phase of segment l (l = 0..L), seg_first[L+1] = n_phases
+  void* d_ws = nullptr;
+  int w_dtype = 0, TT = 1, nst = 3, stage_bytes = 0, xbuf_off = 0;
+  size_t smem = 0;
+  int grid = 0;
+};
+
+namespace {
+
+template <typename W, int TT>
+void* kernel_ptr() { return (void*)decode_pass_kernel<W, TT>; }
+
+void* pick_kernel(int w_dtype, int TT) {
+  if (w_dtype == MOBILE_BF16) return TT == 1 ? kernel_ptr<__nv_bfloat16, 1>() : TT == 2 ? kernel_ptr<__nv_bfloat16, 2>() : kernel_ptr<__nv_bfloat16, 4>();
+  return TT == 1 ? kernel_ptr<float, 1>() : TT == 2 ? kernel_ptr<float, 2>() : kernel_ptr<float, 4>();
+}
+
+Group dense_group(const void* w, long long w_l, int K, int rows, int epi) {
+  Group g{};
+  g.w = (const char*)w;
+  g.w_l = w_l;
+  g.K = K;
+  g.rows = rows;
+  g.kind = GK_DENSE;
+  g.epi = epi;
+  g.n_exp = 1;
+  g.split = rows;
+  return g;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mobile_dp_create(const mobile_dp_model* m, mobile_dp** out) {
+  *out = nullptr;
+  const int B = m->B, d = m->d, L = m->L, E = m->E, k = m->k, S = m->n_shared;
+  const int eb = m->w_dtype == MOBILE_BF16 ? 2 : 4;
+  if (m->w_dtype != MOBILE_BF16 && m->w_dtype != MOBILE_F32) { set_error("decode_pass: unsupported dtype"); return MOBILE_ERR_UNSUPPORTED; }
+  if (B < 1 || B > kMaxB || B * k > kMaxPairs || k > 8 || E > kMaxE || S > kMaxGate || m->n_gate > S || m->H < 1 ||
+      d % m->H || d / m->H > 256 || (d / m->H) % 32 || d % 8 || d > 4096 || L < 1) {
+    set_error("decode_pass: unsupported shape B=%d k=%d E=%d S=%d d=%d H=%d", B, k, E, S, d, m->H);
+    return MOBILE_ERR_UNSUPPORTED;
+  }
+  auto* o = new mobile_dp();
+  o->w_dtype = m->w_dtype;
+  o->TT = B == 1 ? 1 : B == 2 ? 2 : 4;
+  const int G = sm_count();
+  o->grid = G;
+  // ---- shared memory: ring of (64 KB weights + TT activation slices) + xbuf
+  const int xslice = kChunk / eb * 4;
+  o->stage_bytes = kWBytes + o->TT * xslice;
+  const int hd = d / m->H;
+  const size_t xbuf = std::max((size_t)B * d * 4, (size_t)kCW * (hd + 2) * 4);
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, pick_kernel(m->w_dtype, o->TT));
+  const size_t cap = (size_t)optin - fa.sharedSizeBytes;
+  int nst = 3;
+  while (nst > 1 && (size_t)nst * o->stage_bytes + xbuf > cap) --nst;
+  if (nst < 2) { set_error("decode_pass: shared memory does not fit (B=%d d=%d)", B, d); delete o; return MOBILE_ERR_UNSUPPORTED; }
+  o->nst = nst;
+  o->xbuf_off = nst * o->stage_bytes;
+  o->smem = (size_t)o->xbuf_off + xbuf;
+
+  // ---- workspace: sync words, attention partials, head partials
+  const int nc_max = std::max(1, G / std::max(1, B * m->H));
+  const size_t sync_bytes = 4 * (64 + (size_t)B * m->H) + 256;
+  const size_t attn_bytes = 4 * (size_t)B * m->H * nc_max * (hd + 2);
+  const size_t head_bytes = 4 * (size_t)G * kMaxB * 3;
+  const size_t ws = sync_bytes + attn_bytes + head_bytes;
+  if (cudaMalloc(&o->d_ws, ws) != cudaSuccess || cudaMemset(o->d_ws, 0, ws) != cudaSuccess) {
+    set_error("decode_pass: workspace allocation failed");
+    delete o;
+    return MOBILE_ERR_CUDA;
+  }
+  Plan& P = o->plan;
+  P.B = B; P.d = d; P.H = m->H; P.E = E; P.k = k; P.S = S; P.n_gate = m->n_gate; P.gate_norm = m->gate_norm;
+  P.reuse_gates = m->reuse_gates; P.max_len = m->max_len; P.L = L; P.V = m->V; P.nc_max = nc_max; P.TT = o->TT;
+  P.logit_scale = m->logit_scale; P.gamma = m->gamma;
+  P.tok = m->tok; P.pos = m->pos; P.embed = m->embed; P.pe = m->pe; P.kc = m->kc; P.vc = m->vc;
+  P.q = m->q; P.att = m->att; P.Y = m->Y; P.Ys = m->Ys; P.states = m->states; P.extra = m->extra;
+  P.replay = m->replay; P.idx_out = m->idx_out; P.gates_out = m->gates_out; P.active_out = m->active_out;
+  P.head_logits = m->head_logits; P.conf = m->conf; P.argmax = m->argmax; P.fallback = m->fallback;
+  P.sync = (unsigned*)o->d_ws;
+  P.attn_part = (float*)((char*)o->d_ws + sync_bytes);
+  P.head_part = (float*)((char*)o->d_ws + sync_bytes + attn_bytes);
+  P.flags = m->flags;
+  P.trace = nullptr;
+
+  // ---- per-layer phase templates
+  const long long Wsz = (long long)d * d * eb;
+  const int I = m->ffn, Is = m->shared_ffn;
+  const bool swiglu = m->activation == MOBILE_ACT_SWIGLU;
+  const int r13 = swiglu ? 2 * I : I, r13s = swiglu ? 2 * Is : Is;
+  const int act_epi = swiglu ? EP_SWIGLU : EP_RELU;
+  const int ng1 = std::max(m->n_gate, 1);
+  std::vector<Tmpl> ts;
+  {  // qkv
+    Tmpl t{};
+    t.type = PT_GEMV; t.n_groups = 1; t.end_bar = 1;
+    t.g[0] = dense_group(m->qkv, 3 * Wsz, d, 3 * d, EP_QKV);
+    t.xkind0 = XK_EMBED_LN; t.xkind = XK_COMBINE_LN; t.xsrc = m->xa; t.xdst = m->x;
+    ts.push_back(t);
+  }
+  {  // attention
+    Tmpl t{};
+    t.type = PT_ATTN; t.end_bar = 1;
+    ts.push_back(t);
+  }
+  {  // o + residual
+    Tmpl t{};
+    t.type = PT_GEMV; t.n_groups = 1; t.end_bar = 1;
+    t.g[0] = dense_group(m->o, Wsz, d, d, EP_STORE);
+    t.g[0].out = m->xa; t.g[0].out_ld = d; t.g[0].resid = m->x;
+    t.xkind0 = t.xkind = XK_PLAIN; t.xsrc = m->att;
+    ts.push_back(t);
+  }
+  const int router_j = (int)ts.size();
+  {  // router logits (+ shared gates) + shared gate-up
+    Tmpl t{};
+    t.type = PT_GEMV; t.end_bar = 1;
+    t.xkind0 = t.xkind = XK_LN; t.xsrc = m->xa;
+    const int rrows = E + m->n_gate;
+    t.g[0] = dense_group(m->router, (long long)rrows * d * eb, d, rrows, EP_LOGITS);
+    t.g[0].out = m->states; t.g[0].out_l = (long long)B * E; t.g[0].out_ld = E; t.g[0].split = E;
+    t.g[0].out2 = m->extra; t.g[0].out2_l = (long long)B * ng1;
+    t.n_groups = 1;
+    if (S) {
+      Group g{};
+      g.w = (const char*)m->shared; g.w_l = (long long)S * m->shared_stride;
+      g.stride = m->shared_stride; g.K = d; g.rows = r13s; g.kind = GK_SHARED; g.epi = act_epi; g.n_exp = S;
+      g.out = m->Us; g.out_ld = Is; g.split = r13s;
+      t.g[t.n_groups++] = g;
+    }
+    ts.push_back(t);
+  }
+  if (m->offload) {  // publish the layer's selection for the host cache
+    Tmpl t{};
+    t.type = PT_PUBLISH;
+    ts.push_back(t);
+  }
+  const int gu_j = (int)ts.size();
+  {  // shared down (static weights first) + routed gate-up
+    Tmpl t{};
+    t.type = PT_GEMV; t.end_bar = 1; t.has_routed = 1;
+    t.xkind0 = t.xkind = XK_LN; t.keep_x = 1; t.xsrc = m->xa;
+    if (S) {
+      Group g{};
+      g.w = (const char*)m->shared + m->shared_w2_offset; g.w_l = (long long)S * m->shared_stride;
+      g.stride = m->shared_stride; g.K = Is; g.rows = d; g.kind = GK_SHARED; g.epi = EP_STORE; g.n_exp = S;
+      g.out = m->Ys; g.out_ld = d; g.xstage = 1; g.xg = m->Us; g.split = d;
+      t.g[t.n_groups++] = g;
+    }
+    Group g{};
+    g.w = (const char*)m->experts; g.w_l = m->expert_layer_stride;
+    g.stride = m->expert_stride; g.slot = m->slot_table; g.slot_l = E;
+    g.K = d; g.rows = r13; g.kind = GK_ROUTED; g.epi = act_epi; g.n_exp = std::min(E, B * k);
+    g.out = m->U; g.out_ld = I; g.split = r13;
+    t.g[t.n_groups++] = g;
+    ts.push_back(t);
+  }
+  {  // routed down
+    Tmpl t{};
+    t.type = PT_GEMV; t.end_bar = 1; t.has_routed = 1; t.n_groups = 1;
+    Group g{};
+    g.w = (const char*)m->experts + m->expert_w2_offset; g.w_l = m->expert_layer_stride;
+    g.stride = m->expert_stride; g.slot = m->slot_table; g.slot_l = E;
+    g.K = I; g.rows = d; g.kind = GK_ROUTED; g.epi = EP_STORE; g.n_exp = std::min(E, B * k);
+    g.out = m->Y; g.out_ld = d; g.xstage = 1; g.xg = m->U; g.split = d;
+    t.g[0] = g;
+    ts.push_back(t);
+  }
+  const int ppl = (int)ts.size();
+  {  // head
+    Tmpl t{};
+    t.type = PT_GEMV; t.n_groups = 1; t.end_bar = 0;
+    t.xkind0 = t.xkind = XK_COMBINE_LN; t.xsrc = m->xa; t.xdst = m->x;
+    t.g[0] = dense_group(m->head, 0, d, m->V, EP_HEAD);
+    ts.push_back(t);
+  }
+  int upl = 0, bpl = 0;
+  for (size_t i = 0; i < ts.size(); ++i) {
+    Tmpl& t = ts[i];
+    t.units = 0;
+    for (int g = 0; g < t.n_groups; ++g) {
+      Group& gr = t.g[g];
+      gr.units = gr.n_exp * ((gr.rows + kTileRows - 1) / kTileRows);
+      t.units += gr.units;
+      if (gr.K % (eb == 2 ? 8 : 4)) { set_error("decode_pass: K=%d not a multiple of the vector width", gr.K); delete o; return MOBILE_ERR_UNSUPPORTED; }
+      if (gr.epi == EP_SWIGLU && gr.rows % kTileRows) { set_error("decode_pass: SwiGLU rows %% 16"); delete o; return MOBILE_ERR_UNSUPPORTED; }
+    }
+    if (t.type == PT_ATTN) t.units = B * m->H * nc_max;  // rotation only
+    if ((int)i < ppl) { upl += t.units; bpl += t.end_bar; }
+  }
+  for (size_t i = 0; i < ts.size(); ++i) P.t[i] = ts[i];
+  P.ppl = ppl; P.L = L; P.n_phases = ppl * L + 1; P.bpl = bpl; P.upl = upl; P.router_j = router_j;
+  if (m->offload) {  // segments cut before each layer's routed gate-up
+    o->seg_first.push_back(0);
+    for (int l = 0; l < L; ++l) o->seg_first.push_back(l * ppl + gu_j);
+    o->seg_first.push_back(P.n_phases);
+  }
+  void* kern = pick_kernel(o->w_dtype, o->TT);
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)o->smem) != cudaSuccess) {
+    set_error("decode_pass: cannot reserve %zu B of shared memory", o->smem);
+    cudaFree(o->d_ws);
+    delete o;
+    return MOBILE_ERR_UNSUPPORTED;
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, o->smem);
+  if (occ < 1) { set_error("decode_pass: kernel does not fit on an SM"); cudaFree(o->d_ws); delete o; return MOBILE_ERR_UNSUPPORTED; }
+  *out = o;
+  return MOBILE_OK;
+}
+
+void mobile_dp_destroy(mobile_dp* o) {
+  if (!o) return;
+  cudaFree(o->d_ws);
+  delete o;
+}
+
+int mobile_dp_num_segments(const mobile_dp* o) { return o->seg_first.empty() ? 1 : (int)o->seg_first.size() - 1; }
+
+int mobile_dp_info(const mobile_dp* o, int* out4) {
+  out4[0] = o->plan.n_phases;
+  out4[1] = o->nst;
+  out4[2] = (int)o->smem;
+  out4[3] = o->grid;
+  return MOBILE_OK;
+}
+
+int mobile_dp_set_trace(mobile_dp* o, unsigned long long* trace) {
+  o->plan.trace = trace;
+  return MOBILE_OK;
+}
+
+// Launch the whole pass (segment = -1) or one offload segment.
+int mobile_dp_launch(mobile_dp* o, int segment, void* stream) {
+  int first = 0, last = o->plan.n_phases;
+  if (segment >= 0) {
+    if (o->seg_first.empty() || segment + 1 >= (int)o->seg_first.size()) { set_error("decode_pass: bad segment %d", segment); return MOBILE_ERR_INVALID; }
+    first = o->seg_first[segment];
+    last = o->seg_first[segment + 1];
+  }
+  void* kern = pick_kernel(o->w_dtype, o->TT);
+  void* args[] = {(void*)&o->plan, (void*)&first, (void*)&last, (void*)&o->nst, (void*)&o->stage_bytes, (void*)&o->xbuf_off};
+  cudaError_t e = cudaLaunchKernel(kern, dim3(o->grid), dim3(kThreads), args, o->smem, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_status(e, "decode_pass launch");
+  return MOBILE_OK;
+}
+
+}  // extern "C"

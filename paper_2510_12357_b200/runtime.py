@@ -37,7 +37,8 @@ KINDS = ("little", "big", "full")
 
 
 class StepEngine:
-    def __init__(self, dm: DeviceModel, batch: int, max_len: int, runtime=None, graphs: bool = True):
+    def __init__(self, dm: DeviceModel, batch: int, max_len: int, runtime=None, graphs: bool = True,
+                 persistent: bool | None = None):
         s = dm.spec
         if batch > 8:
             raise ValueError("StepEngine: batch <= 8 (GEMV decode path)")
@@ -73,6 +74,10 @@ class StepEngine:
             self.active_host = torch.zeros(L, E + 1, dtype=i32, pin_memory=True)
         self.reuse_gates = False
         self.timer = None  # kernel timer (eager mode only: events are not graph nodes here)
+        # persistent decode-pass kernel (decode_pass.cu): one launch per pass /
+        # offload segment.  None = use it whenever the shape is supported.
+        self.persistent = persistent
+        self.dp = {}
 
     # ------------------------------------------------------------------ kernels
     def _attn(self, l: int, x_in: torch.Tensor) -> torch.Tensor:
@@ -112,6 +117,14 @@ class StepEngine:
     def _seg(self, kind: str, l: int):
         """Segment l of an offloaded pass: experts(l-1) [+ attn/route(l)]."""
         L = self.spec.num_layers
+        if self.dp:
+            row = 1 if kind == "big" else 0
+            if l > 0:
+                K.memcpy_async(self.rt.slot_dev[row, l - 1], self.rt.slot_host[row, l - 1])
+            self._dp_launch(kind, l)
+            if l < L and kind != "big":
+                K.memcpy_async(self.active_host[l], self.active_dev[l])
+            return
         if l == 0:
             K.embed(self.tok, self.pos, self.dm.dw.embed, self.pe, self.x, ln_out=self.ln)
             x_in = self.x
@@ -128,8 +141,97 @@ class StepEngine:
         if kind != "big":
             K.memcpy_async(self.active_host[l], sc["perm"]["active"])
 
+    # ------------------------------------------------------------------ persistent pass
+    def _dp_build(self, gamma: float, reuse_gates: bool) -> bool:
+        """Create one mobile_dp program per pass kind; False if unsupported."""
+        s, dw, B, dev = self.spec, self.dm.dw, self.B, self.dm.device
+        L, E, d = s.num_layers, s.num_experts, s.hidden_dim
+        f32, i32 = torch.float32, torch.int32
+        ng = dw.n_gate_rows
+        kb = s.k_big
+        self.q = torch.empty(B, d, dtype=f32, device=dev)
+        self.extra = torch.zeros(L, B, max(ng, 1), dtype=f32, device=dev)
+        self.gates = {kd: torch.empty(L, B, self.k[kd], dtype=f32, device=dev) for kd in KINDS}
+        self.dpU = torch.empty(B * kb, s.ffn, dtype=f32, device=dev)
+        self.dpY = torch.empty(B * kb, d, dtype=f32, device=dev)
+        S = s.n_shared
+        self.dpUs = torch.empty(max(B * S, 1), max(s.shared_ffn, 1), dtype=f32, device=dev)
+        self.dpYs = torch.empty(max(B * S, 1), d, dtype=f32, device=dev)
+        self.active_dev = torch.zeros(L, E + 1, dtype=i32, device=dev)
+        self.dp_flags = torch.zeros(1, dtype=i32, device=dev)
+        self._dp_models = {}
+        for kd in KINDS:
+            m = N.mobile_dp_model()
+            m.B, m.L, m.d, m.H, m.V, m.E, m.k = B, L, d, s.n_heads, s.vocab_size, E, self.k[kd]
+            m.n_shared, m.n_gate, m.ffn, m.shared_ffn = S, ng, s.ffn, s.shared_ffn if S else 0
+            m.activation = self.dm.moe.act
+            m.gate_norm = self.dm.moe.gate_norm
+            m.reuse_gates = int(bool(reuse_gates))
+            m.w_dtype = self.dm.moe.wcode
+            m.max_len = self.max_len
+            m.offload = int(self.rt is not None)
+            m.logit_scale, m.gamma = float(s.logit_scale), float(gamma)
+            m.qkv, m.o, m.router, m.head = dw.qkv.data_ptr(), dw.o.data_ptr(), dw.router.data_ptr(), dw.head.data_ptr()
+            if S:
+                m.shared = dw.shared.data_ptr()
+                m.shared_stride = dw.shared_bytes
+                m.shared_w2_offset = dw.s_w13_elems * dw.elem_bytes
+            if self.rt is None:
+                m.experts = dw.experts.data_ptr()
+                m.expert_layer_stride = E * dw.expert_bytes
+                m.slot_table = None
+            else:
+                m.experts = self.rt.pool.data_ptr()
+                m.expert_layer_stride = 0
+                m.slot_table = self.rt.slot_dev[1 if kd == "big" else 0].data_ptr()
+            m.expert_stride = dw.expert_bytes
+            m.expert_w2_offset = dw.w13_elems * dw.elem_bytes
+            m.embed, m.pe = dw.embed.data_ptr(), self.pe.data_ptr()
+            m.tok, m.pos = self.tok.data_ptr(), self.pos.data_ptr()
+            m.kc, m.vc = self.sess.kc.data_ptr(), self.sess.vc.data_ptr()
+            m.x, m.xa, m.q, m.att = self.x.data_ptr(), self.xa.data_ptr(), self.q.data_ptr(), self.att.data_ptr()
+            m.U, m.Us, m.Y, m.Ys = self.dpU.data_ptr(), self.dpUs.data_ptr(), self.dpY.data_ptr(), self.dpYs.data_ptr()
+            m.states, m.extra = self.states[kd].data_ptr(), self.extra.data_ptr()
+            m.replay = self.states["little"].data_ptr() if kd == "big" else None
+            m.idx_out, m.gates_out = self.idx[kd].data_ptr(), self.gates[kd].data_ptr()
+            m.active_out = self.active_dev.data_ptr()
+            m.head_logits = None
+            h = self.head[kd]
+            m.conf, m.argmax, m.fallback = h["conf"].data_ptr(), h["argmax"].data_ptr(), h["fallback"].data_ptr()
+            m.flags = self.dp_flags.data_ptr()
+            handle = C.c_void_p()
+            st = N.lib.mobile_dp_create(C.byref(m), C.byref(handle))
+            if st != N.OK:
+                for hh in self.dp.values():
+                    N.lib.mobile_dp_destroy(hh)
+                self.dp = {}
+                if self.persistent:  # explicitly requested
+                    N.check(st, "decode_pass create")
+                return False
+            self.dp[kd] = handle
+            self._dp_models[kd] = m
+        return True
+
+    def dp_info(self, kind: str = "little") -> dict:
+        out = (C.c_int * 4)()
+        N.lib.mobile_dp_info(self.dp[kind], out)
+        return dict(phases=out[0], stages=out[1], smem=out[2], grid=out[3])
+
+    def _dp_launch(self, kind: str, segment: int):
+        K._count()
+        N.check(N.lib.mobile_dp_launch(self.dp[kind], segment, torch.cuda.current_stream().cuda_stream),
+                "decode_pass launch")
+
+    def __del__(self):
+        for h in getattr(self, "dp", {}).values():
+            N.lib.mobile_dp_destroy(h)
+        self.dp = {}
+
     def _whole_pass(self, kind: str):
         """A pass with HBM-resident experts (one graph)."""
+        if self.dp:
+            self._dp_launch(kind, -1)
+            return
         K.embed(self.tok, self.pos, self.dm.dw.embed, self.pe, self.x, ln_out=self.ln)
         x_in = self.x
         for l in range(self.spec.num_layers):
@@ -155,6 +257,11 @@ class StepEngine:
         """Capture the graphs for every pass kind (gamma / reuse are baked in)."""
         self._gamma, self.reuse_gates = gamma, reuse_gates
         L = self.spec.num_layers
+        for h in self.dp.values():
+            N.lib.mobile_dp_destroy(h)
+        self.dp = {}
+        if self.persistent is not False and self.timer is None:
+            self._dp_build(gamma, reuse_gates)
         self._sc = {kd: [None] * L for kd in KINDS}
         self.run = {}
         if self.rt is None:

@@ -1,0 +1,73 @@
+"""Persistent decode-pass kernel (decode_pass.cu) vs the oracle and vs the
+per-op kernel engine on identical weights."""
+from dataclasses import replace
+
+import numpy as np
+import pytest
+import torch
+
+from tests.helpers import OLMOE_MINI, QWEN_MINI, matched, selections_agree
+from tests.test_runtime_gpu import _oracle
+
+pytestmark = pytest.mark.gpu
+
+TOY = dict(num_layers=2, num_experts=16, k_big=4, k_little=2, hidden_dim=256, vocab_size=256, seed=0)
+
+
+@pytest.mark.parametrize("spec_kw,dtype", [(TOY, "float32"), (OLMOE_MINI, "bfloat16"), (QWEN_MINI, "float32")])
+@pytest.mark.parametrize("full", [False, True])
+def test_persistent_matches_oracle(cuda_ok, spec_kw, dtype, full):
+    from paper_2510_12357_b200.runtime import StepEngine
+    o, ms, dm = matched(spec_kw, dtype)
+    eng = StepEngine(dm, 1, 64, persistent=True).build(gamma=0.7)
+    prompt = [3, 17, 42, 7, 9]
+    n = 12
+    flags = [bool(i % 3 == 1) for i in range(n)]
+    eng.prefill(prompt)
+    got = []
+    for i in range(n):
+        tok, fb = eng.step(forced_fallback=flags[i], full=full)
+        lsel = eng.idx["full" if full else "little"][:, 0].cpu().tolist()
+        bsel = eng.idx["big"][:, 0].cpu().tolist() if fb else None
+        got.append((tok, lsel, bsel, eng.states["full" if full else "little"][:, 0].cpu().numpy()))
+    want = _oracle(o, prompt, n, flags, full)
+    assert int(eng.dp_flags.item()) == 0
+    for g, w in zip(got, want):
+        assert selections_agree(g[1], w[1], w[3])[0], (g[1], w[1])
+        if w[2] is not None:
+            assert selections_agree(g[2], w[2], w[3])[0]
+        err = np.abs(g[3] - w[3]).max() / np.abs(w[3]).max()
+        assert err < (1e-4 if dtype == "float32" else 2e-2), err
+    assert [g[0] for g in got] == [w[0] for w in want]
+
+
+@pytest.mark.parametrize("preset", ["c2", "c3", "c4"])
+def test_persistent_equals_per_op_real_shape(cuda_ok, preset):
+    """Real widths (d=2048, 60-64 experts, shared experts), 3 layers: the
+    persistent pass and the per-op engine agree on every selection and token."""
+    from paper_2510_12357_b200.model import DeviceModel
+    from paper_2510_12357_b200.presets import PRESETS
+    from paper_2510_12357_b200.runtime import StepEngine
+    from paper_2510_12357_b200.weights import DeviceWeights
+    spec = replace(PRESETS[preset], num_layers=3)
+    dm = DeviceModel(DeviceWeights.random(spec, torch.device("cuda"), seed=3))
+    a = StepEngine(dm, 1, 96, persistent=True).build()
+    b = StepEngine(dm, 1, 96, persistent=False).build()
+    prompt = np.random.default_rng(0).integers(1, spec.vocab_size, size=40).tolist()
+    stream = np.random.default_rng(1).integers(1, spec.vocab_size, size=16).tolist()
+    a.prefill(prompt)
+    b.prefill(prompt)
+    for i in range(12):
+        fb = i % 4 == 2
+        for e in (a, b):
+            e.step(forced_fallback=fb, next_token=stream[i])
+        for kd in ("little", "big") if fb else ("little",):
+            sa, sb = a.states[kd].cpu().numpy(), b.states[kd].cpu().numpy()
+            assert np.abs(sa - sb).max() <= 1e-3 * np.abs(sb).max()
+            ia, ib = a.idx[kd].cpu().tolist(), b.idx[kd].cpu().tolist()
+            for l in range(spec.num_layers):
+                assert selections_agree([ia[l][0]], [ib[l][0]], sb[l:l + 1, 0], tol=1e-4)[0]
+        ca, cb = a.head["little"]["conf"].item(), b.head["little"]["conf"].item()
+        assert abs(ca - cb) <= 1e-3 * max(cb, 1e-6)
+        assert a.head["little"]["argmax"].item() == b.head["little"]["argmax"].item()
+    assert int(a.dp_flags.item()) == 0

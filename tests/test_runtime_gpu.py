@@ -43,10 +43,11 @@ def _offload_dm(dm, ms):
     return DeviceModel(dw2)
 
 
+@pytest.mark.parametrize("persistent", [False, True])
 @pytest.mark.parametrize("mode", ["resident", "offload"])
 @pytest.mark.parametrize("spec_kw", [QWEN_MINI, DSEEK_MINI, QWEN_MINI_NOPE])
 @pytest.mark.parametrize("full", [False, True])
-def test_step_engine_matches_oracle(cuda_ok, mode, spec_kw, full):
+def test_step_engine_matches_oracle(cuda_ok, mode, spec_kw, full, persistent):
     from paper_2510_12357_b200.offload import OffloadRuntime
     from paper_2510_12357_b200.runtime import StepEngine
     o, ms, dm = matched(spec_kw, "bfloat16")
@@ -54,7 +55,8 @@ def test_step_engine_matches_oracle(cuda_ok, mode, spec_kw, full):
     if mode == "offload":
         dm = _offload_dm(dm, ms)
         rt = OffloadRuntime(dm.dw, slots=ms.num_experts + 2, lookahead=1)
-    eng = StepEngine(dm, 1, 64, runtime=rt).build(gamma=0.7)
+    eng = StepEngine(dm, 1, 64, runtime=rt, persistent=persistent).build(gamma=0.7)
+    assert bool(eng.dp) == persistent
     prompt = [3, 17, 42, 7]
     n = 10
     flags = [bool(i % 3 == 1) for i in range(n)]
