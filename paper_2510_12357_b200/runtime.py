@@ -223,8 +223,10 @@ class StepEngine:
                 "decode_pass launch")
 
     def __del__(self):
-        for h in getattr(self, "dp", {}).values():
-            N.lib.mobile_dp_destroy(h)
+        lib = getattr(N, "lib", None)
+        if lib is not None:
+            for h in getattr(self, "dp", {}).values():
+                lib.mobile_dp_destroy(h)
         self.dp = {}
 
     def _whole_pass(self, kind: str):
