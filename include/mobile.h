@@ -239,7 +239,7 @@ int mobile_combine(const float* x, const float* Y, const float* gates, const int
  *   dense_gemv: y[t, r] = (residual ? residual[t, r] : 0) + (LN?(x[t])) . W[r]
  *               W (N, d) out-major, T <= 8 rows (attention q/k/v and o).
  *   attn_decode: qkv (B, 3d); writes k/v at pos[b] into k/v caches
- *               (B, max_len, d) f32, out (B, d) = softmax(q k^T / sqrt(hd)) v.
+ *               (B, H, max_len, d/H) f32 (head-major), out (B, d) = softmax(q k^T / sqrt(hd)) v.
  *   embed:      x[b] = embed[tok[b]] + pe[pos[b]]  (pe = sinusoidal table);
  *               ln_out (optional) = LN(x[b]).
  *   advance:    pos[b] += 1; tok[b] = next_tok[b] if next_tok.
@@ -370,7 +370,7 @@ typedef struct mobile_dp_model {
   /* state */
   const int* tok;             /* (B,) input token */
   const int* pos;             /* (B,) position */
-  float *kc, *vc;             /* (L, B, max_len, d) */
+  float *kc, *vc;             /* (L, B, H, max_len, d/H) head-major */
   float *x, *xa, *q, *att;    /* (B, d) */
   float *U, *Us, *Y, *Ys;     /* (B*k, ffn), (B*S, shared_ffn), (B*k, d), (B*S, d) */
   float* states;              /* (L, B, E) router logits of this pass */
@@ -393,6 +393,8 @@ int mobile_dp_info(const mobile_dp* p, int* out4); /* phases, stages, smem bytes
 /* optional device buffer (phases x grid x 3 u64): per phase and CTA the
  * globaltimer at [barrier passed, inputs ready, work done]; NULL = off */
 int mobile_dp_set_trace(mobile_dp* p, unsigned long long* trace);
+/* optional event log (grid x 2 roles x 1024 x 2 u64: globaltimer, code<<56 | phase<<32 | item); NULL = off */
+int mobile_dp_set_events(mobile_dp* p, unsigned long long* evt);
 /* segment = -1: the whole pass; else offload segment 0..L */
 int mobile_dp_launch(mobile_dp* p, int segment, void* stream);
 

@@ -126,6 +126,7 @@ _SIGS = {
     "mobile_dp_info": ([P, P], I32),
     "mobile_dp_launch": ([P, I32, P], I32),
     "mobile_dp_set_trace": ([P, P], I32),
+    "mobile_dp_set_events": ([P, P], I32),
 }
 EXPORTED = tuple(_SIGS)
 for _name, (_args, _ret) in _SIGS.items():

@@ -75,6 +75,10 @@ __device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u &
 template <typename W> struct WVec;
 template <> struct WVec<__nv_bfloat16> {
   static constexpr int N = 8;
+  __device__ __forceinline__ static float elem(const uint4& u, int q) {  // q compile-time after unrolling
+    const uint32_t w = q < 2 ? u.x : q < 4 ? u.y : q < 6 ? u.z : u.w;
+    return (q & 1) ? bf16hi(w) : bf16lo(w);
+  }
   __device__ __forceinline__ static void widen(const uint4& u, float* f) {
     f[0] = bf16lo(u.x); f[1] = bf16hi(u.x); f[2] = bf16lo(u.y); f[3] = bf16hi(u.y);
     f[4] = bf16lo(u.z); f[5] = bf16hi(u.z); f[6] = bf16lo(u.w); f[7] = bf16hi(u.w);
@@ -82,6 +86,9 @@ template <> struct WVec<__nv_bfloat16> {
 };
 template <> struct WVec<float> {
   static constexpr int N = 4;
+  __device__ __forceinline__ static float elem(const uint4& u, int q) {
+    return __uint_as_float(q == 0 ? u.x : q == 1 ? u.y : q == 2 ? u.z : u.w);
+  }
   __device__ __forceinline__ static void widen(const uint4& u, float* f) {
     f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y);
     f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);

@@ -56,10 +56,11 @@ constexpr int kMaxE = 256;
 constexpr int kMaxStages = 4;
 constexpr int kMaxGate = 4;                 // shared experts (and sigmoid gates) per layer
 constexpr int kMaxTmpl = 9;
+constexpr int kAttnPart = 4;  // attention partial layout: [m, s, pad, pad, o[hd]]
 
 enum GroupKind { GK_DENSE = 0, GK_SHARED = 1, GK_ROUTED = 2 };
 enum Epi { EP_STORE = 0, EP_RELU = 1, EP_SWIGLU = 2, EP_QKV = 3, EP_LOGITS = 4, EP_HEAD = 5 };
-enum XKind { XK_NONE = 0, XK_LN = 1, XK_PLAIN = 2, XK_COMBINE_LN = 3, XK_EMBED_LN = 4 };
+enum XKind { XK_NONE = 0, XK_LN = 1, XK_PLAIN = 2, XK_COMBINE_LN = 3, XK_EMBED_LN = 4, XK_ATTN = 5 };
 enum PhaseType { PT_GEMV = 0, PT_ATTN = 1, PT_PUBLISH = 2 };
 
 struct Group {
@@ -88,6 +89,8 @@ struct Plan {
   Tmpl t[kMaxTmpl];     // [0, ppl): one layer's phases; [ppl]: head
   int ppl, L, n_phases, bpl, upl, router_j;
   int B, d, H, E, k, S, n_gate, gate_norm, reuse_gates, max_len, V, nc_max, TT;
+  int hd, npi;           // head dim; K/V positions per ring stage
+  int pf_window;         // L2 prefetch distance ahead of the ring, bytes per CTA (0 = off)
   float logit_scale, gamma;
   const int* tok;
   const int* pos;
@@ -114,6 +117,7 @@ struct Plan {
   float* head_part;
   int* flags;
   unsigned long long* trace;  // optional: per (phase, CTA) [barrier passed, inputs ready, work done] ns
+  unsigned long long* evt;    // optional event log: per CTA and role (0 producer, 1 consumers) kEvt x {time, code}
 };
 
 struct Route {          // one layer's selection + permute, in shared memory
@@ -156,10 +160,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
           su32(b)), "r"(parity) : "memory");
 }
+// try_wait with a suspend-time hint: the warp sleeps in hardware until the
+// phase completes or the hint expires (no issue slots burnt polling)
+__device__ __forceinline__ bool mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok) : "r"(su32(b)), "r"(parity), "r"(20000u) : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
       "l"(src), "r"(bytes), "r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   unsigned v;
@@ -196,6 +212,17 @@ __device__ __forceinline__ float reduce_rows16(float (&a)[16][TT], int t, int la
     }
   }
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+constexpr int kEvt = 1024;
+enum EvtCode { EV_W = 1, EV_X = 2, EV_FULL = 3, EV_UNIT = 4, EV_ARRIVE = 5, EV_PASS = 6, EV_READY = 7, EV_ROUTE = 8, EV_WAIT = 9, EV_RED = 10 };
+__device__ __forceinline__ void log_evt(const unsigned long long* base_, int role, int& n, int code, int p, int item) {
+  unsigned long long* base = const_cast<unsigned long long*>(base_);
+  if (base == nullptr || n >= kEvt) return;
+  unsigned long long* e = base + (((size_t)blockIdx.x * 2 + role) * kEvt + n) * 2;
+  e[0] = gtimer();
+  e[1] = ((unsigned long long)code << 56) | ((unsigned long long)(p & 0xffff) << 32) | (unsigned)item;
+  ++n;
 }
 
 constexpr unsigned long long kWatchdogNs = 4000000000ull;  // 4 s: a stuck pass traps instead of hanging
@@ -236,8 +263,8 @@ __device__ __forceinline__ int rot_of(const Plan& P, int j, int l) {
     for (int i = 0; i < j; ++i) c += P.t[i].units;
   return (int)(c % gridDim.x);
 }
-__device__ __forceinline__ Group grp(const Plan& P, int j, int g, int l) {
-  Group G = P.t[j].g[g];
+__device__ __forceinline__ Group grp_t(const Group& G0, int l) {
+  Group G = G0;
   G.w += (long long)l * G.w_l;
   if (G.slot) G.slot += (size_t)l * G.slot_l;
   if (G.out) G.out += (size_t)l * G.out_l;
@@ -250,6 +277,7 @@ __device__ void spin_until(const Plan& P, unsigned target) {
   if (ld_relaxed(P.sync) < target) {
     const unsigned long long t0 = gtimer();
     while (ld_relaxed(P.sync) < target) {
+      __nanosleep(64);
       if (gtimer() - t0 > kWatchdogNs) {
         atomicOr(P.flags, 4);
         __trap();
@@ -260,92 +288,116 @@ __device__ void spin_until(const Plan& P, unsigned target) {
 }
 
 // ------------------------------------------------------------------ routing
-// One warp: stable top-k (toymoe.py:80-88 key order: value desc, index asc,
+// One warp: stable top-k (toymoe.py:80-88 order: value desc, index asc,
 // -0.0 == +0.0), replay (toymoe.py:194-200), gate softmax in selection order
 // (toymoe.py:201) or HF softmax-over-all, then the deterministic permute of
 // the B*k (token, slot) pairs sorted by (expert, pair) (permute.cu contract).
-__device__ void compute_route(const Plan& P, int l, Route& R, bool publish) {
+// Ranks are computed by all-pairs comparison (independent broadcasts, no
+// dependent shuffle chains): expert e is selected at position rank(e) < k.
+template <int kPer>
+__device__ __forceinline__ void compute_route_k(const Plan& P, int l, Route& R, bool publish) {
   const int lane = threadIdx.x & 31;
   const int E = P.E, k = P.k, B = P.B;
-  constexpr int kPer = kMaxE / 32;
   bool bad = false;
   for (int b = 0; b < B; ++b) {
     const float* own = P.states + ((size_t)l * B + b) * E;
     const float* rep = P.replay ? P.replay + ((size_t)l * B + b) * E : nullptr;
     const float* sel_src = rep ? rep : own;
     const float* gate_src = (rep && P.reuse_gates) ? rep : own;
-    unsigned long long key[kPer];
+    uint32_t key[kPer];
+    float gv[kPer];
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const int e = lane + 32 * i;
-      if (e < E) {
-        const float v = __ldcg(sel_src + e);
-        bad |= !isfinite(v);
-        key[i] = topk_key(v, e);
-      } else {
-        key[i] = 0ull;
+      const float v = e < E ? __ldcg(sel_src + e) : 0.f;
+      gv[i] = e < E ? (gate_src == sel_src ? v : __ldcg(gate_src + e)) : -INFINITY;
+      bad |= e < E && !isfinite(v);
+      key[i] = e < E ? order_key_f32(v) : 0u;
+    }
+    int rank[kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) rank[i] = 0;
+#pragma unroll 4
+    for (int j = 0; j < E; ++j) {  // compact runtime loop: keeps the kernel's code small (i-cache)
+      uint32_t kown = key[0];
+#pragma unroll
+      for (int i = 1; i < kPer; ++i)
+        if ((j >> 5) == i) kown = key[i];
+      const uint32_t kj = __shfl_sync(0xffffffffu, kown, j & 31);
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const int e = lane + 32 * i;
+        rank[i] += (kj > key[i] || (kj == key[i] && j < e)) ? 1 : 0;
       }
     }
-    int sel_local = -1;
-    for (int j = 0; j < k; ++j) {
-      unsigned long long best = 0ull;
 #pragma unroll
-      for (int i = 0; i < kPer; ++i) best = key[i] > best ? key[i] : best;
-      best = warp_max_u64(best);
-      const int e = topk_key_index(best);
+    for (int i = 0; i < kPer; ++i) {
+      const int e = lane + 32 * i;
+      if (e < E && rank[i] < k) {
+        R.idx[b * k + rank[i]] = (short)e;
+        R.gates[b * k + rank[i]] = gv[i];  // raw gate logit, normalised below
+      }
+    }
+    float zall = 0.f, mall = -INFINITY;
+    if (P.gate_norm != MOBILE_GATE_SELECTED_SOFTMAX) {
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) mall = fmaxf(mall, gv[i]);
+      mall = warp_max(mall);
 #pragma unroll
       for (int i = 0; i < kPer; ++i)
-        if (key[i] == best) key[i] = 0ull;
-      if (lane == j) sel_local = e;
+        if (lane + 32 * i < E) zall += expf(gv[i] - mall);
+      zall = warp_sum(zall);
     }
-    if (lane < k) R.idx[b * k + lane] = sel_local;
-    if (P.gate_norm == MOBILE_GATE_SELECTED_SOFTMAX) {
-      const float gl = lane < k ? __ldcg(gate_src + sel_local) : -INFINITY;
-      const float m = warp_max(gl);
-      const float ex = lane < k ? expf(gl - m) : 0.f;
-      float s = 0.f;
-      for (int j = 0; j < k; ++j) s += __shfl_sync(0xffffffffu, ex, j);
-      if (lane < k) R.gates[b * k + lane] = ex / s;
-    } else {
-      float m = -INFINITY;
-      for (int e = lane; e < E; e += 32) m = fmaxf(m, __ldcg(gate_src + e));
-      m = warp_max(m);
-      float z = 0.f;
-      for (int e = lane; e < E; e += 32) z += expf(__ldcg(gate_src + e) - m);
-      z = warp_sum(z);
-      if (lane < k) R.gates[b * k + lane] = expf(__ldcg(gate_src + sel_local) - m) / z;
+    __syncwarp();
+    if (lane < k) {
+      const float gl = R.gates[b * k + lane];
+      float g;
+      if (P.gate_norm == MOBILE_GATE_SELECTED_SOFTMAX) {  // softmax over the selection, summed in order
+        float m = -INFINITY;
+#pragma unroll 1
+        for (int j = 0; j < k; ++j) m = fmaxf(m, R.gates[b * k + j]);
+        float s = 0.f;
+#pragma unroll 1
+        for (int j = 0; j < k; ++j) s += expf(R.gates[b * k + j] - m);
+        g = expf(gl - m) / s;
+      } else {
+        g = expf(gl - mall) / zall;
+      }
+      __syncwarp(__activemask());
+      R.gates[b * k + lane] = g;
     }
+    __syncwarp();
   }
-  __syncwarp();
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(P.flags, 1);
-  // permute: bitonic sort of (expert << 6 | pair) over <= 32 pairs
+  // permute: pairs sorted by (expert, pair); active experts in ascending order
   const int NP = B * k;
-  int key = 0x7fffffff;
-  if (lane < NP) key = (R.idx[lane] << 6) | lane;
-#pragma unroll
-  for (int kk = 2; kk <= 32; kk <<= 1) {
-#pragma unroll
-    for (int j = kk >> 1; j > 0; j >>= 1) {
-      const int other = __shfl_xor_sync(0xffffffffu, key, j);
-      const bool up = (lane & kk) == 0, lower = (lane & j) == 0;
-      key = (lower == up) ? min(key, other) : max(key, other);
+  int e_me = 0x7fff, pos = 0, first = 0, cnt = 0, a_me = 0;
+  if (lane < NP) {
+    e_me = R.idx[lane];
+    first = 1;
+#pragma unroll 1
+    for (int q = 0; q < NP; ++q) {
+      const int eq = R.idx[q];
+      pos += (eq < e_me || (eq == e_me && q < lane)) ? 1 : 0;
+      cnt += eq == e_me ? 1 : 0;
+      if (eq == e_me && q < lane) first = 0;
     }
   }
-  const bool valid = lane < NP;
-  const int e_me = valid ? (key >> 6) : 0x7fffffff;
-  if (valid) R.pairs[lane] = key & 63;
-  const int e_prev = __shfl_up_sync(0xffffffffu, e_me, 1);
-  const bool first = valid && (lane == 0 || e_prev != e_me);
-  const unsigned fm = __ballot_sync(0xffffffffu, first);
-  const int nact = __popc(fm);
-  if (first) {
-    const int a = __popc(fm & ((1u << lane) - 1u));
-    R.act_e[a] = e_me;
-    R.act_p0[a] = lane;
-    const unsigned after = fm & ~((2u << lane) - 1u);  // next first-lane above me
-    const int end = after ? __ffs(after) - 1 : NP;
-    R.act_n[a] = end - lane;
+  const unsigned fm = __ballot_sync(0xffffffffu, lane < NP && first);
+#pragma unroll 1
+  for (int q = 0; q < NP; ++q) {  // active index = distinct experts below mine
+    const int eq = __shfl_sync(0xffffffffu, e_me, q);
+    a_me += (((fm >> q) & 1u) && eq < e_me) ? 1 : 0;
   }
+  if (lane < NP) {
+    R.pairs[pos] = (short)lane;
+    if (first) {
+      R.act_e[a_me] = (short)e_me;
+      R.act_p0[a_me] = (short)(pos);
+      R.act_n[a_me] = (short)cnt;
+    }
+  }
+  const int nact = __popc(fm);
   if (lane == 0) R.n_active = nact;
   __syncwarp();
   if (publish) {
@@ -354,11 +406,16 @@ __device__ void compute_route(const Plan& P, int l, Route& R, bool publish) {
       P.gates_out[(size_t)l * NP + i] = R.gates[i];
     }
     if (P.active_out) {
-      int* a = P.active_out + (size_t)l * (E + 1);
-      if (lane == 0) a[0] = nact;
-      if (lane < nact) a[1 + lane] = R.act_e[lane];
+      int* ao = P.active_out + (size_t)l * (E + 1);
+      if (lane == 0) ao[0] = nact;
+      if (lane < nact) ao[1 + lane] = R.act_e[lane];
     }
   }
+}
+
+__device__ __forceinline__ void compute_route(const Plan& P, int l, Route& R, bool publish) {
+  if (P.E <= 64) compute_route_k<2>(P, l, R, publish);
+  else compute_route_k<8>(P, l, R, publish);
 }
 
 // ------------------------------------------------------------------ work items
@@ -366,26 +423,36 @@ __device__ void compute_route(const Plan& P, int l, Route& R, bool publish) {
 // units u with (u + rot) % G == c; an item is (unit, K chunk).
 struct Item {           // everything the producer and the consumers need about one unit
   int g, a, rb, rr, nkc, n;
+  int routed;
+  int attn, b, h, c, p0, np;  // attention unit: sequence, head, chunk of old positions [p0, p0 + np)
   int K, rows, epi, xstage, out_ld, split;
   const char* wrow;     // first byte of the tile's rows (chunk 0)
   const float* xg;
   float* out;
   float* out2;
   const float* resid;
-  int pr[kMaxB];        // output pair index per token slot
-  int tb[kMaxB];        // token per slot
+  int kind;
 };
+// output pair / token of token slot t of a unit (no per-unit arrays: they
+// would be indexed dynamically in the epilogue and land in local memory)
+__device__ __forceinline__ int unit_pair(const Plan& P, const Item& it, const Route& R, int t) {
+  if (it.kind == GK_ROUTED) return R.pairs[R.act_p0[it.a] + t];
+  if (it.kind == GK_SHARED) return t * P.S + it.a;
+  return t;
+}
+__device__ __forceinline__ int unit_token(const Plan& P, const Item& it, const Route& R, int t) {
+  return it.kind == GK_ROUTED ? R.pairs[R.act_p0[it.a] + t] / P.k : t;
+}
 
 // decode unit u of (template j, layer l); false = no work (inactive routed slot)
 template <typename W>
-__device__ bool decode_unit(const Plan& P, int j, int l, int u, const Route& R, Item& it) {
-  const Tmpl& T = P.t[j];
+__device__ __forceinline__ bool decode_unit(const Plan& P, const Tmpl& T, int l, int u, const Route& R, Item& it) {
   int uu = u, g = 0;
   for (; g < T.n_groups - 1; ++g) {
     if (uu < T.g[g].units) break;
     uu -= T.g[g].units;
   }
-  const Group G = grp(P, j, g, l);
+  const Group G = grp_t(T.g[g], l);
   const int upe = (G.rows + kTileRows - 1) / kTileRows;
   const int a = uu / upe;
   it.g = g;
@@ -400,28 +467,42 @@ __device__ bool decode_unit(const Plan& P, int j, int l, int u, const Route& R, 
     const int s = G.slot ? G.slot[e] : e;
     base = G.w + (long long)s * G.stride;
     it.n = R.act_n[a];
-#pragma unroll
-    for (int t = 0; t < kMaxB; ++t) {
-      const int q = t < it.n ? R.pairs[R.act_p0[a] + t] : 0;
-      it.pr[t] = q;
-      it.tb[t] = q / P.k;
-    }
   } else if (G.kind == GK_SHARED) {
     base = G.w + (long long)a * G.stride;
     it.n = P.B;
-#pragma unroll
-    for (int t = 0; t < kMaxB; ++t) { it.pr[t] = t * P.S + a; it.tb[t] = t; }
   } else {
     base = G.w;
     it.n = P.B;
-#pragma unroll
-    for (int t = 0; t < kMaxB; ++t) { it.pr[t] = t; it.tb[t] = t; }
   }
   it.wrow = base + (size_t)it.rb * kTileRows * G.K * sizeof(W);
+  it.attn = 0;
+  it.routed = G.kind == GK_ROUTED;
+  it.kind = G.kind;
   it.K = G.K; it.rows = G.rows; it.epi = G.epi; it.xstage = G.xstage; it.out_ld = G.out_ld; it.split = G.split;
   it.xg = G.xg; it.out = G.out; it.out2 = G.out2; it.resid = G.resid;
   return true;
 }
+// Attention units: (sequence b, head h, chunk c) over the positions [0, pos)
+// already in the KV cache; the new position's K/V (written by this pass's
+// qkv phase) is added by the last chunk.  nc chunks per head, B*H*nc <= grid.
+__device__ __forceinline__ int attn_nc(const Plan& P, const int* spos) {
+  int ctx = 1;
+  for (int b = 0; b < P.B; ++b) ctx = max(ctx, spos[b] + 1);
+  return max(1, min(min((int)gridDim.x / (P.B * P.H), P.nc_max), (ctx + 7) / 8));
+}
+__device__ __forceinline__ void decode_attn(const Plan& P, int u, int nc, const int* spos, Item& it) {
+  it.attn = 1;
+  it.routed = 0;
+  it.b = u / (P.H * nc);
+  const int r = u - it.b * P.H * nc;
+  it.h = r / nc;
+  it.c = r - it.h * nc;
+  const int old = spos[it.b];
+  it.p0 = (int)((long long)old * it.c / nc);
+  it.np = (int)((long long)old * (it.c + 1) / nc) - it.p0;
+  it.nkc = (it.np + P.npi - 1) / P.npi;
+}
+
 __device__ __forceinline__ int group_of_unit(const Tmpl& T, int u) {
   int g = 0;
   for (; g < T.n_groups - 1; ++g) {
@@ -483,6 +564,47 @@ __device__ void load_x(const Plan& P, int xkind, const float* xsrc, float* xdst,
     for (int i = tid + 4 * kCW * 32; i < B * nv; i += kCW * 32) xb4[i] = __ldcg(src + i);
     cbar();
     if (xkind == XK_LN) block_ln_rows(xbuf, B, d, red);
+  } else if (xkind == XK_ATTN) {
+    // att[b, h*hd + e] = merge of the head's chunk partials (chunk order): one
+    // warp per (b, h); lane c holds chunk c's (m, s); two parallel round trips
+    const int hd = P.hd, nc = attn_nc(P, spos), lane = tid & 31, warp = tid >> 5;
+    for (int bh = warp; bh < B * P.H; bh += kCW) {
+      const float* base = P.attn_part + (size_t)bh * P.nc_max * (hd + kAttnPart);
+      float mc = -INFINITY, sc = 0.f;
+      if (lane < nc) {
+        const float2 ms = __ldcg(reinterpret_cast<const float2*>(base + (size_t)lane * (hd + kAttnPart)));
+        mc = ms.x;
+        sc = ms.y;
+      }
+      const float M = warp_max(sc != 0.f ? mc : -INFINITY);
+      const float f = sc != 0.f ? expf(mc - M) : 0.f;
+      float S = 0.f;
+      for (int c = 0; c < nc; ++c) S += __shfl_sync(0xffffffffu, sc * f, c);
+      const float inv = 1.0f / S;
+      const int b = bh / P.H, h = bh - b * P.H;
+      for (int e0 = 0; e0 < hd; e0 += 128) {  // warp-uniform trip count (shuffles below)
+        const int e = e0 + lane * 4;
+        const bool act = e < hd;
+        float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c0 = 0; c0 < nc; c0 += 8) {
+          float4 o4[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            if (act && c0 + c < nc)
+              o4[c] = __ldcg(reinterpret_cast<const float4*>(base + (size_t)(c0 + c) * (hd + kAttnPart) + kAttnPart + e));
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float fc = __shfl_sync(0xffffffffu, f, (c0 + c) & 31);
+            if (act && c0 + c < nc && fc != 0.f) {
+              O.x = fmaf(o4[c].x, fc, O.x); O.y = fmaf(o4[c].y, fc, O.y);
+              O.z = fmaf(o4[c].z, fc, O.z); O.w = fmaf(o4[c].w, fc, O.w);
+            }
+          }
+        }
+        if (act) xb4[((size_t)b * d + h * hd + e) / 4] = make_float4(O.x * inv, O.y * inv, O.z * inv, O.w * inv);
+      }
+    }
+    cbar();
   } else if (xkind == XK_EMBED_LN) {  // x = embed[tok] + pe[pos]   (toymoe.py:172)
     for (int b = 0; b < B; ++b) {
       const float4* er = reinterpret_cast<const float4*>(P.embed + (size_t)P.tok[b] * d);
@@ -549,145 +671,104 @@ __device__ void load_x(const Plan& P, int xkind, const float* xsrc, float* xdst,
 
 // ------------------------------------------------------------------ attention
 // Single-query attention over the KV cache (toymoe.py:178-186 at one
-// position).  Items (b, h, chunk) are spread over the grid; each CTA's warps
-// run an online softmax over interleaved positions, merge in warp order, and
-// write a partial; the last chunk of a head to finish merges the partials in
-// chunk order (ticket) into att.
+// position).  A unit's K and V position blocks arrive through the weight ring
+// (they are static during the pass); each warp runs an online softmax over
+// its positions (4 in flight), the warps merge in warp order and the unit's
+// partial (m, s, o) goes to global memory.  The o-projection's input build
+// merges the chunks of every head in chunk order (XK_ATTN).
+
 template <int PER>
-__device__ void attn_item(const Plan& P, int l, int b, int h, int c, int nc, int ctx, float* scratch,
-                          bool& last_s) {
-  constexpr int NB = PER <= 2 ? 8 : PER == 4 ? 6 : 3;  // positions in flight per warp
+__device__ void attn_unit(const Plan& P, int l, const Item& it, int nc, const char* smem, int stage_bytes, int nst,
+                          uint32_t& ic, uint64_t* full, uint64_t* empty, float* scratch, const int* spos) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int H = P.H, d = P.d, hd = PER * 32, B = P.B;
   const float scale = 1.0f / sqrtf((float)hd);
-  const int p0 = (int)((long long)ctx * c / nc), p1 = (int)((long long)ctx * (c + 1) / nc);
   float qv[PER], o[PER];
-  const float* qrow = P.q + (size_t)b * d + h * hd;
+  const float* qrow = P.q + (size_t)it.b * d + it.h * hd;
 #pragma unroll
   for (int j = 0; j < PER; ++j) { qv[j] = __ldcg(qrow + lane + 32 * j); o[j] = 0.f; }
   float m = -INFINITY, s = 0.f;
-  const size_t cache0 = ((size_t)l * B + b) * P.max_len;
-  for (int base = p0 + warp; base < p1; base += kCW * NB) {
-    float kv[NB][PER], vv[NB][PER];
+  auto update = [&](float sc, const float* vr) {
+    const float v = sc * scale;
+    const float mn = fmaxf(m, v);
+    const float a = expf(m - mn), e = expf(v - mn);
+    s = s * a + e;
 #pragma unroll
-    for (int n = 0; n < NB; ++n) {
-      const int p = base + kCW * n;
-      const bool ok = p < p1;
-      const float* kr = P.kc + (cache0 + (ok ? p : p0)) * d + h * hd;
-      const float* vr = P.vc + (cache0 + (ok ? p : p0)) * d + h * hd;
+    for (int j = 0; j < PER; ++j) o[j] = o[j] * a + e * vr[lane + 32 * j];
+    m = mn;
+  };
+  for (int item = 0; item < it.nkc; ++item, ++ic) {
+    const int st = (int)(ic % (uint32_t)nst);
+    const int n = min(P.npi, it.np - item * P.npi);
+    mbar_wait(&full[st], (ic / nst) & 1u);
+    const float* Ks = reinterpret_cast<const float*>(smem + (size_t)st * stage_bytes);
+    const float* Vs = Ks + (size_t)P.npi * hd;
+    for (int j0 = warp; j0 < n; j0 += kCW * 4) {
+      float sc[4];
 #pragma unroll
-      for (int j = 0; j < PER; ++j) {
-        kv[n][j] = ok ? __ldcg(kr + lane + 32 * j) : 0.f;
-        vv[n][j] = ok ? __ldcg(vr + lane + 32 * j) : 0.f;
+      for (int t = 0; t < 4; ++t) {
+        const int j = min(j0 + kCW * t, n - 1);
+        float dot = 0.f;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) dot = fmaf(qv[e], Ks[(size_t)j * hd + lane + 32 * e], dot);
+        sc[t] = dot;
       }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) sc[t] += __shfl_xor_sync(0xffffffffu, sc[t], off);
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (j0 + kCW * t < n) update(sc[t], Vs + (size_t)(j0 + kCW * t) * hd);
     }
-    float sc[NB];
-#pragma unroll
-    for (int n = 0; n < NB; ++n) {
-      float dot = 0.f;
-#pragma unroll
-      for (int j = 0; j < PER; ++j) dot = fmaf(qv[j], kv[n][j], dot);
-      sc[n] = dot;
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-      for (int n = 0; n < NB; ++n) sc[n] += __shfl_xor_sync(0xffffffffu, sc[n], off);
-#pragma unroll
-    for (int n = 0; n < NB; ++n) {
-      if (base + kCW * n >= p1) break;
-      const float v = sc[n] * scale;
-      const float mn = fmaxf(m, v);
-      const float a = expf(m - mn), e = expf(v - mn);
-      s = s * a + e;
-#pragma unroll
-      for (int j = 0; j < PER; ++j) o[j] = o[j] * a + e * vv[n][j];
-      m = mn;
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
   }
-  // warp partials -> smem, merged in warp order by warp 0
-  float* wp = scratch + (size_t)warp * (hd + 2);
+  if (it.c == nc - 1 && warp == 0) {  // the new position, written by this pass's qkv phase
+    const size_t row = (((size_t)l * B + it.b) * H + it.h) * P.max_len + spos[it.b];
+    const float* kr = P.kc + row * hd;
+    const float* vr = P.vc + row * hd;
+    float kv[PER], vv[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) { kv[e] = __ldcg(kr + lane + 32 * e); vv[e] = __ldcg(vr + lane + 32 * e); }
+    float dot = 0.f;
+#pragma unroll
+    for (int e = 0; e < PER; ++e) dot = fmaf(qv[e], kv[e], dot);
+    dot = warp_sum(dot);
+    const float v = dot * scale;
+    const float mn = fmaxf(m, v);
+    const float a = expf(m - mn), e2 = expf(v - mn);
+    s = s * a + e2;
+#pragma unroll
+    for (int e = 0; e < PER; ++e) o[e] = o[e] * a + e2 * vv[e];
+    m = mn;
+  }
+  // warps -> smem -> merged in warp order by warp 0 -> partial
+  float* wp = scratch + (size_t)warp * (hd + kAttnPart);
   if (lane == 0) { wp[0] = m; wp[1] = s; }
 #pragma unroll
-  for (int j = 0; j < PER; ++j) wp[2 + lane + 32 * j] = o[j];
+  for (int e = 0; e < PER; ++e) wp[kAttnPart + lane + 32 * e] = o[e];
   cbar();
   if (warp == 0) {
-    float* part = P.attn_part + ((size_t)(b * H + h) * P.nc_max + c) * (hd + 2);
     float M = -INFINITY;
-    for (int w = 0; w < kCW; ++w) M = fmaxf(M, scratch[(size_t)w * (hd + 2)]);
-    float Ssum = 0.f, acc[PER];
+    for (int w = 0; w < kCW; ++w) M = fmaxf(M, scratch[(size_t)w * (hd + kAttnPart)]);
+    float S = 0.f, acc[PER];
 #pragma unroll
-    for (int j = 0; j < PER; ++j) acc[j] = 0.f;
+    for (int e = 0; e < PER; ++e) acc[e] = 0.f;
     for (int w = 0; w < kCW; ++w) {
-      const float* q = scratch + (size_t)w * (hd + 2);
+      const float* q = scratch + (size_t)w * (hd + kAttnPart);
       if (q[1] == 0.f) continue;
       const float f = expf(q[0] - M);
-      Ssum += q[1] * f;
+      S += q[1] * f;
 #pragma unroll
-      for (int j = 0; j < PER; ++j) acc[j] += q[2 + lane + 32 * j] * f;
+      for (int e = 0; e < PER; ++e) acc[e] += q[kAttnPart + lane + 32 * e] * f;
     }
-    if (lane == 0) { part[0] = M; part[1] = Ssum; }
+    float* part = P.attn_part + ((size_t)(it.b * H + it.h) * P.nc_max + it.c) * (hd + kAttnPart);
+    if (lane == 0) { part[0] = M; part[1] = S; }
 #pragma unroll
-    for (int j = 0; j < PER; ++j) part[2 + lane + 32 * j] = acc[j];
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) last_s = atomicAdd(P.sync + 64 + b * H + h, 1u) == (unsigned)(nc - 1);
-    __syncwarp();
-    if (last_s) {  // last chunk of this head: merge the partials in chunk order
-      __threadfence();
-      const float* base = P.attn_part + (size_t)(b * H + h) * P.nc_max * (hd + 2);
-      float mm[16], ss[16];
-#pragma unroll
-      for (int cc = 0; cc < 16; ++cc) {
-        mm[cc] = cc < nc ? __ldcg(base + (size_t)cc * (hd + 2)) : -INFINITY;
-        ss[cc] = cc < nc ? __ldcg(base + (size_t)cc * (hd + 2) + 1) : 0.f;
-      }
-      float MM = -INFINITY;
-      for (int cc = 0; cc < nc; ++cc) MM = fmaxf(MM, cc < 16 ? mm[cc] : __ldcg(base + (size_t)cc * (hd + 2)));
-      float SS = 0.f;
-#pragma unroll
-      for (int j = 0; j < PER; ++j) acc[j] = 0.f;
-      for (int cc = 0; cc < nc; ++cc) {
-        const float* q = base + (size_t)cc * (hd + 2);
-        const float sq = cc < 16 ? ss[cc] : __ldcg(q + 1);
-        if (sq == 0.f) continue;
-        const float f = expf((cc < 16 ? mm[cc] : __ldcg(q)) - MM);
-        SS += sq * f;
-#pragma unroll
-        for (int j = 0; j < PER; ++j) acc[j] += __ldcg(q + 2 + lane + 32 * j) * f;
-      }
-      const float inv = 1.0f / SS;
-#pragma unroll
-      for (int j = 0; j < PER; ++j) P.att[(size_t)b * d + h * hd + lane + 32 * j] = acc[j] * inv;
-      if (lane == 0) P.sync[64 + b * H + h] = 0u;
-    }
+    for (int e = 0; e < PER; ++e) part[kAttnPart + lane + 32 * e] = acc[e];
   }
   cbar();
-}
-
-// Single-query attention over the KV cache (toymoe.py:178-186 at one
-// position).  Items (b, h, chunk) are spread over the grid; each warp keeps
-// NB positions of K/V in flight, runs an online softmax over them, the warps
-// merge in warp order and write a partial; the last chunk of a head to finish
-// merges the partials in chunk order (ticket) into att.
-__device__ void attn_phase(const Plan& P, int layer, float* scratch, int rot, const int* spos) {
-  const int B = P.B, H = P.H, hd = P.d / H;
-  const int G = gridDim.x;
-  __shared__ bool last_s;
-  int ctx_max = 1;
-  for (int b = 0; b < B; ++b) ctx_max = max(ctx_max, spos[b] + 1);
-  const int nc = max(1, min(min(G / (B * H), P.nc_max), (ctx_max + 7) / 8));
-  for (int i = ((int)blockIdx.x - rot % G + G) % G; i < B * H * nc; i += G) {
-    const int b = i / (H * nc), r = i - b * H * nc;
-    const int h = r / nc, c = r - h * nc;
-    const int ctx = spos[b] + 1;
-    switch (hd / 32) {
-      case 1: attn_item<1>(P, layer, b, h, c, nc, ctx, scratch, last_s); break;
-      case 2: attn_item<2>(P, layer, b, h, c, nc, ctx, scratch, last_s); break;
-      case 4: attn_item<4>(P, layer, b, h, c, nc, ctx, scratch, last_s); break;
-      default: attn_item<8>(P, layer, b, h, c, nc, ctx, scratch, last_s); break;
-    }
-  }
 }
 
 __device__ __forceinline__ void online_add(float& m, float& s, int& arg, float l, int idx) {
@@ -716,6 +797,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
   __shared__ StageMeta meta[kMaxStages];
   __shared__ Route rt_c, rt_p;
   __shared__ int spos[kMaxB];
+  __shared__ __align__(16) Tmpl cph, pph;  // consumers' / producer's copy of the current phase template
   __shared__ __align__(16) float red2[kCW * kTileRows * TT];  // cross-warp row sums / LN / head merge
   __shared__ bool is_last;
   float* red = red2;
@@ -742,15 +824,37 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
     // matrices: always; routed experts: once the layer's selection is).
     // Activation cursor (X): issues the staged activation slices of items
     // whose inputs come from the previous phase, once its barrier completed.
+    int nev = 0;                  // event-log count (debug)
     int wp = first, wu = 0, wkc = 0, wj = 0, wl = 0;
     unsigned wtgt = 0;            // barrier count after which this phase's activations exist
     Item wit;
     int rt_layer = -1;
-    auto seek = [&](bool fresh) -> int {  // 0 = ok, 1 = done, 2 = blocked on routing (warp-uniform)
+    int pph_j = -1;
+    bool fresh = true;
+    auto seek = [&]() -> int {  // 0 = ok, 1 = done, 2 = blocked on routing (warp-uniform)
       while (wp < last) {
         phase_jl(P, wp, wj, wl);
-        const Tmpl& T = P.t[wj];
-        if (T.type != PT_GEMV) { ++wp; fresh = true; continue; }
+        if (pph_j != wj) {  // template -> shared memory (one constant-bank read per phase)
+          __syncwarp();
+          const int4* src = reinterpret_cast<const int4*>(&P.t[wj]);
+          int4* dst = reinterpret_cast<int4*>(&pph);
+          for (int i = lane; i < (int)(sizeof(Tmpl) / 16); i += 32) dst[i] = src[i];
+          __syncwarp();
+          pph_j = wj;
+        }
+        const Tmpl& T = pph;
+        if (T.type == PT_PUBLISH) { ++wp; fresh = true; continue; }
+        if (T.type == PT_ATTN) {  // K/V blocks of the positions already cached
+          if (fresh) { wu = (blockIdx.x - rot_of(P, wj, wl) + G) % G; wkc = 0; fresh = false; }
+          const int nc = attn_nc(P, spos);
+          for (; wu < P.B * P.H * nc; wu += G) {
+            decode_attn(P, wu, nc, spos, wit);
+            if (wit.nkc > 0) return 0;
+          }
+          ++wp;
+          fresh = true;
+          continue;
+        }
         if (fresh) {
           wu = (blockIdx.x - rot_of(P, wj, wl) + G) % G;
           wkc = 0;
@@ -771,8 +875,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
             fence_acq_rel();
             compute_route(P, wl, rt_p, false);
             rt_layer = wl;
+            if (lane == 0) log_evt(P.evt, 0, nev, EV_ROUTE, wp, 0);
           }
-          if (decode_unit<W>(P, wj, wl, wu, rt_p, wit)) return 0;
+          if (decode_unit<W>(P, T, wl, wu, rt_p, wit)) return 0;
           wu += G;
         }
         ++wp;
@@ -780,13 +885,65 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
       }
       return 1;
     };
-    int st = seek(true);
+    int st = 2;  // 2 = (re)seek needed
+    // ---- L2 prefetch cursor: walks the same unit sequence ahead of the ring
+    // and pulls static tiles (dense / shared weights, cached K/V blocks) into
+    // L2 with cp.async.bulk.prefetch, so HBM keeps streaming while the ring is
+    // full and the consumers wait on a barrier.  Routed units are skipped (their
+    // address is only known after routing); it never blocks.
+    int pp = first, pu = 0, pj = 0, pl = 0;
+    bool pfresh = true, pdone = false;
+    unsigned long long pf_bytes = 0, w_static = 0;  // prefetched / issued-by-W static bytes
+    const unsigned long long pf_window = (unsigned long long)P.pf_window;
+    auto pf_step = [&]() -> bool {  // one unit; false = nothing left
+      while (pp < last) {
+        phase_jl(P, pp, pj, pl);
+        const Tmpl& T = P.t[pj];
+        if (T.type == PT_PUBLISH) { ++pp; pfresh = true; continue; }
+        if (pfresh) { pu = (blockIdx.x - rot_of(P, pj, pl) + G) % G; pfresh = false; }
+        if (T.type == PT_ATTN) {
+          const int nc = attn_nc(P, spos);
+          if (pu < P.B * P.H * nc) {
+            Item a;
+            decode_attn(P, pu, nc, spos, a);
+            pu += G;
+            if (a.np > 0) {
+              const uint32_t bytes = (uint32_t)a.np * P.hd * 4u;
+              const size_t row = (((size_t)pl * P.B + a.b) * P.H + a.h) * P.max_len + a.p0;
+              if (lane == 0) { prefetch_l2(P.kc + row * P.hd, bytes); prefetch_l2(P.vc + row * P.hd, bytes); }
+              pf_bytes += 2ull * bytes;
+            }
+            return true;
+          }
+        } else if (pu < T.units) {
+          const int g = group_of_unit(T, pu);
+          const Group& Gg = T.g[g];
+          if (Gg.kind != GK_ROUTED) {
+            int uu = pu;
+            for (int i = 0; i < g; ++i) uu -= T.g[i].units;
+            const int upe = (Gg.rows + kTileRows - 1) / kTileRows;
+            const int a = uu / upe, rb = uu - a * upe;
+            const int rr = min(kTileRows, Gg.rows - rb * kTileRows);
+            const char* w = Gg.w + (long long)pl * Gg.w_l + (Gg.kind == GK_SHARED ? (long long)a * Gg.stride : 0ll) +
+                            (size_t)rb * kTileRows * Gg.K * sizeof(W);
+            const uint32_t bytes = (uint32_t)((size_t)rr * Gg.K * sizeof(W));
+            if (lane == 0) prefetch_l2(w, bytes);
+            pf_bytes += bytes;
+          }
+          pu += G;
+          return true;
+        }
+        ++pp;
+        pfresh = true;
+      }
+      return false;
+    };
     uint32_t iw = 0, ix = 0;      // items issued (weights) / completed (activations)
     unsigned long long t0 = 0;
     unsigned seen = 0;            // last observed barrier counter
     while (true) {
       bool progress = false;
-      if (st == 2) st = seek(false);
+      if (st == 2) st = seek();
       // ---- weight cursor
       if (st == 0 && iw < ix + (uint32_t)nst) {
         const int s = (int)(iw % (uint32_t)nst);
@@ -796,10 +953,34 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
           if (lane == 0) ok = mbar_test(&empty[s], ((iw / nst) - 1) & 1u) ? 1u : 0u;
           free_ = __shfl_sync(0xffffffffu, ok, 0) != 0;
         }
-        if (free_) {
+        if (free_ && wit.attn) {
+          const int q0 = wit.p0 + wkc * P.npi;
+          const int n = min(P.npi, wit.p0 + wit.np - q0);
+          const uint32_t bytes = (uint32_t)n * P.hd * 4u;
+          if (lane == 0) {
+            if (iw >= (uint32_t)nst) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            meta[s].needx = 0;
+            char* stg = smem + (size_t)s * stage_bytes;
+            const size_t row = (((size_t)wl * P.B + wit.b) * P.H + wit.h) * P.max_len + q0;
+            mbar_arrive_tx(&full[s], 2u * bytes);
+            bulk_g2s(stg, P.kc + row * P.hd, bytes, &full[s]);
+            bulk_g2s(stg + (size_t)P.npi * P.hd * 4, P.vc + row * P.hd, bytes, &full[s]);
+          }
+          w_static += 2ull * bytes;
+          if (lane == 0) log_evt(P.evt, 0, nev, EV_W, wp, (int)iw);
+          ++iw;
+          progress = true;
+          if (++wkc >= wit.nkc) {
+            wkc = 0;
+            wu += G;
+            st = 2;
+          }
+        } else if (free_) {
           const Item& Gr = wit;
           const int k0 = wkc * KC, kn = min(KC, Gr.K - k0);
           const uint32_t wbytes = (uint32_t)(wit.rr * kn * sizeof(W));
+          if (!wit.routed) w_static += wbytes;
+          if (lane == 0) log_evt(P.evt, 0, nev, EV_W, wp, (int)iw);
           char* stg = smem + (size_t)s * stage_bytes;
           if (lane == 0) {
             if (iw >= (uint32_t)nst) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -809,7 +990,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
               mt.nt = wit.n;
               mt.xbytes = kn * (int)sizeof(float);
               mt.tgt = wtgt;
-              for (int t = 0; t < kMaxB; ++t) mt.xrow[t] = Gr.xg + (size_t)wit.pr[t] * Gr.K + k0;
+#pragma unroll
+              for (int t = 0; t < kMaxB; ++t)
+                mt.xrow[t] = Gr.xg + (size_t)(t < wit.n ? unit_pair(P, wit, rt_p, t) : 0) * Gr.K + k0;
               mbar_tx_only(&full[s], wbytes);
             } else {
               mbar_arrive_tx(&full[s], wbytes);
@@ -827,9 +1010,14 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
           if (++wkc >= wit.nkc) {
             wkc = 0;
             wu += G;
-            st = seek(false);
+            st = 2;
           }
         }
+      }
+      // ---- L2 prefetch cursor (bounded distance ahead of the ring)
+      if (!pdone && pf_bytes < w_static + pf_window) {
+        pdone = !pf_step();
+        progress = true;
       }
       // ---- activation cursor
       __syncwarp();
@@ -854,6 +1042,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
               mbar_arrive_tx(&full[s], (uint32_t)(mt.nt * mt.xbytes));
               for (int t = 0; t < mt.nt; ++t)
                 bulk_g2s(stg + (size_t)t * mt.xbytes, mt.xrow[t], (uint32_t)mt.xbytes, &full[s]);
+              log_evt(P.evt, 0, nev, EV_X, 0, (int)ix);
             }
             ++ix;
             progress = true;
@@ -867,7 +1056,17 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
           if (lane == 0) atomicOr(P.flags, 8);
           __trap();
         }
-        __nanosleep(20);
+        // The producer shares an SM sub-partition with consumer warps 0 and 4
+        // and the scheduler favours the highest warp id: never busy-poll.
+        // Ring full -> sleep in hardware on the stage's empty barrier;
+        // waiting for a grid barrier / routing -> back off.
+        if (st == 0 && iw >= (uint32_t)nst && iw < ix + (uint32_t)nst) {
+          const int s = (int)(iw % (uint32_t)nst);
+          if (lane == 0) mbar_wait_sleep(&empty[s], ((iw / nst) - 1) & 1u);
+          __syncwarp();
+        } else {
+          __nanosleep(256);
+        }
       } else {
         t0 = 0;
       }
@@ -880,38 +1079,56 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
   float hm = -INFINITY, hs = 0.f;  // head: online (max, sum-exp, first argmax) of this thread's row
   int ha = 0x7fffffff;
   int rtc_layer = -1;
+  int cev = 0;
   constexpr int SL = KC / kCW;  // K elements of a chunk owned by one warp (= 32 lanes x V)
   for (int p = first; p < last; ++p) {
     int j, l;
     phase_jl(P, p, j, l);
-    const Tmpl& T = P.t[j];
+    {  // the phase template -> shared memory (the previous phase ended with a cbar)
+      const int4* src = reinterpret_cast<const int4*>(&P.t[j]);
+      int4* dst = reinterpret_cast<int4*>(&cph);
+      for (int i = tid; i < (int)(sizeof(Tmpl) / 16); i += kCW * 32) dst[i] = src[i];
+    }
+    const Tmpl& T = cph;
     // ---- wait for the phase's inputs
     if (tid == 0) {
       const int dep = dep_of(P, p);
       if (dep >= first) spin_until(P, bar_target(P, dep, first));
     }
     cbar();
+    if (tid == 0) log_evt(P.evt, 1, cev, EV_PASS, p, 0);
     unsigned long long* tr = P.trace ? P.trace + ((size_t)(p - first) * G + blockIdx.x) * 3 : nullptr;
     if (tr && tid == 0) tr[0] = gtimer();
     const int rot = rot_of(P, j, l);
-    if (T.type == PT_PUBLISH) {
-      if (blockIdx.x == 0 && warp == 0) compute_route(P, l, rt_c, true);
+    // ---- the layer's selection (one call site: inlined once)
+    const bool pub = T.type == PT_PUBLISH;
+    if (warp == 1 && (pub ? blockIdx.x == 0 : (T.type == PT_GEMV && T.has_routed && rtc_layer != l)))
+      compute_route(P, l, rt_c, pub || blockIdx.x == 0);
+    if (!pub && T.type == PT_GEMV && T.has_routed) rtc_layer = l;
+    if (pub) {
     } else if (T.type == PT_ATTN) {
-      attn_phase(P, l, xbuf, rot, spos);
-    } else {
-      if (T.has_routed && rtc_layer != l) {
-        if (warp == 0) compute_route(P, l, rt_c, blockIdx.x == 0);
-        rtc_layer = l;
+      const int nc = attn_nc(P, spos);
+      Item it;
+      for (int u = (blockIdx.x - rot + G) % G; u < P.B * P.H * nc; u += G) {
+        decode_attn(P, u, nc, spos, it);
+        switch (P.hd / 32) {
+          case 1: attn_unit<1>(P, l, it, nc, smem, stage_bytes, nst, ic, full, empty, xbuf, spos); break;
+          case 2: attn_unit<2>(P, l, it, nc, smem, stage_bytes, nst, ic, full, empty, xbuf, spos); break;
+          case 4: attn_unit<4>(P, l, it, nc, smem, stage_bytes, nst, ic, full, empty, xbuf, spos); break;
+          default: attn_unit<8>(P, l, it, nc, smem, stage_bytes, nst, ic, full, empty, xbuf, spos); break;
+        }
       }
+    } else {
       const int xk = l == 0 ? T.xkind0 : T.xkind;
       if (xk != XK_NONE && (!T.keep_x || p == first)) load_x(P, xk, T.xsrc, T.xdst, l - 1, xbuf, red, rt_c, spos);
       cbar();
       if (tr && tid == 0) tr[1] = gtimer();
+      if (tid == 0) log_evt(P.evt, 1, cev, EV_READY, p, 0);
       const bool head_phase = T.g[0].epi == EP_HEAD;
       if (head_phase) { hm = -INFINITY; hs = 0.f; ha = 0x7fffffff; }
       Item it;
       for (int u = (blockIdx.x - rot + G) % G; u < T.units; u += G) {
-        if (!decode_unit<W>(P, j, l, u, rt_c, it)) continue;
+        if (!decode_unit<W>(P, T, l, u, rt_c, it)) continue;
         const Item& Gr = it;
         const int nt = it.n, rr = it.rr;
         // warp w owns K elements [w*SL, (w+1)*SL) of every row of the tile
@@ -924,15 +1141,19 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
           const int s = (int)(ic % (uint32_t)nst);
           const int k0 = kc * KC, kn = min(KC, Gr.K - k0);
           const int e0 = warp * SL + lane * V;
+          if (tid == 0) log_evt(P.evt, 1, cev, EV_WAIT, p, (int)ic);
           mbar_wait(&full[s], (ic / nst) & 1u);
+          if (tid == 0) log_evt(P.evt, 1, cev, EV_FULL, p, (int)ic);
           if (e0 < kn) {
             const char* stg = smem + (size_t)s * stage_bytes;
-            float xv[TT][V];
+            float xv[TT][V];  // absent token slots are zero: no predicates in the FMA chains
 #pragma unroll
             for (int t = 0; t < TT; ++t) {
-              if (t < nt) {
+#pragma unroll
+              for (int q = 0; q < V; ++q) xv[t][q] = 0.f;
+              if (TT == 1 || t < nt) {
                 const float* xr = Gr.xstage ? reinterpret_cast<const float*>(stg + kWBytes) + (size_t)t * kn + e0
-                                            : xbuf + (size_t)it.tb[t < kMaxB ? t : 0] * Gr.K + k0 + e0;
+                                            : xbuf + (size_t)unit_token(P, it, rt_c, t) * Gr.K + k0 + e0;
 #pragma unroll
                 for (int qq = 0; qq < V / 4; ++qq) {
                   const float4 x4 = reinterpret_cast<const float4*>(xr)[qq];
@@ -941,16 +1162,24 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
               }
             }
             const W* wb = reinterpret_cast<const W*>(stg) + e0;
+            // all 16 rows' vectors in flight first, then q-outer / row-inner
+            // FMAs: 16 independent accumulation chains (same per-row order)
+            constexpr int RB = TT == 1 ? 4 : 2;  // rows in flight: small enough that the interleaved order survives
 #pragma unroll
-            for (int r = 0; r < kTileRows; ++r) {
-              if (r < rr) {
-                float f[V];
-                WVec<W>::widen(*reinterpret_cast<const uint4*>(wb + (size_t)r * kn), f);
+            for (int r0 = 0; r0 < kTileRows; r0 += RB) {
+              // rows >= rr read stale stage bytes: their sums are never used (the
+              // butterfly below never mixes rows), so no predicate either
+              uint4 wv[RB];
 #pragma unroll
-                for (int t = 0; t < TT; ++t)
-                  if (t < nt)
+              for (int r = 0; r < RB; ++r) wv[r] = *reinterpret_cast<const uint4*>(wb + (size_t)(r0 + r) * kn);
 #pragma unroll
-                    for (int q = 0; q < V; ++q) acc[r][t] = fmaf(f[q], xv[t][q], acc[r][t]);
+              for (int q = 0; q < V; ++q) {
+#pragma unroll
+                for (int r = 0; r < RB; ++r) {
+                  const float f = WVec<W>::elem(wv[r], q);
+#pragma unroll
+                  for (int t = 0; t < TT; ++t) acc[r0 + r][t] = fmaf(f, xv[t][q], acc[r0 + r][t]);
+                }
               }
             }
           }
@@ -961,18 +1190,20 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
         float rs[TT];
 #pragma unroll
         for (int t = 0; t < TT; ++t) rs[t] = reduce_rows16<TT>(acc, t, lane);
+        if (tid == 0) log_evt(P.evt, 1, cev, EV_RED, p, 0);
         cbar();  // the previous unit's epilogue has read red2
         if ((lane & 1) == 0)
 #pragma unroll
           for (int t = 0; t < TT; ++t) red2[(warp * kTileRows + ((lane >> 1) & 15)) * TT + t] = rs[t];
         cbar();
-        if (tid < kTileRows * TT) {
-          const int t = tid >> 4, i = tid & 15;
-          if (t < nt && i < rr) {
+        if (tid == 0) log_evt(P.evt, 1, cev, EV_UNIT, p, 0);
+        {  // epilogue spread over the warps: warp w, lane (2t + h) -> row 2w + h, token t
+          const int t = lane >> 1, i = 2 * warp + (lane & 1);
+          if (lane < 2 * TT && t < nt && i < rr) {
             float v = 0.f;
             for (int w = 0; w < kCW; ++w) v += red2[(w * kTileRows + i) * TT + t];
             const int r0 = it.rb * kTileRows + i;
-            const int pr = it.pr[t], tb = it.tb[t];
+            const int pr = unit_pair(P, it, rt_c, t), tb = unit_token(P, it, rt_c, t);
             if (Gr.epi == EP_HEAD) {
               const float lg = v * P.logit_scale;
               if (P.head_logits) P.head_logits[(size_t)tb * P.V + r0] = lg;
@@ -989,7 +1220,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
               else {
                 float* cache = r0 < 2 * d ? P.kc : P.vc;
                 const int c = r0 < 2 * d ? r0 - d : r0 - 2 * d;
-                cache[(((size_t)l * P.B + tb) * P.max_len + spos[tb]) * d + c] = v;
+                const int hh = c / P.hd;
+                cache[((((size_t)l * P.B + tb) * P.H + hh) * P.max_len + spos[tb]) * P.hd + (c - hh * P.hd)] = v;
               }
             } else if (Gr.epi == EP_LOGITS) {
               if (r0 < Gr.split) Gr.out[(size_t)tb * Gr.out_ld + r0] = v;
@@ -1006,10 +1238,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
       if (head_phase) {
         // merge the 16 row-threads of each token (row order), then CTAs (CTA order) in the last CTA
         cbar();
-        if (tid < kTileRows * TT) {
-          red2[tid * 3] = hm;
-          red2[tid * 3 + 1] = hs;
-          red2[tid * 3 + 2] = __int_as_float(ha);
+        if (lane < 2 * TT) {
+          const int q = ((lane >> 1) * kTileRows + 2 * warp + (lane & 1)) * 3;  // (token, row)
+          red2[q] = hm;
+          red2[q + 1] = hs;
+          red2[q + 2] = __int_as_float(ha);
         }
         cbar();
         if (tid < P.B) {
@@ -1047,6 +1280,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
     // ---- end of phase: grid barrier arrival
     cbar();
     if (tr && tid == 0) tr[2] = gtimer();
+    if (tid == 0) log_evt(P.evt, 1, cev, EV_ARRIVE, p, 0);
     if (T.end_bar && tid == 0) red_release_add(P.sync, 1u);
   }
   // exit ticket: the last CTA out resets the barrier for the next launch
@@ -1065,6 +1299,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
 
 // ====================================================================== host
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 using namespace mobile;
@@ -1125,13 +1360,14 @@ int mobile_dp_create(const mobile_dp_model* m, mobile_dp** out) {
   const int xslice = kChunk / eb * 4;
   o->stage_bytes = kWBytes + o->TT * xslice;
   const int hd = d / m->H;
-  const size_t xbuf = std::max((size_t)B * d * 4, (size_t)kCW * (hd + 2) * 4);
+  const size_t xbuf = std::max((size_t)B * d * 4, (size_t)kCW * (hd + kAttnPart) * 4);
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
   cudaFuncAttributes fa{};
   cudaFuncGetAttributes(&fa, pick_kernel(m->w_dtype, o->TT));
   const size_t cap = (size_t)optin - fa.sharedSizeBytes;
   int nst = 3;
+  if (const char* e = std::getenv("MOBILE_DP_STAGES")) nst = std::max(2, std::min(3, std::atoi(e)));
   while (nst > 1 && (size_t)nst * o->stage_bytes + xbuf > cap) --nst;
   if (nst < 2) { set_error("decode_pass: shared memory does not fit (B=%d d=%d)", B, d); delete o; return MOBILE_ERR_UNSUPPORTED; }
   o->nst = nst;
@@ -1139,9 +1375,9 @@ int mobile_dp_create(const mobile_dp_model* m, mobile_dp** out) {
   o->smem = (size_t)o->xbuf_off + xbuf;
 
   // ---- workspace: sync words, attention partials, head partials
-  const int nc_max = std::max(1, G / std::max(1, B * m->H));
-  const size_t sync_bytes = 4 * (64 + (size_t)B * m->H) + 256;
-  const size_t attn_bytes = 4 * (size_t)B * m->H * nc_max * (hd + 2);
+  const int nc_max = std::min(32, std::max(1, G / std::max(1, B * m->H)));
+  const size_t sync_bytes = (4 * (64 + (size_t)B * m->H) + 511) / 256 * 256;
+  const size_t attn_bytes = 4 * (size_t)B * m->H * nc_max * (hd + kAttnPart);
   const size_t head_bytes = 4 * (size_t)G * kMaxB * 3;
   const size_t ws = sync_bytes + attn_bytes + head_bytes;
   if (cudaMalloc(&o->d_ws, ws) != cudaSuccess || cudaMemset(o->d_ws, 0, ws) != cudaSuccess) {
@@ -1153,6 +1389,9 @@ int mobile_dp_create(const mobile_dp_model* m, mobile_dp** out) {
   P.B = B; P.d = d; P.H = m->H; P.E = E; P.k = k; P.S = S; P.n_gate = m->n_gate; P.gate_norm = m->gate_norm;
   P.reuse_gates = m->reuse_gates; P.max_len = m->max_len; P.L = L; P.V = m->V; P.nc_max = nc_max; P.TT = o->TT;
   P.logit_scale = m->logit_scale; P.gamma = m->gamma;
+  P.hd = hd; P.npi = kWBytes / (2 * hd * 4);
+  P.pf_window = 0;  // measured: L2 prefetch ahead of the ring slows the pass (latency-bound)
+  if (const char* e = std::getenv("MOBILE_DP_PF_KB")) P.pf_window = std::max(0, std::atoi(e)) * 1024;
   P.tok = m->tok; P.pos = m->pos; P.embed = m->embed; P.pe = m->pe; P.kc = m->kc; P.vc = m->vc;
   P.q = m->q; P.att = m->att; P.Y = m->Y; P.Ys = m->Ys; P.states = m->states; P.extra = m->extra;
   P.replay = m->replay; P.idx_out = m->idx_out; P.gates_out = m->gates_out; P.active_out = m->active_out;
@@ -1162,6 +1401,7 @@ int mobile_dp_create(const mobile_dp_model* m, mobile_dp** out) {
   P.head_part = (float*)((char*)o->d_ws + sync_bytes + attn_bytes);
   P.flags = m->flags;
   P.trace = nullptr;
+  P.evt = nullptr;
 
   // ---- per-layer phase templates
   const long long Wsz = (long long)d * d * eb;
@@ -1188,7 +1428,7 @@ int mobile_dp_create(const mobile_dp_model* m, mobile_dp** out) {
     t.type = PT_GEMV; t.n_groups = 1; t.end_bar = 1;
     t.g[0] = dense_group(m->o, Wsz, d, d, EP_STORE);
     t.g[0].out = m->xa; t.g[0].out_ld = d; t.g[0].resid = m->x;
-    t.xkind0 = t.xkind = XK_PLAIN; t.xsrc = m->att;
+    t.xkind0 = t.xkind = XK_ATTN; t.xsrc = m->att;
     ts.push_back(t);
   }
   const int router_j = (int)ts.size();
@@ -1302,6 +1542,11 @@ int mobile_dp_info(const mobile_dp* o, int* out4) {
   out4[1] = o->nst;
   out4[2] = (int)o->smem;
   out4[3] = o->grid;
+  return MOBILE_OK;
+}
+
+int mobile_dp_set_events(mobile_dp* o, unsigned long long* evt) {
+  o->plan.evt = evt;
   return MOBILE_OK;
 }
 

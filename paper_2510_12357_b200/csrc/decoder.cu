@@ -131,8 +131,10 @@ __global__ void attn_decode_kernel(const float* __restrict__ qkv, float* __restr
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   float* q = sc + max_len;
   const float* src = qkv + (size_t)b * 3 * d;
-  float* kr = kc + ((size_t)b * max_len + p) * d + hh * hd;
-  float* vr = vc + ((size_t)b * max_len + p) * d + hh * hd;
+  // head-major cache (B, H, max_len, hd)
+  const size_t head0 = ((size_t)b * H + hh) * max_len;
+  float* kr = kc + (head0 + p) * hd;
+  float* vr = vc + (head0 + p) * hd;
   for (int e = threadIdx.x; e < hd; e += blockDim.x) {
     q[e] = src[hh * hd + e];
     kr[e] = src[d + hh * hd + e];
@@ -144,7 +146,7 @@ __global__ void attn_decode_kernel(const float* __restrict__ qkv, float* __restr
   // scores: one warp per position
   float mx = -INFINITY;
   for (int j = warp; j <= p; j += nw) {
-    const float* kj = kc + ((size_t)b * max_len + j) * d + hh * hd;
+    const float* kj = kc + (head0 + j) * hd;
     float s = 0.f;
     for (int e = lane; e < hd; e += 32) s = fmaf(q[e], kj[e], s);
     s = warp_sum(s) * scale;
@@ -170,7 +172,7 @@ __global__ void attn_decode_kernel(const float* __restrict__ qkv, float* __restr
   const float inv = 1.0f / sum;
   for (int e = threadIdx.x; e < hd; e += blockDim.x) {
     float acc = 0.f;
-    for (int j = 0; j <= p; ++j) acc = fmaf(sc[j], vc[((size_t)b * max_len + j) * d + hh * hd + e], acc);
+    for (int j = 0; j <= p; ++j) acc = fmaf(sc[j], vc[(head0 + j) * hd + e], acc);
     out[(size_t)b * d + hh * hd + e] = acc * inv;
   }
 }

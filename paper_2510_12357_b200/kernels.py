@@ -207,7 +207,7 @@ def dense_gemv(x, w, *, do_ln=False, residual=None, out=None, stream=None):
 def attn_decode(qkv, k_cache, v_cache, pos, n_heads, out=None, stream=None):
     B, d3 = qkv.shape
     d = d3 // 3
-    max_len = k_cache.shape[1]
+    max_len = k_cache.shape[2]  # head-major (B, H, max_len, head_dim)
     if out is None:
         out = torch.empty(B, d, device=qkv.device, dtype=torch.float32)
     _count()

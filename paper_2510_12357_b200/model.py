@@ -411,7 +411,10 @@ class DecodeSession:
         s = model.spec
         self.m, self.B, self.max_len = model, batch, max_len
         dev = model.device
-        self.kc = torch.zeros(s.num_layers, batch, max_len, s.hidden_dim, device=dev, dtype=torch.float32)
+        # head-major KV cache (L, B, H, max_len, head_dim): one head's positions
+        # are contiguous, so a (head, position-chunk) block is one bulk copy
+        H = s.n_heads
+        self.kc = torch.zeros(s.num_layers, batch, H, max_len, s.hidden_dim // H, device=dev, dtype=torch.float32)
         self.vc = torch.zeros_like(self.kc)
         self.pos = 0
 
@@ -427,17 +430,17 @@ class DecodeSession:
         h = Fn.layer_norm(x, (d,), eps=1e-5)
         q, k, v = m._lin(h, dw.qkv[layer]).split(d, dim=-1)
         q, k, v = (t.reshape(Bn, n, d) for t in (q, k, v))
+        kn = k.view(Bn, n, H, hd).transpose(1, 2)
+        vn = v.view(Bn, n, H, hd).transpose(1, 2)
         if rows is None:
-            self.kc[layer, :, pos:pos + n] = k
-            self.vc[layer, :, pos:pos + n] = v
-            K_, V_ = self.kc[layer, :, :pos + n], self.vc[layer, :, :pos + n]
+            self.kc[layer, :, :, pos:pos + n] = kn
+            self.vc[layer, :, :, pos:pos + n] = vn
+            kh, vh = self.kc[layer, :, :, :pos + n], self.vc[layer, :, :, :pos + n]
         else:
-            self.kc[layer, rows, pos:pos + n] = k
-            self.vc[layer, rows, pos:pos + n] = v
-            K_, V_ = self.kc[layer, rows, :pos + n], self.vc[layer, rows, :pos + n]
+            self.kc[layer, rows, :, pos:pos + n] = kn
+            self.vc[layer, rows, :, pos:pos + n] = vn
+            kh, vh = self.kc[layer, rows, :, :pos + n], self.vc[layer, rows, :, :pos + n]
         qh = q.view(Bn, n, H, hd).transpose(1, 2)
-        kh = K_.view(Bn, pos + n, H, hd).transpose(1, 2)
-        vh = V_.view(Bn, pos + n, H, hd).transpose(1, 2)
         scores = (qh @ kh.transpose(-1, -2)) / math.sqrt(hd)
         if n > 1:
             mask = torch.ones(n, pos + n, dtype=torch.bool, device=x.device).triu(1 + pos)
