@@ -53,7 +53,7 @@ constexpr int kMaxB = 4;
 constexpr int kMaxPairs = 32;
 constexpr int kMaxG = 3;
 constexpr int kMaxE = 256;
-constexpr int kMaxStages = 4;
+constexpr int kMaxStages = 3;
 constexpr int kMaxGate = 4;                 // shared experts (and sigmoid gates) per layer
 constexpr int kMaxTmpl = 9;
 constexpr int kAttnPart = 4;  // attention partial layout: [m, s, pad, pad, o[hd]]
@@ -120,11 +120,11 @@ struct Plan {
   unsigned long long* evt;    // optional event log: per CTA and role (0 producer, 1 consumers) kEvt x {time, code}
 };
 
-struct Route {          // one layer's selection + permute, in shared memory
+struct Route {          // one layer's selection + permute, in shared memory (E <= 256)
   int n_active;
-  short act_e[kMaxPairs], act_p0[kMaxPairs], act_n[kMaxPairs];
-  short pairs[kMaxPairs];
-  short idx[kMaxPairs];
+  uint8_t act_e[kMaxPairs], act_p0[kMaxPairs], act_n[kMaxPairs];
+  uint8_t pairs[kMaxPairs];
+  uint8_t idx[kMaxPairs];
   float gates[kMaxPairs];
 };
 
@@ -334,7 +334,7 @@ __device__ __forceinline__ void compute_route_k(const Plan& P, int l, Route& R, 
     for (int i = 0; i < kPer; ++i) {
       const int e = lane + 32 * i;
       if (e < E && rank[i] < k) {
-        R.idx[b * k + rank[i]] = (short)e;
+        R.idx[b * k + rank[i]] = (uint8_t)e;
         R.gates[b * k + rank[i]] = gv[i];  // raw gate logit, normalised below
       }
     }
@@ -390,11 +390,11 @@ __device__ __forceinline__ void compute_route_k(const Plan& P, int l, Route& R, 
     a_me += (((fm >> q) & 1u) && eq < e_me) ? 1 : 0;
   }
   if (lane < NP) {
-    R.pairs[pos] = (short)lane;
+    R.pairs[pos] = (uint8_t)lane;
     if (first) {
-      R.act_e[a_me] = (short)e_me;
-      R.act_p0[a_me] = (short)(pos);
-      R.act_n[a_me] = (short)cnt;
+      R.act_e[a_me] = (uint8_t)e_me;
+      R.act_p0[a_me] = (uint8_t)(pos);
+      R.act_n[a_me] = (uint8_t)cnt;
     }
   }
   const int nact = __popc(fm);
@@ -798,9 +798,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
   __shared__ Route rt_c, rt_p;
   __shared__ int spos[kMaxB];
   __shared__ __align__(16) Tmpl cph, pph;  // consumers' / producer's copy of the current phase template
-  __shared__ __align__(16) float red2[kCW * kTileRows * TT];  // cross-warp row sums / LN / head merge
+  __shared__ __align__(16) float red2b[2][kCW * kTileRows * TT];  // double-buffered cross-warp row sums
+  __shared__ __align__(8) uint64_t rfull[2], rempty[2];            // row sums written / read by the epilogue
+  float* red2 = red2b[0];                                          // LN / head-merge scratch
   __shared__ bool is_last;
-  float* red = red2;
+  float* red = red2b[0];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int V = WVec<W>::N;
   constexpr int KC = kChunk / (int)sizeof(W);
@@ -811,6 +813,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kCW);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&rfull[b], kCW);
+      mbar_init(&rempty[b], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1076,8 +1082,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
 
   // ================================================================== consumers
   uint32_t ic = 0;  // items consumed
-  float hm = -INFINITY, hs = 0.f;  // head: online (max, sum-exp, first argmax) of this thread's row
-  int ha = 0x7fffffff;
+  float hm[2] = {-INFINITY, -INFINITY}, hs[2] = {0.f, 0.f};  // head: online (max, sum-exp, argmax)
+  int ha[2] = {0x7fffffff, 0x7fffffff};                         // per (token, row) slot of this lane
+  uint32_t uc = 0;  // units reduced (red2 double-buffer / epilogue rotation)
   int rtc_layer = -1;
   int cev = 0;
   constexpr int SL = KC / kCW;  // K elements of a chunk owned by one warp (= 32 lanes x V)
@@ -1125,7 +1132,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
       if (tr && tid == 0) tr[1] = gtimer();
       if (tid == 0) log_evt(P.evt, 1, cev, EV_READY, p, 0);
       const bool head_phase = T.g[0].epi == EP_HEAD;
-      if (head_phase) { hm = -INFINITY; hs = 0.f; ha = 0x7fffffff; }
+      if (head_phase) {
+        hm[0] = hm[1] = -INFINITY;
+        hs[0] = hs[1] = 0.f;
+        ha[0] = ha[1] = 0x7fffffff;
+      }
       Item it;
       for (int u = (blockIdx.x - rot + G) % G; u < T.units; u += G) {
         if (!decode_unit<W>(P, T, l, u, rt_c, it)) continue;
@@ -1164,7 +1175,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
             const W* wb = reinterpret_cast<const W*>(stg) + e0;
             // all 16 rows' vectors in flight first, then q-outer / row-inner
             // FMAs: 16 independent accumulation chains (same per-row order)
-            constexpr int RB = TT == 1 ? 4 : 2;  // rows in flight: small enough that the interleaved order survives
+            constexpr int RB = TT == 1 ? 8 : 2;  // rows in flight
 #pragma unroll
             for (int r0 = 0; r0 < kTileRows; r0 += RB) {
               // rows >= rr read stale stage bytes: their sums are never used (the
@@ -1191,65 +1202,95 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
 #pragma unroll
         for (int t = 0; t < TT; ++t) rs[t] = reduce_rows16<TT>(acc, t, lane);
         if (tid == 0) log_evt(P.evt, 1, cev, EV_RED, p, 0);
-        cbar();  // the previous unit's epilogue has read red2
+        // ---- hand the row sums to this unit's epilogue warp (uc % kCW) through
+        // a double-buffered smem area: no CTA-wide barrier per unit
+        const int bb = (int)(uc & 1u);
+        if (uc >= 2) mbar_wait(&rempty[bb], ((uc - 2) >> 1) & 1u);
+        float* rb = red2b[bb];
         if ((lane & 1) == 0)
 #pragma unroll
-          for (int t = 0; t < TT; ++t) red2[(warp * kTileRows + ((lane >> 1) & 15)) * TT + t] = rs[t];
-        cbar();
-        if (tid == 0) log_evt(P.evt, 1, cev, EV_UNIT, p, 0);
-        {  // epilogue spread over the warps: warp w, lane (2t + h) -> row 2w + h, token t
-          const int t = lane >> 1, i = 2 * warp + (lane & 1);
-          if (lane < 2 * TT && t < nt && i < rr) {
-            float v = 0.f;
-            for (int w = 0; w < kCW; ++w) v += red2[(w * kTileRows + i) * TT + t];
-            const int r0 = it.rb * kTileRows + i;
-            const int pr = unit_pair(P, it, rt_c, t), tb = unit_token(P, it, rt_c, t);
-            if (Gr.epi == EP_HEAD) {
-              const float lg = v * P.logit_scale;
-              if (P.head_logits) P.head_logits[(size_t)tb * P.V + r0] = lg;
-              online_add(hm, hs, ha, lg, r0);
-            } else if (Gr.epi == EP_SWIGLU) {  // tile rows [8 gate | 8 up]
-              if (i < 8) {
-                float u2 = 0.f;
-                for (int w = 0; w < kCW; ++w) u2 += red2[(w * kTileRows + i + 8) * TT + t];
-                Gr.out[(size_t)pr * Gr.out_ld + it.rb * 8 + i] = silu_f(v) * u2;
+          for (int t = 0; t < TT; ++t) rb[(warp * kTileRows + ((lane >> 1) & 15)) * TT + t] = rs[t];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rfull[bb]);
+        if (warp == (int)(uc % kCW)) {
+          mbar_wait(&rfull[bb], (uc >> 1) & 1u);
+          if (tid == (int)(uc % kCW) * 32) log_evt(P.evt, 1, cev, EV_UNIT, p, 0);
+#pragma unroll
+          for (int xi = 0; xi < 2; ++xi) {  // (token, row) slots lane and lane + 32
+            const int x = lane + 32 * xi;
+            const int t = x >> 4, i = x & 15;
+            if (x < kTileRows * TT && t < nt && i < rr) {
+              float v = 0.f;
+#pragma unroll
+              for (int w = 0; w < kCW; ++w) v += rb[(w * kTileRows + i) * TT + t];
+              const int r0 = it.rb * kTileRows + i;
+              const int pr = unit_pair(P, it, rt_c, t), tb = unit_token(P, it, rt_c, t);
+              if (Gr.epi == EP_HEAD) {
+                const float lg = v * P.logit_scale;
+                if (P.head_logits) P.head_logits[(size_t)tb * P.V + r0] = lg;
+                online_add(hm[xi], hs[xi], ha[xi], lg, r0);
+              } else if (Gr.epi == EP_SWIGLU) {  // tile rows [8 gate | 8 up]
+                if (i < 8) {
+                  float u2 = 0.f;
+#pragma unroll
+                  for (int w = 0; w < kCW; ++w) u2 += rb[(w * kTileRows + i + 8) * TT + t];
+                  Gr.out[(size_t)pr * Gr.out_ld + it.rb * 8 + i] = silu_f(v) * u2;
+                }
+              } else if (Gr.epi == EP_QKV) {
+                const int d = P.d;
+                if (r0 < d) P.q[(size_t)tb * d + r0] = v;
+                else {
+                  float* cache = r0 < 2 * d ? P.kc : P.vc;
+                  const int c = r0 < 2 * d ? r0 - d : r0 - 2 * d;
+                  const int hh = c / P.hd;
+                  cache[((((size_t)l * P.B + tb) * P.H + hh) * P.max_len + spos[tb]) * P.hd + (c - hh * P.hd)] = v;
+                }
+              } else if (Gr.epi == EP_LOGITS) {
+                if (r0 < Gr.split) Gr.out[(size_t)tb * Gr.out_ld + r0] = v;
+                else Gr.out2[(size_t)tb * (Gr.rows - Gr.split) + (r0 - Gr.split)] = v;
+              } else {
+                const size_t o0 = (size_t)pr * Gr.out_ld + r0;
+                if (Gr.epi == EP_RELU) v = fmaxf(v, 0.f);
+                else if (Gr.resid) v += __ldcg(Gr.resid + o0);
+                Gr.out[o0] = v;
               }
-            } else if (Gr.epi == EP_QKV) {
-              const int d = P.d;
-              if (r0 < d) P.q[(size_t)tb * d + r0] = v;
-              else {
-                float* cache = r0 < 2 * d ? P.kc : P.vc;
-                const int c = r0 < 2 * d ? r0 - d : r0 - 2 * d;
-                const int hh = c / P.hd;
-                cache[((((size_t)l * P.B + tb) * P.H + hh) * P.max_len + spos[tb]) * P.hd + (c - hh * P.hd)] = v;
-              }
-            } else if (Gr.epi == EP_LOGITS) {
-              if (r0 < Gr.split) Gr.out[(size_t)tb * Gr.out_ld + r0] = v;
-              else Gr.out2[(size_t)tb * (Gr.rows - Gr.split) + (r0 - Gr.split)] = v;
-            } else {
-              const size_t o0 = (size_t)pr * Gr.out_ld + r0;
-              if (Gr.epi == EP_RELU) v = fmaxf(v, 0.f);
-              else if (Gr.resid) v += __ldcg(Gr.resid + o0);
-              Gr.out[o0] = v;
             }
           }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&rempty[bb]);
         }
+        ++uc;
       }
       if (head_phase) {
         // merge the 16 row-threads of each token (row order), then CTAs (CTA order) in the last CTA
+        // merge each warp's 16 row slots per token (fixed butterfly), then the
+        // warps in warp order, then CTAs (CTA order) in the last CTA
+#pragma unroll
+        for (int xi = 0; xi < 2; ++xi)
+#pragma unroll
+          for (int off = 8; off > 0; off >>= 1) {
+            const float om = __shfl_xor_sync(0xffffffffu, hm[xi], off);
+            const float os = __shfl_xor_sync(0xffffffffu, hs[xi], off);
+            const int oa = __shfl_xor_sync(0xffffffffu, ha[xi], off);
+            online_merge(hm[xi], hs[xi], ha[xi], om, os, oa);
+          }
         cbar();
-        if (lane < 2 * TT) {
-          const int q = ((lane >> 1) * kTileRows + 2 * warp + (lane & 1)) * 3;  // (token, row)
-          red2[q] = hm;
-          red2[q + 1] = hs;
-          red2[q + 2] = __int_as_float(ha);
+#pragma unroll
+        for (int xi = 0; xi < 2; ++xi) {
+          const int x = lane + 32 * xi, t = x >> 4;
+          if ((x & 15) == 0 && t < TT) {
+            float* q = red2 + (warp * kMaxB + t) * 3;
+            q[0] = hm[xi];
+            q[1] = hs[xi];
+            q[2] = __int_as_float(ha[xi]);
+          }
         }
         cbar();
         if (tid < P.B) {
           float M = -INFINITY, S = 0.f;
           int A = 0x7fffffff;
-          for (int i = 0; i < kTileRows; ++i) {
-            const float* q = red2 + (tid * kTileRows + i) * 3;
+          for (int w = 0; w < kCW; ++w) {
+            const float* q = red2 + (w * kMaxB + tid) * 3;
             online_merge(M, S, A, q[0], q[1], __float_as_int(q[2]));
           }
           float* hp = P.head_part + ((size_t)blockIdx.x * kMaxB + tid) * 3;
