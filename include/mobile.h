@@ -335,6 +335,16 @@ int mobile_offload_run_pass(mobile_offload* o, const unsigned long long* graph_e
                             const void* slot_dev_row, long long slot_row_bytes, int lookahead, int* fresh_out);
 /* bytes copied H2D so far, transfers issued */
 int mobile_offload_counters(const mobile_offload* o, long long* out2);
+/* zero-sync mode (decode_pass.cu): per-slot copy tickets written by the copy
+ * stream (cuStreamWriteValue32), slot reuse ordered after the kernel's
+ * progress counter (cuStreamWaitValue32) */
+int mobile_offload_zs_enable(mobile_offload* o, void** done_out, void** prog_out, void** prog_mirror_dev_out,
+                             void** prog_mirror_host_out);
+int mobile_offload_zs_require(mobile_offload* o, int layer, const int* experts, int n, int* out2, int* issued_out,
+                              int (*wait_fn)(void*), void* wait_ctx);
+int mobile_offload_zs_prefetch(mobile_offload* o, int layer, int expert, int* status_out);
+int mobile_offload_zs_release(mobile_offload* o, int layer, const int* experts, int n, long long release_prog);
+long long* mobile_offload_zs_base(mobile_offload* o); /* progress value at the next pass start (shared by all passes) */
 
 
 /* ---- persistent decode pass (decode_pass.cu) -------------------------------
@@ -395,8 +405,19 @@ int mobile_dp_info(const mobile_dp* p, int* out4); /* phases, stages, smem bytes
 int mobile_dp_set_trace(mobile_dp* p, unsigned long long* trace);
 /* optional event log (grid x 2 roles x 1024 x 2 u64: globaltimer, code<<56 | phase<<32 | item); NULL = off */
 int mobile_dp_set_events(mobile_dp* p, unsigned long long* evt);
+/* watchdog diagnostics (host memory, readable after a trapped launch):
+ * [0] 1 = producer stalled / 2 = grid barrier stalled, then CTA, phase, ... */
+int mobile_dp_diag(const mobile_dp* p, int* out16);
 /* segment = -1: the whole pass; else offload segment 0..L */
 int mobile_dp_launch(mobile_dp* p, int segment, void* stream);
+/* Zero-sync offloaded pass (one launch): the host runs the engine.py:121-169
+ * cache protocol while the kernel runs -- demand passes read each layer's
+ * selection from mapped host memory, planned passes (big, replay) use
+ * `targets` (L x k); misses are copied on the runtime's copy stream and
+ * announced to the kernel with per-slot tickets.  p must be created with
+ * offload = 1. */
+int mobile_dp_run_offload_pass(mobile_dp* p, mobile_offload* o, int planned, const int* targets, int k,
+                               int lookahead, void* stream, int* fresh_out);
 
 #ifdef __cplusplus
 }

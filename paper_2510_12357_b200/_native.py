@@ -127,6 +127,13 @@ _SIGS = {
     "mobile_dp_launch": ([P, I32, P], I32),
     "mobile_dp_set_trace": ([P, P], I32),
     "mobile_dp_set_events": ([P, P], I32),
+    "mobile_dp_diag": ([P, P], I32),
+    "mobile_dp_run_offload_pass": ([P, P, I32, P, I32, I32, P, P], I32),
+    "mobile_offload_zs_enable": ([P, P, P, P, P], I32),
+    "mobile_offload_zs_require": ([P, I32, P, I32, P, P, P, P], I32),
+    "mobile_offload_zs_prefetch": ([P, I32, I32, P], I32),
+    "mobile_offload_zs_release": ([P, I32, P, I32, I64], I32),
+    "mobile_offload_zs_base": ([P], P),
 }
 EXPORTED = tuple(_SIGS)
 for _name, (_args, _ret) in _SIGS.items():

@@ -63,7 +63,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     if OUT.exists() and not force and all(o.stat().st_mtime <= OUT.stat().st_mtime for o in objs):
         return OUT
     tmp = OUT.with_suffix(".so.tmp")
-    cmd = [NVCC] + ARCH + ["-shared", "-o", str(tmp)] + [str(o) for o in objs] + ["-lcuda"]
+    cmd = [NVCC] + ARCH + ["-shared", "-o", str(tmp)] + [str(o) for o in objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -117,6 +117,21 @@ struct Plan {
   float* head_part;
   int* flags;
   unsigned long long* trace;  // optional: per (phase, CTA) [barrier passed, inputs ready, work done] ns
+  // zero-sync offload pass (mobile_dp_run_offload_pass): the kernel publishes
+  // each layer's selection to mapped host memory, the host cache driver answers
+  // with (slot, ticket) per expert, copies land in the background
+  int zs;
+  unsigned zs_epoch, zs_prog_base;
+  const unsigned* zs_done;     // device: per slot, ticket of the last copy landed
+  unsigned* zs_prog;           // device: progress (layers consumed) for slot reuse
+  unsigned* zs_prog_h;         // mapped mirror of zs_prog
+  int* zs_route_h;             // mapped (L, E + 1) active lists
+  int* zs_route_flag_h;        // mapped (L): epoch when published
+  const int* zs_slots_h;       // mapped (L, E, 2): slot, ticket
+  const int* zs_slots_flag_h;  // mapped (L): epoch when written
+  int* zs_slots_d;             // device copy relayed by CTA 0 (only one warp reads host memory)
+  int* zs_slots_flag_d;
+  int* diag;                  // optional mapped host int[16]: watchdog diagnostics (survive the trap)
   unsigned long long* evt;    // optional event log: per CTA and role (0 producer, 1 consumers) kEvt x {time, code}
 };
 
@@ -183,6 +198,21 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   return v;
 }
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_volatile_s32(const int* p) {
+  int v;
+  asm volatile("ld.volatile.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_volatile_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -272,7 +302,7 @@ __device__ __forceinline__ Group grp_t(const Group& G0, int l) {
   return G;
 }
 
-__device__ void spin_until(const Plan& P, unsigned target) {
+__device__ void spin_until(const Plan& P, unsigned target, int p = -1) {
   if (target == 0u) return;
   if (ld_relaxed(P.sync) < target) {
     const unsigned long long t0 = gtimer();
@@ -280,6 +310,10 @@ __device__ void spin_until(const Plan& P, unsigned target) {
       __nanosleep(64);
       if (gtimer() - t0 > kWatchdogNs) {
         atomicOr(P.flags, 4);
+        if (P.diag && atomicCAS(P.diag, 0, 2) == 0) {
+          P.diag[1] = blockIdx.x; P.diag[2] = p; P.diag[3] = (int)target; P.diag[4] = (int)ld_relaxed(P.sync);
+          __threadfence_system();
+        }
         __trap();
       }
     }
@@ -424,6 +458,7 @@ __device__ __forceinline__ void compute_route(const Plan& P, int l, Route& R, bo
 struct Item {           // everything the producer and the consumers need about one unit
   int g, a, rb, rr, nkc, n;
   int routed;
+  int zslot, tkt;             // zero-sync: slot and copy ticket of a routed unit
   int attn, b, h, c, p0, np;  // attention unit: sequence, head, chunk of old positions [p0, p0 + np)
   int K, rows, epi, xstage, out_ld, split;
   const char* wrow;     // first byte of the tile's rows (chunk 0)
@@ -446,7 +481,8 @@ __device__ __forceinline__ int unit_token(const Plan& P, const Item& it, const R
 
 // decode unit u of (template j, layer l); false = no work (inactive routed slot)
 template <typename W>
-__device__ __forceinline__ bool decode_unit(const Plan& P, const Tmpl& T, int l, int u, const Route& R, Item& it) {
+__device__ __forceinline__ bool decode_unit(const Plan& P, const Tmpl& T, int l, int u, const Route& R, Item& it,
+                                            bool zs = false, int zs_slot = 0, int zs_tkt = 0) {
   int uu = u, g = 0;
   for (; g < T.n_groups - 1; ++g) {
     if (uu < T.g[g].units) break;
@@ -464,7 +500,12 @@ __device__ __forceinline__ bool decode_unit(const Plan& P, const Tmpl& T, int l,
   if (G.kind == GK_ROUTED) {
     if (a >= R.n_active) return false;
     const int e = R.act_e[a];
-    const int s = G.slot ? G.slot[e] : e;
+    int s = G.slot ? G.slot[e] : e;
+    if (zs) {  // warp-uniform: lane a holds active expert a's (slot, ticket)
+      s = __shfl_sync(0xffffffffu, zs_slot, a & 31);
+      it.tkt = __shfl_sync(0xffffffffu, zs_tkt, a & 31);
+      it.zslot = s;
+    }
     base = G.w + (long long)s * G.stride;
     it.n = R.act_n[a];
   } else if (G.kind == GK_SHARED) {
@@ -837,6 +878,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
     int rt_layer = -1;
     int pph_j = -1;
     bool fresh = true;
+    int zs_layer = -1, zs_slot = 0, zs_tkt = 0;  // zero-sync: lane a = active expert a
     auto seek = [&]() -> int {  // 0 = ok, 1 = done, 2 = blocked on routing (warp-uniform)
       while (wp < last) {
         phase_jl(P, wp, wj, wl);
@@ -883,7 +925,30 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
             rt_layer = wl;
             if (lane == 0) log_evt(P.evt, 0, nev, EV_ROUTE, wp, 0);
           }
-          if (decode_unit<W>(P, T, wl, wu, rt_p, wit)) return 0;
+          const bool routed = T.g[g].kind == GK_ROUTED;
+          if (P.zs && routed && zs_layer != wl) {  // the host cache's answer for this layer
+            int ok = 0;
+            if (lane == 0) {
+              int v;
+              asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(P.zs_slots_flag_d + wl) : "memory");
+              ok = v == (int)P.zs_epoch;
+            }
+            if (!__shfl_sync(0xffffffffu, ok, 0)) return 2;
+            if (lane < rt_p.n_active) {
+              const int* q = P.zs_slots_d + ((size_t)wl * P.E + rt_p.act_e[lane]) * 2;
+              zs_slot = ld_volatile_s32(q);
+              zs_tkt = ld_volatile_s32(q + 1);
+            }
+            zs_layer = wl;
+          }
+          if (decode_unit<W>(P, T, wl, wu, rt_p, wit, P.zs && routed, zs_slot, zs_tkt)) {
+            if (P.zs && routed) {  // stream the expert's tiles once its copy has landed
+              int ok = 0;
+              if (lane == 0) ok = (int)(ld_volatile_u32(P.zs_done + wit.zslot) - (unsigned)wit.tkt) >= 0;
+              if (!__shfl_sync(0xffffffffu, ok, 0)) return 2;
+            }
+            return 0;
+          }
           wu += G;
         }
         ++wp;
@@ -945,6 +1010,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
       return false;
     };
     uint32_t iw = 0, ix = 0;      // items issued (weights) / completed (activations)
+    int relay_l = 0;              // zero-sync: next layer whose slot table CTA 0 relays
+    unsigned long long relay_t = 0;
     unsigned long long t0 = 0;
     unsigned seen = 0;            // last observed barrier counter
     while (true) {
@@ -1020,6 +1087,28 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
           }
         }
       }
+      // ---- zero-sync relay (CTA 0 only): the host's slot tables -> device memory
+      if (P.zs && blockIdx.x == 0 && relay_l < P.L) {
+        const unsigned long long now = gtimer();
+        if (now - relay_t > 400) {
+          relay_t = now;
+          int ok = 0;
+          if (lane == 0) ok = ld_acquire_sys(P.zs_slots_flag_h + relay_l) == (int)P.zs_epoch;
+          if (__shfl_sync(0xffffffffu, ok, 0)) {
+            const int n = P.E * 2;
+            for (int i = lane; i < n; i += 32)
+              P.zs_slots_d[(size_t)relay_l * n + i] = ld_volatile_s32(P.zs_slots_h + (size_t)relay_l * n + i);
+            __syncwarp();
+            if (lane == 0) {
+              __threadfence();
+              asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(P.zs_slots_flag_d + relay_l), "r"((int)P.zs_epoch)
+                           : "memory");
+            }
+            ++relay_l;
+            progress = true;
+          }
+        }
+      }
       // ---- L2 prefetch cursor (bounded distance ahead of the ring)
       if (!pdone && pf_bytes < w_static + pf_window) {
         pdone = !pf_step();
@@ -1055,18 +1144,29 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
           }
         }
       }
-      if (st == 1 && ix == iw) break;
+      if (st == 1 && ix == iw && !(P.zs && blockIdx.x == 0 && relay_l < P.L)) break;
       if (!progress) {
         if (t0 == 0) t0 = gtimer();
         else if (gtimer() - t0 > kWatchdogNs) {
-          if (lane == 0) atomicOr(P.flags, 8);
+          if (lane == 0) {
+            atomicOr(P.flags, 8);
+            if (P.diag && atomicCAS(P.diag, 0, 1) == 0) {
+              P.diag[1] = blockIdx.x; P.diag[2] = wp; P.diag[3] = wl; P.diag[4] = st; P.diag[5] = (int)iw;
+              P.diag[6] = (int)ix; P.diag[7] = zs_layer; P.diag[8] = wit.zslot; P.diag[9] = wit.tkt;
+              P.diag[10] = P.zs ? (int)ld_volatile_u32(P.zs_done + wit.zslot) : -1;
+              P.diag[11] = (int)ld_relaxed(P.sync); P.diag[12] = P.zs ? ld_volatile_s32(P.zs_slots_flag_h + wl) : -1;
+              P.diag[13] = (int)P.zs_epoch; P.diag[14] = rt_layer; P.diag[15] = wit.routed;
+              __threadfence_system();
+            }
+          }
           __trap();
         }
         // The producer shares an SM sub-partition with consumer warps 0 and 4
         // and the scheduler favours the highest warp id: never busy-poll.
         // Ring full -> sleep in hardware on the stage's empty barrier;
         // waiting for a grid barrier / routing -> back off.
-        if (st == 0 && iw >= (uint32_t)nst && iw < ix + (uint32_t)nst) {
+        const bool relaying = P.zs && blockIdx.x == 0 && relay_l < P.L;
+        if (!relaying && st == 0 && iw >= (uint32_t)nst && iw < ix + (uint32_t)nst) {
           const int s = (int)(iw % (uint32_t)nst);
           if (lane == 0) mbar_wait_sleep(&empty[s], ((iw / nst) - 1) & 1u);
           __syncwarp();
@@ -1100,7 +1200,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
     // ---- wait for the phase's inputs
     if (tid == 0) {
       const int dep = dep_of(P, p);
-      if (dep >= first) spin_until(P, bar_target(P, dep, first));
+      if (dep >= first) spin_until(P, bar_target(P, dep, first), p);
     }
     cbar();
     if (tid == 0) log_evt(P.evt, 1, cev, EV_PASS, p, 0);
@@ -1109,8 +1209,23 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
     const int rot = rot_of(P, j, l);
     // ---- the layer's selection (one call site: inlined once)
     const bool pub = T.type == PT_PUBLISH;
-    if (warp == 1 && (pub ? blockIdx.x == 0 : (T.type == PT_GEMV && T.has_routed && rtc_layer != l)))
+    if (warp == 1 && (pub ? blockIdx.x == 0 : (T.type == PT_GEMV && T.has_routed && rtc_layer != l))) {
       compute_route(P, l, rt_c, pub || blockIdx.x == 0);
+      if (pub && P.zs) {  // selection -> mapped host memory, then the flag (engine.py:137: demand requests)
+        int* r = P.zs_route_h + (size_t)l * (P.E + 1);
+        if (lane == 0) r[0] = rt_c.n_active;
+        if (lane < rt_c.n_active) r[1 + lane] = rt_c.act_e[lane];
+        __threadfence_system();
+        __syncwarp();
+        if (lane == 0) asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(P.zs_route_flag_h + l), "r"((int)P.zs_epoch) : "memory");
+      }
+    }
+    if (P.zs && blockIdx.x == 0 && tid == 0 && ((j == 0 && l > 0) || j == P.ppl)) {
+      // every CTA is past layer l-1's routed down (this phase's barrier): its slots may be reused
+      const unsigned v = P.zs_prog_base + (unsigned)l;
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.zs_prog), "r"(v) : "memory");
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(P.zs_prog_h), "r"(v) : "memory");
+    }
     if (!pub && T.type == PT_GEMV && T.has_routed) rtc_layer = l;
     if (pub) {
     } else if (T.type == PT_ATTN) {
@@ -1340,7 +1455,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
 
 // ====================================================================== host
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cstdlib>
+#include <cstring>
+#include <tuple>
 #include <vector>
 
 using namespace mobile;
@@ -1348,6 +1467,16 @@ using namespace mobile::dp;
 
 struct mobile_dp {
   Plan plan{};
+  // zero-sync offload state (mapped host buffers)
+  int* h_route = nullptr;
+  int* h_route_flag = nullptr;
+  int* h_slots = nullptr;
+  int* h_slots_flag = nullptr;
+  unsigned* h_prog = nullptr;
+  unsigned epoch = 0, prog_base = 0;
+  int* h_diag = nullptr;
+  int* d_slots = nullptr;
+  int* d_slots_flag = nullptr;
   std::vector<int> seg_first;  // offload: first phase of segment l (l = 0..L), seg_first[L+1] = n_phases
   void* d_ws = nullptr;
   int w_dtype = 0, TT = 1, nst = 3, stage_bytes = 0, xbuf_off = 0;
@@ -1443,6 +1572,13 @@ int mobile_dp_create(const mobile_dp_model* m, mobile_dp** out) {
   P.flags = m->flags;
   P.trace = nullptr;
   P.evt = nullptr;
+  P.diag = nullptr;
+  if (cudaHostAlloc((void**)&o->h_diag, sizeof(int) * 16, cudaHostAllocMapped | cudaHostAllocPortable) == cudaSuccess) {
+    std::memset(o->h_diag, 0, sizeof(int) * 16);
+    void* dd = nullptr;
+    cudaHostGetDevicePointer(&dd, o->h_diag, 0);
+    P.diag = (int*)dd;
+  }
 
   // ---- per-layer phase templates
   const long long Wsz = (long long)d * d * eb;
@@ -1572,6 +1708,14 @@ int mobile_dp_create(const mobile_dp_model* m, mobile_dp** out) {
 
 void mobile_dp_destroy(mobile_dp* o) {
   if (!o) return;
+  if (o->h_route) cudaFreeHost(o->h_route);
+  if (o->h_route_flag) cudaFreeHost(o->h_route_flag);
+  if (o->h_slots) cudaFreeHost(o->h_slots);
+  if (o->h_slots_flag) cudaFreeHost(o->h_slots_flag);
+  if (o->h_prog) cudaFreeHost(o->h_prog);
+  if (o->h_diag) cudaFreeHost(o->h_diag);
+  if (o->d_slots) cudaFree(o->d_slots);
+  if (o->d_slots_flag) cudaFree(o->d_slots_flag);
   cudaFree(o->d_ws);
   delete o;
 }
@@ -1583,6 +1727,12 @@ int mobile_dp_info(const mobile_dp* o, int* out4) {
   out4[1] = o->nst;
   out4[2] = (int)o->smem;
   out4[3] = o->grid;
+  return MOBILE_OK;
+}
+
+int mobile_dp_diag(const mobile_dp* o, int* out16) {
+  if (!o->h_diag) return MOBILE_ERR_INVALID;
+  for (int i = 0; i < 16; ++i) out16[i] = ((volatile int*)o->h_diag)[i];
   return MOBILE_OK;
 }
 
@@ -1608,6 +1758,144 @@ int mobile_dp_launch(mobile_dp* o, int segment, void* stream) {
   void* args[] = {(void*)&o->plan, (void*)&first, (void*)&last, (void*)&o->nst, (void*)&o->stage_bytes, (void*)&o->xbuf_off};
   cudaError_t e = cudaLaunchKernel(kern, dim3(o->grid), dim3(kThreads), args, o->smem, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_status(e, "decode_pass launch");
+  return MOBILE_OK;
+}
+
+// ---------------------------------------------------------------- zero-sync offload pass
+// One launch runs the whole pass; this host loop is StreamSimulator.run_pass
+// (engine.py:121-169) against the running kernel:
+//   per layer l: unpin layer l-1 (engine.py:152-153) -> issue window
+//   (planned pass, engine.py:98-119) -> the layer's selection (planned: the
+//   replayed targets; demand: published by the kernel into mapped memory, the
+//   host's sync point) -> request + pin, misses issued (engine.py:137-145) ->
+//   (slot, ticket) of every selected expert back to the kernel.
+// Cache decisions are the same function of the request sequence as in the
+// segmented driver; copies overlap the kernel's hits / shared experts / next
+// phases instead of waiting for a launch boundary.
+namespace {
+struct ZsWait {
+  volatile unsigned* prog;  // the runtime's mapped progress mirror
+  unsigned need;
+};
+int zs_wait_progress(void* ctx) {  // deadlock stall: the kernel consumed every earlier layer
+  auto* w = (ZsWait*)ctx;
+  volatile unsigned* pr = w->prog;
+  const auto t0 = std::chrono::steady_clock::now();
+  while ((int)(*pr - w->need) < 0) {
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(10)) {
+      set_error("decode_pass: zero-sync stall timed out waiting for kernel progress (need %u, at %u)", w->need,
+                (unsigned)*pr);
+      return MOBILE_ERR_CUDA;
+    }
+  }
+  return MOBILE_OK;
+}
+}  // namespace
+
+int mobile_dp_run_offload_pass(mobile_dp* dp, mobile_offload* o, int planned, const int* targets, int k, int lookahead,
+                               void* stream, int* fresh_out) {
+  Plan& P = dp->plan;
+  const int L = P.L, E = P.E;
+  if (!dp->h_route) {
+    const unsigned fl = cudaHostAllocMapped | cudaHostAllocPortable;
+    if (cudaHostAlloc((void**)&dp->h_route, sizeof(int) * L * (E + 1), fl) != cudaSuccess ||
+        cudaHostAlloc((void**)&dp->h_route_flag, sizeof(int) * L, fl) != cudaSuccess ||
+        cudaHostAlloc((void**)&dp->h_slots, sizeof(int) * L * E * 2, fl) != cudaSuccess ||
+        cudaHostAlloc((void**)&dp->h_slots_flag, sizeof(int) * L, fl) != cudaSuccess) {
+      set_error("decode_pass: mapped host allocation failed");
+      return MOBILE_ERR_CUDA;
+    }
+    if (cudaMalloc((void**)&dp->d_slots, sizeof(int) * L * E * 2) != cudaSuccess ||
+        cudaMalloc((void**)&dp->d_slots_flag, sizeof(int) * L) != cudaSuccess ||
+        cudaMemset(dp->d_slots_flag, 0, sizeof(int) * L) != cudaSuccess) {
+      set_error("decode_pass: device slot-table allocation failed");
+      return MOBILE_ERR_CUDA;
+    }
+    P.zs_slots_d = dp->d_slots;
+    P.zs_slots_flag_d = dp->d_slots_flag;
+    std::memset(dp->h_route_flag, 0, sizeof(int) * L);
+    std::memset(dp->h_slots_flag, 0, sizeof(int) * L);
+    void *d1, *d2, *d3, *d4;
+    cudaHostGetDevicePointer(&d1, dp->h_route, 0);
+    cudaHostGetDevicePointer(&d2, dp->h_route_flag, 0);
+    cudaHostGetDevicePointer(&d3, dp->h_slots, 0);
+    cudaHostGetDevicePointer(&d4, dp->h_slots_flag, 0);
+    P.zs_route_h = (int*)d1;
+    P.zs_route_flag_h = (int*)d2;
+    P.zs_slots_h = (const int*)d3;
+    P.zs_slots_flag_h = (const int*)d4;
+  }
+  void *done = nullptr, *prog = nullptr, *mirror_d = nullptr, *mirror_h = nullptr;
+  if (int rc = mobile_offload_zs_enable(o, &done, &prog, &mirror_d, &mirror_h)) return rc;
+  P.zs_done = (const unsigned*)done;
+  P.zs_prog = (unsigned*)prog;
+  P.zs_prog_h = (unsigned*)mirror_d;
+  P.zs = 1;
+  P.zs_epoch = ++dp->epoch;
+  long long* pbase = mobile_offload_zs_base(o);  // shared by every pass kind on this runtime
+  P.zs_prog_base = (unsigned)*pbase;
+  const unsigned base = (unsigned)*pbase;
+  int rc = mobile_dp_launch(dp, -1, stream);
+  P.zs = 0;
+  if (rc) return rc;
+  volatile int* route_flag = dp->h_route_flag;
+  volatile int* slots_flag = dp->h_slots_flag;
+  std::vector<std::tuple<int, int, int>> waiting;  // (earliest_issue_layer, layer, expert), policy.py:86-106
+  if (planned) {
+    for (int l = 0; l < L; ++l)
+      for (int j = 0; j < k; ++j) waiting.emplace_back(std::max(0, l - lookahead), l, targets[l * k + j]);
+    std::sort(waiting.begin(), waiting.end());
+  }
+  std::vector<int> prev, cur, out2;
+  int fresh = 0;
+  for (int l = 0; l < L; ++l) {
+    if (l > 0) mobile_offload_zs_release(o, l - 1, prev.data(), (int)prev.size(), (long long)base + l);
+    if (planned) {  // speculative issue window at the layer boundary
+      std::vector<std::tuple<int, int, int>> kept;
+      size_t i = 0;
+      for (; i < waiting.size(); ++i) {
+        const auto& en = waiting[i];
+        if (std::get<0>(en) > l) break;
+        if (std::get<1>(en) < l) continue;
+        int st = 0;
+        const int r = mobile_offload_zs_prefetch(o, std::get<1>(en), std::get<2>(en), &st);
+        if (r == MOBILE_ERR_DEFERRED) kept.push_back(en);
+        else if (r != MOBILE_OK) return r;
+      }
+      kept.insert(kept.end(), waiting.begin() + i, waiting.end());
+      waiting.swap(kept);
+      cur.assign(targets + l * k, targets + (l + 1) * k);
+    } else {  // the kernel publishes the layer's selection: the pass's sync point
+      const auto t0 = std::chrono::steady_clock::now();
+      while (route_flag[l] != (int)P.zs_epoch) {
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(10)) {
+          set_error("decode_pass: zero-sync pass timed out waiting for layer %d routing", l);
+          return MOBILE_ERR_CUDA;
+        }
+      }
+      std::atomic_thread_fence(std::memory_order_acquire);
+      mobile_offload_sync(o);
+      const int* r = dp->h_route + (size_t)l * (E + 1);
+      cur.assign(r + 1, r + 1 + r[0]);
+    }
+    out2.resize(2 * cur.size());
+    int issued = 0;
+    ZsWait wctx{(volatile unsigned*)mirror_h, base + (unsigned)l};
+    if (int r = mobile_offload_zs_require(o, l, cur.data(), (int)cur.size(), out2.data(), &issued, zs_wait_progress, &wctx))
+      return r;
+    fresh += issued;
+    int* tbl = dp->h_slots + (size_t)l * E * 2;
+    for (size_t i = 0; i < cur.size(); ++i) {
+      tbl[2 * cur[i]] = out2[2 * i];
+      tbl[2 * cur[i] + 1] = out2[2 * i + 1];
+    }
+    std::atomic_thread_fence(std::memory_order_release);
+    slots_flag[l] = (int)P.zs_epoch;
+    prev.swap(cur);
+  }
+  mobile_offload_zs_release(o, L - 1, prev.data(), (int)prev.size(), (long long)base + L);
+  *pbase = (long long)base + L;
+  if (fresh_out) *fresh_out = fresh;
   return MOBILE_OK;
 }
 

@@ -12,6 +12,7 @@
 // A slot is never overwritten while a kernel may still read it: each slot has
 // a last-use event recorded on the compute stream after the layer's expert
 // kernels, and a new copy into the slot waits on it first.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -42,6 +43,14 @@ struct mobile_offload {
   double clock = 0.0;
   std::vector<std::pair<int, int>> awaited;   // waited on since the last sync
   long long bytes = 0, transfers = 0;
+  // ---- zero-sync mode (one persistent kernel per pass, see decode_pass.cu)
+  unsigned* zs_done = nullptr;                // device: last copy ticket landed per slot (stream-written)
+  unsigned* zs_prog = nullptr;                // device: layers whose experts the kernel has consumed
+  std::vector<unsigned> zs_ticket;            // per slot: ticket of its latest copy
+  std::vector<long long> zs_last_use;         // per slot: progress value that frees it (0 = free)
+  long long zs_base = 0;                      // progress value at the start of the next pass
+  unsigned* zs_prog_h = nullptr;              // mapped host mirror of zs_prog (the host polls it)
+  unsigned* zs_prog_hd = nullptr;             // its device address
 };
 
 static const double kInf = std::numeric_limits<double>::infinity();
@@ -103,6 +112,9 @@ mobile_offload* mobile_offload_create(int slots, long long expert_bytes, void* s
 
 void mobile_offload_destroy(mobile_offload* o) {
   if (!o) return;
+  if (o->zs_done) cudaFree(o->zs_done);
+  if (o->zs_prog) cudaFree(o->zs_prog);
+  if (o->zs_prog_h) cudaFreeHost(o->zs_prog_h);
   for (auto e : o->copy_done) cudaEventDestroy(e);
   for (auto e : o->last_use) cudaEventDestroy(e);
   mobile_cache_destroy(o->cache);
@@ -233,6 +245,10 @@ int mobile_offload_run_pass(mobile_offload* o, const unsigned long long* graph_e
   }
   std::vector<int> prev, cur;
   for (int l = 0; l < L; ++l) {
+    OFF_CUDA(cudaGraphLaunch((cudaGraphExec_t)graph_execs[l], cs), "segment launch");  // (5) of l-1, (2)
+    if (l > 0) {  // (6) unpin layer l-1 before layer l's window, as engine.py:152-153 -> 131
+      if (int rc = mobile_offload_release(o, l - 1, prev.data(), (int)prev.size(), stream)) return rc;
+    }
     if (planned) {  // (1) issue window
       std::vector<std::tuple<int, int, int>> kept;
       size_t i = 0;
@@ -247,10 +263,6 @@ int mobile_offload_run_pass(mobile_offload* o, const unsigned long long* graph_e
       }
       kept.insert(kept.end(), waiting.begin() + i, waiting.end());
       waiting.swap(kept);
-    }
-    OFF_CUDA(cudaGraphLaunch((cudaGraphExec_t)graph_execs[l], cs), "segment launch");  // (2)
-    if (l > 0) {
-      if (int rc = mobile_offload_release(o, l - 1, prev.data(), (int)prev.size(), stream)) return rc;  // (6)
     }
     cur.clear();
     if (planned) {
@@ -272,6 +284,142 @@ int mobile_offload_run_pass(mobile_offload* o, const unsigned long long* graph_e
   (void)slot_dev_row;
   (void)slot_row_bytes;
   if (fresh_out) *fresh_out = fresh;
+  return MOBILE_OK;
+}
+
+// ---------------------------------------------------------------- zero-sync
+// The copy for slot s is ordered after the kernel's release of the slot's
+// previous occupant with cuStreamWaitValue32 on the kernel's progress counter,
+// and announces completion with cuStreamWriteValue32(done[s], ticket): the
+// kernel streams an expert's tiles once done[s] >= its ticket.  No host sync.
+int mobile_offload_zs_enable(mobile_offload* o, void** done_out, void** prog_out, void** prog_mirror_dev_out,
+                             void** prog_mirror_host_out) {
+  if (!o->zs_done) {
+    void* hd = nullptr;
+    if (cudaMalloc(&o->zs_done, sizeof(unsigned) * o->slots) != cudaSuccess ||
+        cudaMemset(o->zs_done, 0, sizeof(unsigned) * o->slots) != cudaSuccess ||
+        cudaMalloc(&o->zs_prog, sizeof(unsigned) * 4) != cudaSuccess ||
+        cudaMemset(o->zs_prog, 0, sizeof(unsigned) * 4) != cudaSuccess ||
+        cudaHostAlloc((void**)&o->zs_prog_h, sizeof(unsigned) * 4, cudaHostAllocMapped | cudaHostAllocPortable) !=
+            cudaSuccess ||
+        cudaHostGetDevicePointer(&hd, o->zs_prog_h, 0) != cudaSuccess) {
+      mobile::set_error("offload: zero-sync state allocation failed");
+      return MOBILE_ERR_CUDA;
+    }
+    o->zs_prog_h[0] = 0u;
+    o->zs_prog_hd = (unsigned*)hd;
+    o->zs_ticket.assign(o->slots, 0u);
+    o->zs_last_use.assign(o->slots, 0ll);
+  }
+  *done_out = o->zs_done;
+  *prog_out = o->zs_prog;
+  *prog_mirror_dev_out = o->zs_prog_hd;
+  *prog_mirror_host_out = o->zs_prog_h;
+  return MOBILE_OK;
+}
+
+// Stream memory operations come from the driver API; they are resolved at run
+// time so libmobile.so does not link libcuda (it must import on GPU-less hosts).
+typedef CUresult (*StreamValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static StreamValueFn driver_fn(const char* name) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return (StreamValueFn)fn;
+}
+static StreamValueFn stream_wait_value() {
+  static StreamValueFn f = driver_fn("cuStreamWaitValue32");
+  return f;
+}
+static StreamValueFn stream_write_value() {
+  static StreamValueFn f = driver_fn("cuStreamWriteValue32");
+  return f;
+}
+
+static int zs_issue_copy(mobile_offload* o, int layer, int expert, int slot) {
+  CUstream cs = (CUstream)o->copy;
+  const long long need = o->zs_last_use[slot];
+  if (!stream_wait_value() || !stream_write_value()) {
+    mobile::set_error("offload: cuStreamWaitValue32 / cuStreamWriteValue32 unavailable");
+    return MOBILE_ERR_UNSUPPORTED;
+  }
+  if (need > 0) {  // the slot's previous occupant must have been consumed
+    if (stream_wait_value()(cs, (CUdeviceptr)o->zs_prog, (cuuint32_t)need, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
+      mobile::set_error("offload: cuStreamWaitValue32 failed");
+      return MOBILE_ERR_CUDA;
+    }
+  }
+  const char* src = o->host + (long long)layer * o->layer_stride + (long long)expert * o->expert_stride;
+  char* dst = o->pool + (long long)slot * o->expert_bytes;
+  OFF_CUDA(cudaMemcpyAsync(dst, src, (size_t)o->expert_bytes, cudaMemcpyHostToDevice, o->copy), "expert H2D");
+  const unsigned t = ++o->zs_ticket[slot];
+  if (stream_write_value()(cs, (CUdeviceptr)(o->zs_done + slot), (cuuint32_t)t, CU_STREAM_WRITE_VALUE_DEFAULT) !=
+      CUDA_SUCCESS) {
+    mobile::set_error("offload: cuStreamWriteValue32 failed");
+    return MOBILE_ERR_CUDA;
+  }
+  o->slot_layer[slot] = layer;
+  o->slot_expert[slot] = expert;
+  o->bytes += o->expert_bytes;
+  o->transfers++;
+  return MOBILE_OK;
+}
+
+// Required experts of `layer` (engine.py:137-145): request + pin; misses are
+// issued; out2[2i] = slot, out2[2i+1] = ticket to wait for.  `now_prog` is the
+// progress value the kernel has certainly reached (deadlock retry: the host
+// waits for the kernel / copies through wait_fn).
+int mobile_offload_zs_require(mobile_offload* o, int layer, const int* experts, int n, int* out2, int* issued_out,
+                              int (*wait_fn)(void*), void* wait_ctx) {
+  int fresh = 0;
+  for (int i = 0; i < n; ++i) {
+    const int e = experts[i];
+    int status = 0, slot = -1;
+    double ready = 0;
+    int st = mobile_cache_request(o->cache, layer, e, o->clock, 0, nullptr, kInf, &status, &ready, &slot);
+    if (st == MOBILE_ERR_DEADLOCK && wait_fn) {  // the simulator's stall: drain, settle, retry once
+      if (int rc = wait_fn(wait_ctx)) return rc;
+      OFF_CUDA(cudaStreamSynchronize(o->copy), "deadlock stall (copy)");
+      settle_all(o);
+      st = mobile_cache_request(o->cache, layer, e, o->clock, 0, nullptr, kInf, &status, &ready, &slot);
+    }
+    if (st != MOBILE_OK) return st;
+    if (status == MOBILE_STATUS_ISSUED) {
+      if (int r = zs_issue_copy(o, layer, e, slot)) return r;
+      ++fresh;
+    }
+    mobile_cache_pin(o->cache, layer, e);
+    if (ready == kInf) o->awaited.emplace_back(layer, e);
+    out2[2 * i] = slot;
+    out2[2 * i + 1] = (int)o->zs_ticket[slot];
+  }
+  if (issued_out) *issued_out = fresh;
+  return MOBILE_OK;
+}
+
+long long* mobile_offload_zs_base(mobile_offload* o) { return &o->zs_base; }
+
+int mobile_offload_zs_prefetch(mobile_offload* o, int layer, int expert, int* status_out) {
+  int status = 0, slot = -1;
+  double ready = 0;
+  int st = mobile_cache_request(o->cache, layer, expert, o->clock, 1, nullptr, kInf, &status, &ready, &slot);
+  if (st != MOBILE_OK) return st;
+  if (status == MOBILE_STATUS_ISSUED)
+    if (int r = zs_issue_copy(o, layer, expert, slot)) return r;
+  if (status_out) *status_out = status;
+  return MOBILE_OK;
+}
+
+// Unpin (engine.py:152-153); the slots stay busy until the kernel's progress
+// counter reaches `release_prog` (it has consumed this layer).
+int mobile_offload_zs_release(mobile_offload* o, int layer, const int* experts, int n, long long release_prog) {
+  for (int i = 0; i < n; ++i) {
+    int slot = -1;
+    if (mobile_cache_lookup(o->cache, layer, experts[i], nullptr, &slot) == MOBILE_OK)
+      o->zs_last_use[slot] = release_prog;
+    mobile_cache_unpin(o->cache, layer, experts[i]);
+  }
   return MOBILE_OK;
 }
 

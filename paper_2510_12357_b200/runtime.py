@@ -25,6 +25,7 @@ segments, prefetches and waits are enqueued back to back.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import torch
 
@@ -38,7 +39,7 @@ KINDS = ("little", "big", "full")
 
 class StepEngine:
     def __init__(self, dm: DeviceModel, batch: int, max_len: int, runtime=None, graphs: bool = True,
-                 persistent: bool | None = None):
+                 persistent: bool | None = None, zero_sync: bool | None = None):
         s = dm.spec
         if batch > 8:
             raise ValueError("StepEngine: batch <= 8 (GEMV decode path)")
@@ -60,7 +61,8 @@ class StepEngine:
         self.xa = torch.empty(B, d, dtype=f32, device=dev)
         self.k = {"little": s.k_little, "big": s.k_big, "full": s.k_big}
         self.k_tok = {kd: torch.full((B,), self.k[kd], dtype=i32, device=dev) for kd in KINDS}
-        self.states = {kd: torch.empty(L, B, E, dtype=f32, device=dev) for kd in KINDS}
+        # zero-initialised: the graph warm-up replays states["little"] before any real pass
+        self.states = {kd: torch.zeros(L, B, E, dtype=f32, device=dev) for kd in KINDS}
         self.idx = {kd: torch.empty(L, B, self.k[kd], dtype=i32, device=dev) for kd in KINDS}
         self.ones = torch.ones(B, dtype=torch.uint8, device=dev)
         self.head = {kd: dict(conf=torch.empty(B, dtype=f32, device=dev), argmax=torch.empty(B, dtype=i32, device=dev),
@@ -78,6 +80,10 @@ class StepEngine:
         # offload segment.  None = use it whenever the shape is supported.
         self.persistent = persistent
         self.dp = {}
+        # zero-sync offload (persistent + offloaded experts): one launch per pass,
+        # the C++ cache driver answers each layer's published selection while
+        # the kernel runs (decode_pass.cu mobile_dp_run_offload_pass)
+        self.zero_sync = zero_sync if zero_sync is not None else os.environ.get("MOBILE_ZS", "1") != "0"
 
     # ------------------------------------------------------------------ kernels
     def _attn(self, l: int, x_in: torch.Tensor) -> torch.Tensor:
@@ -276,6 +282,8 @@ class StepEngine:
             for kd in KINDS:
                 self.run[kd] = [self._capture((kd, l), lambda kd=kd, l=l: self._seg(kd, l)) for l in range(L + 1)]
         torch.cuda.synchronize()
+        if self.dp:
+            self.dp_flags.zero_()
         return self
 
     # ------------------------------------------------------------------ passes
@@ -286,10 +294,31 @@ class StepEngine:
     def pass_resident(self, kind: str):
         self._launch(self.run[kind])
 
+    def _pass_offload_zs(self, kind: str):
+        """Whole offloaded pass in one persistent launch; the C++ driver runs
+        the cache protocol against the running kernel (no per-layer sync)."""
+        rt, s = self.rt, self.spec
+        planned = kind == "big"
+        targets, k = None, 0
+        if planned:
+            with torch.cuda.stream(self.stream):
+                idx, _ = K.topk_rows(self.states["little"][:, 0].contiguous(), s.k_big)
+                flat = idx.cpu().reshape(-1).tolist()  # one D2H for the whole planned pass
+            k = s.k_big
+            targets = (C.c_int * len(flat))(*flat)
+        fresh = C.c_int()
+        K._count()
+        N.check(N.lib.mobile_dp_run_offload_pass(self.dp[kind], rt.h, int(planned), targets, k, rt.lookahead,
+                                                 self.stream.cuda_stream, C.byref(fresh)), "zero-sync offload pass")
+        rt.fresh += fresh.value
+
     def pass_offload(self, kind: str):
         """Drive the L+1 segments with the engine.py:121-169 protocol: in C++
         (mobile_offload_run_pass) when the segments are captured graphs, else
-        from Python (eager mode, used for per-kernel instrumentation)."""
+        from Python (eager mode, used for per-kernel instrumentation).  With the
+        persistent kernel and zero_sync: one launch per pass."""
+        if self.dp and self.zero_sync:
+            return self._pass_offload_zs(kind)
         if self.use_graphs:
             return self._pass_offload_native(kind)
         rt, L = self.rt, self.spec.num_layers
@@ -303,6 +332,9 @@ class StepEngine:
             waiting = list(plan_from_targets(targets, rt.lookahead).entries)
         prev = None
         for l in range(L):
+            self._launch(segs[l])  # experts(l-1), (2) attention(l), routing(l)
+            if prev is not None:  # (6) unpin l-1 before layer l's window (engine.py:152-153, 131)
+                self._release(l - 1, prev)
             if kind == "big":  # (1) issue window at the layer boundary (engine.py:98-119)
                 kept = []
                 for i, e in enumerate(waiting):
@@ -317,9 +349,6 @@ class StepEngine:
                     else:
                         N.check(rc, "offload prefetch")
                 waiting = kept
-            self._launch(segs[l])  # experts(l-1), (2) attention(l), routing(l)
-            if prev is not None:
-                self._release(l - 1, prev)
             if kind == "big":
                 experts = targets[l]
             else:  # on demand: the layer's selection comes back to the host

@@ -71,3 +71,32 @@ def test_persistent_equals_per_op_real_shape(cuda_ok, preset):
         assert abs(ca - cb) <= 1e-3 * max(cb, 1e-6)
         assert a.head["little"]["argmax"].item() == b.head["little"]["argmax"].item()
     assert int(a.dp_flags.item()) == 0
+
+
+@pytest.mark.parametrize("slots", [6, 14])
+def test_zero_sync_offload_equals_segmented(cuda_ok, slots):
+    """One-launch zero-sync offloaded passes vs the segmented driver: same
+    tokens, selections, cache decisions (hits / issued / coalesced) and
+    transfers (engine.py:121-169 protocol either way)."""
+    from paper_2510_12357_b200.offload import OffloadRuntime
+    from paper_2510_12357_b200.runtime import StepEngine
+    from tests.test_runtime_gpu import _offload_dm
+    o, ms, dm0 = matched(QWEN_MINI, "bfloat16")
+    res = []
+    for zs in (False, True):
+        dm = _offload_dm(dm0, ms)
+        rt = OffloadRuntime(dm.dw, slots=slots, lookahead=1)
+        eng = StepEngine(dm, 1, 64, runtime=rt, persistent=True, zero_sync=zs).build(gamma=0.7)
+        eng.prefill([3, 17, 42, 7])
+        toks, sels = [], []
+        for i in range(12):
+            tok, fb = eng.step(forced_fallback=(i % 3 == 1), full=(i % 5 == 4))
+            toks.append(tok)
+            sels.append(eng.idx["little"][:, 0].cpu().tolist())
+        st = rt.cache.stats
+        res.append((toks, sels, (st.hits, st.issued, st.coalesced), rt.counters()))
+        assert int(eng.dp_flags.item()) == 0
+    assert res[0][0] == res[1][0]
+    assert res[0][1] == res[1][1]
+    assert res[0][2] == res[1][2]
+    assert res[0][3] == res[1][3]
