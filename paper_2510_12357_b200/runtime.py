@@ -80,6 +80,8 @@ class StepEngine:
         # offload segment.  None = use it whenever the shape is supported.
         self.persistent = persistent
         self.dp = {}
+        self.record_passes = False  # metrics.measure_stream
+        self.pass_log: list = []
         # zero-sync offload (persistent + offloaded experts): one launch per pass,
         # the C++ cache driver answers each layer's published selection while
         # the kernel runs (decode_pass.cu mobile_dp_run_offload_pass)
@@ -399,10 +401,23 @@ class StepEngine:
                 "offload release")
 
     def run_pass(self, kind: str):
+        rec = getattr(self, "record_passes", False)
+        if rec:  # metrics.measure_stream: device time + cache accounting of this pass
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(self.stream)
+            fresh0 = self.rt.fresh if self.rt else 0
+            xfer0 = self.rt.counters()[1] if self.rt else 0
         if self.rt is None:
             self.pass_resident(kind)
         else:
             self.pass_offload(kind)
+        if rec:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(self.stream)
+            demand = self.spec.num_layers * self.k[kind] * self.B  # required requests of the pass
+            misses = (self.rt.fresh - fresh0) if self.rt else 0
+            fresh = (self.rt.counters()[1] - xfer0) if self.rt else 0
+            self.pass_log.append((kind, e0, e1, demand - misses, misses, fresh))
 
     # ------------------------------------------------------------------ decode API
     def prefill(self, prompt: list[int], prefill_k: int | None = None):
