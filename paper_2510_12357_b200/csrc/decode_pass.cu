@@ -1527,7 +1527,12 @@ int mobile_dp_create(const mobile_dp_model* m, mobile_dp** out) {
   const int G = sm_count();
   o->grid = G;
   // ---- shared memory: ring of (64 KB weights + TT activation slices) + xbuf
-  const int xslice = kChunk / eb * 4;
+  // staged activation slices: TT rows of at most one K chunk of the widest
+  // staged input (routed down K = ffn, shared down K = shared_ffn)
+  const int kc_elems = kChunk / eb;
+  int xk = std::min(kc_elems, m->ffn);
+  if (S) xk = std::max(xk, std::min(kc_elems, m->shared_ffn));
+  const int xslice = (xk * 4 + 127) / 128 * 128;
   o->stage_bytes = kWBytes + o->TT * xslice;
   const int hd = d / m->H;
   const size_t xbuf = std::max((size_t)B * d * 4, (size_t)kCW * (hd + kAttnPart) * 4);

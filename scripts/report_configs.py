@@ -1,0 +1,106 @@
+"""Per-config report (BASELINE.json configs C2-C5, 1 GPU, experts HBM-resident):
+decode pass times of the persistent kernel for the little / replayed big /
+full-top-k passes, MoBiLE tokens/s at the paper's fallback ratio vs the
+full-top-k baseline, each pass's HBM roofline fraction; prefill tokens/s
+(per-op engine: tcgen05 grouped GEMM experts) with the expert GEMMs' tensor
+roofline fraction.  Writes JSON to stdout (profiles/r1_configs.json).
+
+    python scripts/report_configs.py [c2 c3 c4 c5]
+"""
+import json
+import sys
+import time
+from dataclasses import replace
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+from paper_2510_12357_b200.model import DeviceModel  # noqa: E402
+from paper_2510_12357_b200.presets import NAMES, PRESETS  # noqa: E402
+from paper_2510_12357_b200.runtime import StepEngine  # noqa: E402
+from paper_2510_12357_b200.weights import DeviceWeights  # noqa: E402
+
+PK = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+R_PAPER = {"c2": 0.21, "c3": 0.11, "c4": 0.11, "c5": 0.11}  # PAPER.md fallback ratios (OLMoE 0.21, Qwen 0.11)
+PROMPT = {"c2": 512, "c3": 512, "c4": 512, "c5": 2048}
+BATCHES = {"c4": (1, 2, 4)}
+
+
+def pass_bytes(spec, dw, kind_k, ctx, B):
+    eb, d, L = dw.elem_bytes, spec.hidden_dim, spec.num_layers
+    experts = min(spec.num_experts, B * kind_k) * dw.expert_bytes
+    per_layer = (4 * d * d + (spec.num_experts + dw.n_gate_rows) * d) * eb + experts + spec.n_shared * dw.shared_bytes \
+        + B * 2 * ctx * d * 4
+    return L * per_layer + spec.vocab_size * d * eb
+
+
+def time_graph(eng, kind, reps=10):
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(eng.stream):
+        e0.record()
+        for _ in range(reps):
+            eng.graphs[kind].replay()
+        e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps / 1e3
+
+
+out = {"peaks": {"hbm_gbs": PK["hbm_gbs"], "bf16_tflops": PK["bf16_tflops"]}}
+for name in sys.argv[1:] or ["c2", "c3", "c4", "c5"]:
+    spec = PRESETS[name]
+    t0 = time.time()
+    dw = DeviceWeights.random(spec, torch.device("cuda"), seed=0)
+    dm = DeviceModel(dw)
+    res = {"model": NAMES[name], "init_s": round(time.time() - t0, 1), "decode": {}}
+    ctx = PROMPT[name]
+    for B in BATCHES.get(name, (1,)):
+        eng = StepEngine(dm, B, ctx + 48, persistent=True).build()
+        # B sequences at a common position: fill the caches with random K/V rows
+        eng.sess.kc.normal_()
+        eng.sess.vc.normal_()
+        eng.pos.fill_(ctx)
+        eng.tok.copy_(torch.randint(1, spec.vocab_size, (B,), device="cuda", dtype=torch.int32))
+        for kd in ("little", "big", "full"):
+            eng.graphs[kd].replay()
+        torch.cuda.synchronize()
+        r = R_PAPER[name]
+        row = {"dp_info": eng.dp_info()}
+        for kd in ("little", "big", "full"):
+            t = time_graph(eng, kd)
+            nb = pass_bytes(spec, dw, eng.k[kd], ctx, B)
+            row[kd] = {"ms": round(t * 1e3, 3), "bytes": nb, "gbs": round(nb / t / 1e9, 1),
+                       "hbm_frac": round(nb / t / 1e9 / PK["hbm_gbs"], 3)}
+        t_mob = row["little"]["ms"] + r * row["big"]["ms"]
+        row["mobile_tokens_s"] = round(B * 1e3 / t_mob, 2)
+        row["full_topk_tokens_s"] = round(B * 1e3 / row["full"]["ms"], 2)
+        row["speedup_vs_full_topk"] = round(row["full"]["ms"] / t_mob, 4)
+        row["r"] = r
+        row["note"] = "tokens/s = B / (T_l + r T_b), T from graph-replayed persistent passes, ctx %d" % ctx
+        res["decode"][f"B{B}"] = row
+        del eng
+        torch.cuda.empty_cache()
+    # prefill: the per-op engine (attention + tcgen05 grouped-GEMM experts) over the prompt
+    sess_eng = StepEngine(dm, 1, ctx + 8, persistent=False)
+    prompt = np.random.default_rng(0).integers(1, spec.vocab_size, size=ctx + 1).tolist()
+    sess_eng.prefill(prompt)  # warm-up (TMA maps, scratch)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    sess_eng.prefill(prompt)
+    torch.cuda.synchronize()
+    tp = time.perf_counter() - t1
+    I, Is, d = spec.ffn, spec.shared_ffn, spec.hidden_dim
+    moe_flops = 2.0 * ctx * spec.num_layers * (spec.k_big * 3 * d * I + spec.n_shared * 3 * d * Is)
+    res["prefill"] = {"tokens": ctx, "ms": round(tp * 1e3, 2), "tokens_s": round(ctx / tp, 1),
+                      "expert_gemm_tflop": round(moe_flops / 1e12, 3),
+                      "expert_tflops_whole_prefill": round(moe_flops / tp / 1e12, 1),
+                      "note": "wall clock of the full prefill (attention in torch, experts on the tcgen05 grouped "
+                              "GEMM); the GEMM kernel alone: scripts/bench_gemm.py"}
+    out[name] = res
+    print(json.dumps({name: res}), flush=True)
+    del sess_eng, dm, dw
+    torch.cuda.empty_cache()
+print(json.dumps(out, indent=1))
