@@ -100,3 +100,46 @@ def test_zero_sync_offload_equals_segmented(cuda_ok, slots):
     assert res[0][1] == res[1][1]
     assert res[0][2] == res[1][2]
     assert res[0][3] == res[1][3]
+
+
+@pytest.mark.parametrize("preset,B", [("c4", 2), ("c4", 4), ("c3", 3), ("c5", 1)])
+def test_persistent_batched_and_wide_equal_per_op(cuda_ok, preset, B):
+    """Batched decode (B = 2..4 sequences, the TT = 2 / 4 kernels) and the
+    Mixtral width (d = 4096, 2-stage ring): one pass of every kind from the
+    same random KV state, persistent kernel vs per-op engine."""
+    from paper_2510_12357_b200.model import DeviceModel
+    from paper_2510_12357_b200.presets import PRESETS
+    from paper_2510_12357_b200.runtime import StepEngine
+    from paper_2510_12357_b200.weights import DeviceWeights
+    spec = replace(PRESETS[preset], num_layers=2)
+    dm = DeviceModel(DeviceWeights.random(spec, torch.device("cuda"), seed=4))
+    ctx = 37
+    engines = [StepEngine(dm, B, 64, persistent=p).build() for p in (True, False)]
+    g = torch.Generator(device="cuda").manual_seed(0)
+    kc = torch.randn(engines[0].sess.kc.shape, device="cuda", generator=g)
+    vc = torch.randn(engines[0].sess.vc.shape, device="cuda", generator=g)
+    tok = torch.randint(1, spec.vocab_size, (B,), device="cuda", dtype=torch.int32, generator=g)
+    for kd in ("little", "big", "full"):
+        for e in engines:
+            e.sess.kc.copy_(kc)
+            e.sess.vc.copy_(vc)
+            e.pos.fill_(ctx)
+            e.tok.copy_(tok)
+            if kd == "big":  # replay the same little logits in both
+                e.states["little"].copy_(engines[1].states["little"])
+            torch.cuda.synchronize()  # state set on the default stream; passes run on the engine's stream
+            e.run_pass(kd)
+        torch.cuda.synchronize()
+        a, b = engines
+        sa, sb = a.states[kd].cpu().numpy(), b.states[kd].cpu().numpy()
+        assert np.abs(sa - sb).max() <= 1e-3 * np.abs(sb).max(), (kd, np.abs(sa - sb).max(axis=-1))
+        ia, ib = a.idx[kd].cpu().numpy(), b.idx[kd].cpu().numpy()
+        for l in range(spec.num_layers):
+            for s in range(B):
+                assert selections_agree([ia[l, s].tolist()], [ib[l, s].tolist()], sb[l:l + 1, s], tol=1e-4)[0]
+        ca, cb = a.head[kd]["conf"].cpu().numpy(), b.head[kd]["conf"].cpu().numpy()
+        assert np.abs(ca - cb).max() <= 1e-3 * max(np.abs(cb).max(), 1e-6), kd
+        assert (a.head[kd]["argmax"].cpu() == b.head[kd]["argmax"].cpu()).all(), kd
+        # the new position's K/V rows went to the same cache slots
+        assert torch.allclose(a.sess.kc[:, :, :, ctx], b.sess.kc[:, :, :, ctx], rtol=1e-3, atol=1e-3)
+    assert int(engines[0].dp_flags.item()) == 0
