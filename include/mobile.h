@@ -107,6 +107,12 @@ int mobile_head_confidence(const float* x, const void* w_head, int w_dtype, int 
                            float logit_scale, float gamma, float* logits_out, float* conf_out,
                            int* argmax_out, uint8_t* fallback_out, void* workspace, void* stream);
 
+/* The head's outputs from precomputed raw logits rows (T, V) f32 (large-batch
+ * decode, where LN(x) @ head runs as a tcgen05 GEMM): l = raw * logit_scale,
+ * conf / argmax / fallback exactly as mobile_head_confidence. */
+int mobile_logits_confidence(const float* logits, int T, int V, float logit_scale, float gamma,
+                             float* conf_out, int* argmax_out, uint8_t* fallback_out, void* stream);
+
 /* probs = softmax(logits) row-wise (toymoe.py:91-94), T rows of V; f32/f64
  * in, f32/f64 out (f64 accumulation when either side is f64). */
 int mobile_softmax_rows(const void* logits, int in_dtype, void* probs, int out_dtype, int T, int V,
@@ -213,6 +219,8 @@ int mobile_stream_head(const float* x_ln, int T, int d, const void* w_head, int 
  *   epi 1: SwiGLU on 16-column groups [8 gate | 8 up] -> bf16
  *          out_bf16[r * ldo + e*out_expert_stride + f]
  *   epi 2: bf16 store of D.
+ *   epi 3: out_f32[r * ldo + e*out_expert_stride + n] += D (residual
+ *          projections of the large-batch decode step: out holds x).
  * K % 64 == 0, N % 128 == 0; max_tiles bounds the number of 128x128 tiles
  * (surplus CTAs exit); the tile list is derived on the device. */
 int mobile_grouped_gemm(const void* A, int rows_a, int K, const void* B_base, long long b_expert_stride,
@@ -393,7 +401,7 @@ typedef struct mobile_dp_model {
   float* conf;                /* (B,) max softmax prob */
   int* argmax;                /* (B,) */
   uint8_t* fallback;          /* (B,) conf <= gamma (policy.py:69-79) */
-  int* flags;                 /* |= 1 non-finite router logits, 4/8 watchdog */
+  int* flags;                 /* |= 1 non-finite router logits, 4/8 watchdog, 16 pos >= max_len */
 } mobile_dp_model;
 typedef struct mobile_dp mobile_dp;
 int mobile_dp_create(const mobile_dp_model* m, mobile_dp** out);

@@ -80,6 +80,7 @@ _SIGS = {
     "mobile_head_ws_bytes": ([I32, I32], SZ),
     "mobile_head_confidence": ([P, P, I32, I32, I32, I32, F, F, P, P, P, P, P, P], I32),
     "mobile_softmax_rows": ([P, I32, P, I32, I32, I32, P], I32),
+    "mobile_logits_confidence": ([P, I32, I32, F, F, P, P, P, P], I32),
     "mobile_probs_check": ([P, I32, I32, P, P], I32),
     "mobile_permute": ([P, P, I32, I32, I32, P, P, P, P], I32),
     "mobile_expert_gate_up": ([P, P, P, P, I32, I32, I32, I32, I32, P, I64, P, I32, I32, P, P], I32),
@@ -140,6 +141,30 @@ for _name, (_args, _ret) in _SIGS.items():
     _f = getattr(lib, _name)
     _f.argtypes = _args
     _f.restype = _ret
+
+
+# Finalizers run wherever the GC fires -- possibly inside another engine's
+# CUDA-graph capture, where the cudaFree / cudaFreeHost / stream destroys of a
+# native handle would invalidate that capture.  Destroys are queued instead
+# and run at the next safe point (`reap`, called before graph captures and
+# handle creation), with the torch objects the handle points into kept alive.
+_deferred: list = []
+
+
+def defer_destroy(fn_name: str, handle, keepalive=()) -> None:
+    _deferred.append((fn_name, handle, tuple(keepalive)))
+
+
+def reap() -> None:
+    """Run queued native destroys (not during a capture: callers ensure it)."""
+    if not _deferred:
+        return
+    import torch
+    if torch.cuda.is_available():
+        torch.cuda.synchronize()
+    while _deferred:
+        fn_name, handle, _keep = _deferred.pop(0)
+        getattr(lib, fn_name)(handle)
 
 
 def last_error() -> str:

@@ -861,7 +861,14 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (tid < P.B) spos[tid] = P.pos[tid];
+  if (tid < P.B) {
+    int p = P.pos[tid];
+    if (p < 0 || p >= P.max_len) {  // position outside the KV cache: flag it, stay in bounds
+      if (blockIdx.x == 0) atomicOr(P.flags, 16);
+      p = 0;
+    }
+    spos[tid] = p;
+  }
   __syncthreads();
 
   if (warp == kCW) {

@@ -129,6 +129,10 @@ __global__ void attn_decode_kernel(const float* __restrict__ qkv, float* __restr
   const int hd = d / H;
   const int p = pos[b];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (p < 0 || p >= max_len) {  // position outside the cache: poison the output, touch nothing
+    for (int e = threadIdx.x; e < d / H; e += blockDim.x) out[(size_t)b * d + hh * (d / H) + e] = __int_as_float(0x7fc00000);
+    return;
+  }
   float* q = sc + max_len;
   const float* src = qkv + (size_t)b * 3 * d;
   // head-major cache (B, H, max_len, hd)

@@ -16,6 +16,7 @@
 //               (warp w reads TMEM lanes 32*(w%4)..), then
 //                 SWIGLU: 16-column groups [8 gate | 8 up] -> silu(g)*u, bf16
 //                 STORE : f32, row scattered to its pair id (combine input)
+//                 ACCUM : f32 out += acc (residual projections: out holds x)
 // Tiles are enumerated on the device from the expert offsets, so no host sync
 // is needed between routing and the GEMM; surplus CTAs exit.
 #include "common.cuh"
@@ -30,7 +31,7 @@ constexpr int kGgABytes = kGgBM * kGgBK * 2;  // 16 KB
 constexpr int kGgBBytes = kGgBN * kGgBK * 2;  // 16 KB
 constexpr int kGgStageBytes = kGgABytes + kGgBBytes;
 
-enum GgEpi { kGgStoreF32Scatter = 0, kGgSwigluBf16 = 1, kGgStoreBf16 = 2 };
+enum GgEpi { kGgStoreF32Scatter = 0, kGgSwigluBf16 = 1, kGgStoreBf16 = 2, kGgAccumF32 = 3 };
 
 struct GgArgs {
   CUtensorMap tma_a;       // (K, rows_a)      box (64, 128)
@@ -180,6 +181,14 @@ __global__ void __launch_bounds__(kGgThreads, 1) grouped_gemm_kernel(const __gri
             pw[j] = *reinterpret_cast<const uint32_t*>(&b2);
           }
           *reinterpret_cast<uint4*>(o) = pk;
+        } else if (a.epi == kGgAccumF32) {
+          float* o = a.out_f32 + (size_t)row * a.ldo + (size_t)T.e * a.out_expert_stride + n;
+#pragma unroll
+          for (int j = 0; j < 16; j += 4) {
+            float4 r4 = *reinterpret_cast<const float4*>(o + j);
+            r4.x += v[j]; r4.y += v[j + 1]; r4.z += v[j + 2]; r4.w += v[j + 3];
+            *reinterpret_cast<float4*>(o + j) = r4;
+          }
         } else if (a.epi == kGgStoreF32Scatter) {
           const int orow = a.row_to_pair ? a.row_to_pair[row] : row;
           float* o = a.out_f32 + (size_t)orow * a.ldo + (size_t)T.e * a.out_expert_stride + n;

@@ -207,6 +207,50 @@ static int head_grid_x(int V) {
   return g < 1 ? 1 : g;
 }
 
+// ---------------------------------------------------------------- confidence of logits rows
+// Large-batch decode: the head product runs as a tcgen05 GEMM (raw logits,
+// T x V f32); this reduces each row to the head's outputs with the same
+// arithmetic as head_kernel (l = raw * scale, conf = 1 / sum exp(l - max),
+// first maximiser).  One CTA per row; merges in a fixed (thread, warp) order.
+constexpr int kConfThreads = 512;
+
+__device__ __forceinline__ void conf_merge(float& M, float& S, int& A, float m, float s, int a) {
+  if (s == 0.f) return;
+  if (m > M) { S = S * expf(M - m) + s; M = m; A = a; }
+  else { S += s * expf(m - M); if (m == M && a < A) A = a; }
+}
+
+__global__ void __launch_bounds__(kConfThreads) logits_conf_kernel(const float* __restrict__ logits, int V,
+                                                                   float scale, float gamma, float* conf_out,
+                                                                   int* argmax_out, uint8_t* fallback_out) {
+  __shared__ float rm[kConfThreads / 32], rs[kConfThreads / 32];
+  __shared__ int ra[kConfThreads / 32];
+  pdl_trigger();
+  pdl_wait();
+  const int t = blockIdx.x;
+  const float* row = logits + (size_t)t * V;
+  float m = -INFINITY, s = 0.f;
+  int arg = 0x7fffffff;
+  for (int i = threadIdx.x; i < V; i += kConfThreads) online_merge(m, s, arg, row[i] * scale, 1.0f, i);
+  for (int o = 16; o; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    const int a2 = __shfl_xor_sync(0xffffffffu, arg, o);
+    conf_merge(m, s, arg, m2, s2, a2);
+  }
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { rm[warp] = m; rs[warp] = s; ra[warp] = arg; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M = -INFINITY, S = 0.f;
+    int A = 0x7fffffff;
+    for (int w = 0; w < kConfThreads / 32; ++w) conf_merge(M, S, A, rm[w], rs[w], ra[w]);
+    const float conf = 1.0f / S;
+    conf_out[t] = conf;
+    if (argmax_out) argmax_out[t] = A;
+    if (fallback_out) fallback_out[t] = conf <= gamma ? 1 : 0;
+  }
+}
+
 // ---------------------------------------------------------------- softmax rows
 // probs = exp(l - max) / sum (toymoe.py:91-94); accumulation in Acc (double
 // when either side is f64, so the fp64 API keeps |sum - 1| ~ 1e-16).
@@ -319,4 +363,12 @@ extern "C" int mobile_probs_check(const void* probs, int dtype, int V, double* o
   else { set_error("probs: unsupported dtype %d", dtype); return MOBILE_ERR_UNSUPPORTED; }
   MOBILE_CHECK_LAUNCH("probs_check");
   return MOBILE_OK;
+}
+
+extern "C" int mobile_logits_confidence(const float* logits, int T, int V, float logit_scale, float gamma,
+                                        float* conf_out, int* argmax_out, uint8_t* fallback_out, void* stream) {
+  if (T < 0 || V <= 0 || !logits || !conf_out) { set_error("logits_confidence: bad arguments T=%d V=%d", T, V); return MOBILE_ERR_INVALID; }
+  if (T == 0) return MOBILE_OK;
+  return launch_pdl(logits_conf_kernel, dim3(T), dim3(kConfThreads), 0, (cudaStream_t)stream, 1, "logits_confidence",
+                    logits, V, logit_scale, gamma, conf_out, argmax_out, fallback_out);
 }

@@ -275,7 +275,7 @@ def down_combine(groups, w_dtype, max_tokens, x, Y, gates, k_tok, Y_shared, n_sh
     return x_out
 
 
-GG_STORE_F32, GG_SWIGLU_BF16, GG_STORE_BF16 = 0, 1, 2
+GG_STORE_F32, GG_SWIGLU_BF16, GG_STORE_BF16, GG_ACCUM_F32 = 0, 1, 2, 3
 
 
 def _gg_call(A, K, B_base, b_expert_stride, n_slots, n_cols, offsets, active, slot, max_tiles, dense_rows,
@@ -293,6 +293,17 @@ def grouped_gemm(A, K, B_base: int, b_expert_stride: int, n_slots: int, N_: int,
     _count()
     _gg_call(A, K, B_base, b_expert_stride, n_slots, N_, offsets, active, slot, max_tiles, dense_rows, dense_experts,
              epi, out_f32, out_bf16, ldo, out_expert_stride, row_to_pair, stream)
+
+
+def logits_confidence(logits, logit_scale, gamma, out, stream=None):
+    """conf / argmax / fallback of raw logits rows (T, V) f32 (head GEMM output)."""
+    _dev(logits)
+    T, V = logits.shape
+    _count()
+    N.check(N.lib.mobile_logits_confidence(N.ptr(logits), T, V, float(logit_scale), float(gamma), N.ptr(out["conf"]),
+                                           N.ptr(out["argmax"]), N.ptr(out["fallback"]), _s(stream)),
+            "logits_confidence")
+    return out
 
 
 def gather_bf16(src, pairs, div, P, X, stream=None):

@@ -40,13 +40,14 @@ class OffloadRuntime:
         s = dw.spec
         if slots < s.k_big:
             raise ValueError(f"{slots} expert slots cannot hold one layer's k_big={s.k_big} experts")
+        N.reap()  # release handles queued by finalizers before allocating new ones
         self.dw, self.spec = dw, s
         self.L, self.E = s.num_layers, s.num_experts
         self.slots, self.lookahead = slots, lookahead
         dev = dw.device
         self.pool = torch.empty(slots, dw.expert_elems, dtype=dw.wdtype, device=dev)
         self.copy_stream = torch.cuda.Stream(device=dev)
-        host = dw.host_experts
+        host = self._host = dw.host_experts
         eb = dw.expert_bytes
         self.h = N.lib.mobile_offload_create(slots, eb, self.pool.data_ptr(), host.data_ptr(), self.E * eb, eb,
                                              self.L, self.E, self.copy_stream.cuda_stream)
@@ -64,7 +65,8 @@ class OffloadRuntime:
     def __del__(self):
         h = getattr(self, "h", None)
         if h:
-            N.lib.mobile_offload_destroy(h)
+            N.defer_destroy("mobile_offload_destroy", h, (getattr(self, "pool", None), getattr(self, "_host", None),
+                                                           getattr(self, "copy_stream", None)))
             self.h = None
 
     # ------------------------------------------------------------- runtime ops

@@ -35,14 +35,25 @@ from .model import DecodeSession, DeviceModel, pos_rows
 from .policy import plan_from_targets
 
 KINDS = ("little", "big", "full")
+GEMV_MAX_BATCH = 4  # largest batch on the GEMV decode path (stream GEMV / persistent pass tile)
+MAX_BATCH = 1024
 
 
 class StepEngine:
     def __init__(self, dm: DeviceModel, batch: int, max_len: int, runtime=None, graphs: bool = True,
                  persistent: bool | None = None, zero_sync: bool | None = None):
         s = dm.spec
-        if batch > 8:
-            raise ValueError("StepEngine: batch <= 8 (GEMV decode path)")
+        # B <= 8: the GEMV decode path (bulk-copy streaming / persistent pass);
+        # larger batches run the projections and the head as tcgen05 GEMMs
+        self.gemm_path = batch > GEMV_MAX_BATCH
+        if self.gemm_path:
+            if not dm.moe.tc_ok:
+                raise ValueError(f"StepEngine: batch {batch} > {GEMV_MAX_BATCH} needs the tcgen05 GEMM path "
+                                 f"(bf16 SwiGLU shapes)")
+            if runtime is not None:
+                raise ValueError(f"StepEngine: offloaded experts need batch <= {GEMV_MAX_BATCH}")
+            if batch > MAX_BATCH:
+                raise ValueError(f"StepEngine: batch {batch} > {MAX_BATCH}")
         self.dm, self.spec, self.B, self.max_len = dm, s, batch, max_len
         self.rt = runtime
         self.use_graphs = graphs
@@ -68,6 +79,9 @@ class StepEngine:
         self.head = {kd: dict(conf=torch.empty(B, dtype=f32, device=dev), argmax=torch.empty(B, dtype=i32, device=dev),
                               fallback=torch.empty(B, dtype=torch.uint8, device=dev)) for kd in KINDS}
         self.head_ws = K.StreamHeadWorkspace(dev)
+        if self.gemm_path:
+            self.xb = torch.empty(B, d, dtype=torch.bfloat16, device=dev)  # bf16 GEMM operand
+            self.logits = torch.empty(B, s.vocab_size, dtype=f32, device=dev)
         self.gamma = torch.zeros(1)  # host value baked at capture; see set_gamma
         self._gamma = 0.7
         self.graphs: dict = {}
@@ -92,12 +106,33 @@ class StepEngine:
         """q,k,v = LN(x) Wqkv (self.ln holds LN(x_in)); attention; x + att Wo."""
         dw, s = self.dm.dw, self.spec
         d, B = s.hidden_dim, self.B
+        if self.gemm_path:
+            return self._attn_gemm(l, x_in)
         wc = self.dm.moe.wcode
         K.stream_gemv([K.sg_group(w_base=dw.qkv[l].data_ptr(), K=d, rows=3 * d, x=self.ln, dense_T=B,
                                   out=self.qkv)], wc, B)
         K.attn_decode(self.qkv, self.sess.kc[l], self.sess.vc[l], self.pos, s.n_heads, out=self.att)
         K.stream_gemv([K.sg_group(w_base=dw.o[l].data_ptr(), K=d, rows=d, x=self.att, dense_T=B, out=self.xa,
                                   residual=x_in)], wc, B)
+        return self.xa
+
+    def _dense_gemm(self, w: torch.Tensor, n_out: int, out: torch.Tensor, epi: int):
+        """out (B, n_out) [+]= xb @ w^T on the tcgen05 grouped GEMM (dense mode)."""
+        d, B = self.spec.hidden_dim, self.B
+        tiles = (B + 127) // 128 * (n_out // 128)
+        K.grouped_gemm(self.xb, d, w.data_ptr(), w.numel() * w.element_size(), 1, n_out, max_tiles=tiles,
+                       dense_rows=B, dense_experts=1, epi=epi, out_f32=out, ldo=n_out)
+
+    def _attn_gemm(self, l: int, x_in: torch.Tensor) -> torch.Tensor:
+        """Large batch: QKV and O projections as tcgen05 GEMMs (bf16 operands,
+        f32 accumulate), the O projection accumulated onto the residual."""
+        dw, d, B = self.dm.dw, self.spec.hidden_dim, self.B
+        K.gather_bf16(self.ln, None, 1, B, self.xb)
+        self._dense_gemm(dw.qkv[l], 3 * d, self.qkv, K.GG_STORE_F32)
+        K.attn_decode(self.qkv, self.sess.kc[l], self.sess.vc[l], self.pos, self.spec.n_heads, out=self.att)
+        K.gather_bf16(self.att, None, 1, B, self.xb)
+        self.xa.copy_(x_in)
+        self._dense_gemm(dw.o[l], d, self.xa, K.GG_ACCUM_F32)
         return self.xa
 
     def _route(self, l: int, kind: str) -> dict:
@@ -115,6 +150,11 @@ class StepEngine:
     def _head(self, x_last: torch.Tensor, kind: str):
         """LN(x) is already in self.ln (written by the last layer's combine)."""
         s = self.spec
+        if self.gemm_path:
+            K.gather_bf16(self.ln, None, 1, self.B, self.xb)
+            self._dense_gemm(self.dm.dw.head, s.vocab_size, self.logits, K.GG_STORE_F32)
+            K.logits_confidence(self.logits, s.logit_scale, self._gamma, self.head[kind])
+            return
         K.stream_head(self.ln, self.dm.dw.head, self._gamma, s.logit_scale, ws=self.head_ws, out=self.head[kind])
 
     def _offload_loc(self, l: int, kind: str):  # noqa: D401
@@ -231,10 +271,9 @@ class StepEngine:
                 "decode_pass launch")
 
     def __del__(self):
-        lib = getattr(N, "lib", None)
-        if lib is not None:
+        if getattr(N, "lib", None) is not None:
             for h in getattr(self, "dp", {}).values():
-                lib.mobile_dp_destroy(h)
+                N.defer_destroy("mobile_dp_destroy", h)
         self.dp = {}
 
     def _whole_pass(self, kind: str):
@@ -266,11 +305,14 @@ class StepEngine:
     def build(self, gamma: float = 0.7, reuse_gates: bool = False):
         """Capture the graphs for every pass kind (gamma / reuse are baked in)."""
         self._gamma, self.reuse_gates = gamma, reuse_gates
+        N.reap()  # destroys queued by finalizers: never inside the captures below
+        # buffers were zero-filled on the caller's stream; the warm-up runs on ours
+        self.stream.wait_stream(torch.cuda.current_stream())
         L = self.spec.num_layers
         for h in self.dp.values():
             N.lib.mobile_dp_destroy(h)
         self.dp = {}
-        if self.persistent is not False and self.timer is None:
+        if self.persistent is not False and self.timer is None and not self.gemm_path:
             self._dp_build(gamma, reuse_gates)
         self._sc = {kd: [None] * L for kd in KINDS}
         self.run = {}
@@ -401,6 +443,8 @@ class StepEngine:
                 "offload release")
 
     def run_pass(self, kind: str):
+        # work the caller enqueued on its current stream (state fills) precedes the pass
+        self.stream.wait_stream(torch.cuda.current_stream())
         rec = getattr(self, "record_passes", False)
         if rec:  # metrics.measure_stream: device time + cache accounting of this pass
             e0 = torch.cuda.Event(enable_timing=True)

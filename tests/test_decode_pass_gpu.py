@@ -143,3 +143,61 @@ def test_persistent_batched_and_wide_equal_per_op(cuda_ok, preset, B):
         # the new position's K/V rows went to the same cache slots
         assert torch.allclose(a.sess.kc[:, :, :, ctx], b.sess.kc[:, :, :, ctx], rtol=1e-3, atol=1e-3)
     assert int(engines[0].dp_flags.item()) == 0
+
+
+@pytest.mark.parametrize("preset,B", [("c4", 6), ("c3", 130)])
+def test_large_batch_gemm_path_equals_batch1(cuda_ok, preset, B):
+    """Large-batch decode (B > 4): QKV / O / head on the tcgen05 GEMM (bf16
+    operands) and the experts on the grouped GEMM, vs batch-1 engines on the
+    same sequences (GEMV path, f32 activations).  Tolerance: bf16 rounding of
+    the GEMM activations (2e-2 of the row's largest logit); selections may
+    differ only inside that tolerance; the head's argmax must be a maximiser
+    of the batch-1 logits within it."""
+    from paper_2510_12357_b200.model import DeviceModel
+    from paper_2510_12357_b200.presets import PRESETS
+    from paper_2510_12357_b200.runtime import StepEngine
+    from paper_2510_12357_b200.weights import DeviceWeights
+    spec = replace(PRESETS[preset], num_layers=2)
+    dm = DeviceModel(DeviceWeights.random(spec, torch.device("cuda"), seed=5))
+    ctx = 29
+    big = StepEngine(dm, B, 48).build()
+    assert big.gemm_path and not big.dp
+    one = StepEngine(dm, 1, 48, persistent=False).build()
+    g = torch.Generator(device="cuda").manual_seed(1)
+    big.sess.kc.copy_(torch.randn(big.sess.kc.shape, device="cuda", generator=g))
+    big.sess.vc.copy_(torch.randn(big.sess.vc.shape, device="cuda", generator=g))
+    big.tok.copy_(torch.randint(1, spec.vocab_size, (B,), device="cuda", dtype=torch.int32, generator=g))
+    big.pos.fill_(ctx)
+    kc0, vc0 = big.sess.kc.clone(), big.sess.vc.clone()
+    rows = sorted({0, B // 2, B - 1})
+    tol = 2e-2
+    for kd in ("little", "full"):
+        big.sess.kc.copy_(kc0)
+        big.sess.vc.copy_(vc0)
+        torch.cuda.synchronize()
+        big.run_pass(kd)
+        torch.cuda.synchronize()
+        for s_ in rows:
+            one.sess.kc.copy_(kc0[:, s_:s_ + 1])
+            one.sess.vc.copy_(vc0[:, s_:s_ + 1])
+            one.pos.fill_(ctx)
+            one.tok.copy_(big.tok[s_:s_ + 1])
+            torch.cuda.synchronize()
+            one.run_pass(kd)
+            torch.cuda.synchronize()
+            sa, sb = big.states[kd][:, s_].cpu().numpy(), one.states[kd][:, 0].cpu().numpy()
+            assert np.abs(sa - sb).max() <= tol * np.abs(sb).max(), (kd, s_)
+            ia, ib = big.idx[kd][:, s_].cpu().tolist(), one.idx[kd][:, 0].cpu().tolist()
+            assert selections_agree(ia, ib, sb, tol=tol)[0], (kd, s_, ia, ib)
+            # final LN(x) at bf16 tolerance; the head (GEMM on bf16(LN x) +
+            # row confidence) exactly against torch on the same operand
+            la, lb = big.ln[s_].double(), one.ln[0].double()
+            assert float((la - lb).abs().max()) <= tol * float(lb.abs().max()), (kd, s_)
+            ref = (la.to(torch.bfloat16).double() @ dm.dw.head.double().T) * spec.logit_scale
+            conf = float(torch.softmax(ref, dim=0).max())
+            ca = float(big.head[kd]["conf"][s_])
+            assert abs(ca - conf) <= 1e-3 * conf + 1e-6, (kd, s_, ca, conf)
+            am = int(big.head[kd]["argmax"][s_])
+            assert float(ref.max() - ref[am]) <= 1e-5 * float(ref.abs().max()), (kd, s_)
+            assert bool(big.head[kd]["fallback"][s_]) == (ca <= 0.7)
+            assert torch.allclose(big.sess.kc[:, s_, :, ctx], one.sess.kc[:, 0, :, ctx], rtol=2e-2, atol=2e-2)

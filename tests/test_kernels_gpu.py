@@ -306,3 +306,25 @@ def test_stream_head(dev, wdt, T, d, V):
     out = K.stream_head(torch.tensor(xln, device=dev), w2, 0.5, 24.0, ws=ws)
     assert out["argmax"].tolist() == [0] * T
     assert abs(out["conf"][0].item() - 1.0 / V) < 1e-6
+
+
+@pytest.mark.parametrize("T,V", [(1, 256), (7, 50304), (130, 32000)])
+def test_logits_confidence_vs_torch(cuda_ok, T, V):
+    """Row confidence of raw logits (large-batch head): conf = max softmax(l *
+    scale), first maximiser on exact ties, fallback = conf <= gamma."""
+    from paper_2510_12357_b200 import kernels as K
+    g = torch.Generator(device="cuda").manual_seed(T)
+    logits = torch.randn(T, V, device="cuda", generator=g)
+    logits[0, V // 3] = logits[0, V - 1] = logits[0].max() + 1.0  # exact tie: first index wins
+    scale, gamma = 24.0 / 16, 0.5
+    out = dict(conf=torch.empty(T, device="cuda"), argmax=torch.empty(T, device="cuda", dtype=torch.int32),
+               fallback=torch.empty(T, device="cuda", dtype=torch.uint8))
+    K.logits_confidence(logits, scale, gamma, out)
+    torch.cuda.synchronize()
+    p = torch.softmax(logits.double() * scale, dim=-1)
+    conf = p.max(dim=-1).values
+    assert torch.allclose(out["conf"].double(), conf, rtol=1e-5, atol=1e-7)
+    first = (logits == logits.max(dim=-1, keepdim=True).values).int().argmax(dim=-1)
+    assert (out["argmax"].long().cpu() == first.cpu()).all()
+    assert int(out["argmax"][0]) == V // 3
+    assert (out["fallback"].cpu().bool() == (out["conf"].cpu() <= gamma)).all()
