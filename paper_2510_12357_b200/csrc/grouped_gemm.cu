@@ -7,35 +7,47 @@
 // A is the expert-sorted (permuted) activation matrix (P x K bf16, rows of
 // expert e contiguous at offsets[e]..offsets[e+1]); B_e are the expert's
 // weight rows (out-major, K-major), addressed through a 3-D TMA map
-// (K, N, slot).  One CTA computes one 128 x 128 output tile:
+// (K, N, slot).  Persistent: one CTA per SM walks the 128 x BN output tiles
+// (BN = 256, or 128 for N = 128) in a grid stride:
 //   warp 0      TMA producer: A and B K-blocks of 64 (128 B, SWIZZLE_128B)
-//               into a 4-stage smem ring (full/empty mbarriers)
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//               (4 x K=16 MMAs per stage, tcgen05.commit frees the stage)
-//   warps 2-5   epilogue: tcgen05.ld of the 128 x 128 f32 accumulator
+//               into a smem ring that runs across tiles (full/empty mbarriers)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer into one of
+//               two TMEM accumulators (tile i+1 accumulates while the
+//               epilogue drains tile i), tcgen05.commit frees stages / hands
+//               the accumulator to the epilogue
+//   warps 2-5   epilogue: tcgen05.ld of the 128 x BN f32 accumulator
 //               (warp w reads TMEM lanes 32*(w%4)..), then
 //                 SWIGLU: 16-column groups [8 gate | 8 up] -> silu(g)*u, bf16
 //                 STORE : f32, row scattered to its pair id (combine input)
 //                 ACCUM : f32 out += acc (residual projections: out holds x)
-// Tiles are enumerated on the device from the expert offsets, so no host sync
-// is needed between routing and the GEMM; surplus CTAs exit.
+// Tiles are enumerated on the device from the expert offsets (a per-CTA
+// prefix table in smem), so no host sync is needed between routing and the
+// GEMM.  For decode batches (a few rows per expert) the kernel is a weight
+// stream: every B byte is read once, the ring keeps 128-192 KB in flight/SM.
 #include "common.cuh"
 #include "umma.cuh"
 
 namespace mobile {
 
-constexpr int kGgBM = 128, kGgBN = 128, kGgBK = 64;
-constexpr int kGgStages = 4;
+constexpr int kGgBM = 128, kGgBK = 64;
 constexpr int kGgThreads = 192;
 constexpr int kGgABytes = kGgBM * kGgBK * 2;  // 16 KB
-constexpr int kGgBBytes = kGgBN * kGgBK * 2;  // 16 KB
-constexpr int kGgStageBytes = kGgABytes + kGgBBytes;
+constexpr int kGgMaxActive = 256;
+
+template <int BN>
+struct GgCfg {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kBBytes = BN * kGgBK * 2;
+  static constexpr int kStageBytes = kGgABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+  static constexpr size_t kSmem = (size_t)kStages * kStageBytes + 1024;
+};
 
 enum GgEpi { kGgStoreF32Scatter = 0, kGgSwigluBf16 = 1, kGgStoreBf16 = 2, kGgAccumF32 = 3 };
 
 struct GgArgs {
   CUtensorMap tma_a;       // (K, rows_a)      box (64, 128)
-  CUtensorMap tma_b;       // (K, N, slots)    box (64, 128, 1)
+  CUtensorMap tma_b;       // (K, N, slots)    box (64, BN, 1)
   const int* offsets;      // (E+1) row offsets of A per expert; NULL = dense
   const int* active;       // [n, ids] (NULL = dense)
   const int* slot;         // expert -> B slot (NULL = identity / dense expert index)
@@ -52,54 +64,57 @@ struct GgArgs {
 
 struct GgTile {
   int e, row0, nrows, n0, bslot;
-  bool valid;
+};
+
+// Per-CTA tile table: active expert i owns tiles [base[i], base[i+1]).
+struct GgSched {
+  int total;
+  int na;
+  int e[kGgMaxActive], off[kGgMaxActive], n[kGgMaxActive], base[kGgMaxActive + 1];
 };
 
 // tile id -> (expert, m-tile, n-tile): experts in active order, m-tiles of an
-// expert consecutive, n fastest within an m-tile (consecutive CTAs share A).
-__device__ GgTile gg_tile(const GgArgs& a, int tile) {
-  GgTile t{};
-  const int nt = a.N / kGgBN;
+// expert consecutive, n fastest within an m-tile (concurrent CTAs share A and
+// stream neighbouring B tiles of the same expert).
+template <int BN>
+__device__ __forceinline__ GgTile gg_tile(const GgArgs& a, const GgSched& S, int tile) {
+  GgTile t;
+  const int nt = (a.N + BN - 1) / BN;
   if (!a.offsets) {
     const int mt = (a.dense_rows + kGgBM - 1) / kGgBM;
     const int per = mt * nt;
     const int e = tile / per;
-    if (e >= a.dense_experts) return t;
     const int r = tile - e * per;
     t.e = e;
     t.row0 = (r / nt) * kGgBM;
     t.nrows = min(kGgBM, a.dense_rows - t.row0);
-    t.n0 = (r % nt) * kGgBN;
+    t.n0 = (r % nt) * BN;
     t.bslot = a.slot ? a.slot[e] : e;
-    t.valid = true;
     return t;
   }
-  const int na = a.active[0];
-  int base = 0;
-  for (int i = 0; i < na; ++i) {
-    const int e = a.active[1 + i];
-    const int off = a.offsets[e], n = a.offsets[e + 1] - off;
-    const int mt = (n + kGgBM - 1) / kGgBM;
-    if (tile < base + mt * nt) {
-      const int r = tile - base;
-      t.e = e;
-      t.row0 = off + (r / nt) * kGgBM;
-      t.nrows = min(kGgBM, off + n - t.row0);
-      t.n0 = (r % nt) * kGgBN;
-      t.bslot = a.slot ? a.slot[e] : e;
-      t.valid = true;
-      return t;
-    }
-    base += mt * nt;
+  int lo = 0, hi = S.na - 1;  // largest i with base[i] <= tile (empty experts own no tiles)
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (S.base[mid] <= tile) lo = mid;
+    else hi = mid - 1;
   }
+  const int r = tile - S.base[lo];
+  t.e = S.e[lo];
+  t.row0 = S.off[lo] + (r / nt) * kGgBM;
+  t.nrows = min(kGgBM, S.off[lo] + S.n[lo] - t.row0);
+  t.n0 = (r % nt) * BN;
+  t.bslot = a.slot ? a.slot[t.e] : t.e;
   return t;
 }
 
+template <int BN>
 __global__ void __launch_bounds__(kGgThreads, 1) grouped_gemm_kernel(const __grid_constant__ GgArgs a) {
+  using Cfg = GgCfg<BN>;
+  constexpr int S_ = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t gsm[];
-  __shared__ __align__(8) uint64_t full[kGgStages], empty[kGgStages], done;
+  __shared__ __align__(8) uint64_t full[S_], empty[S_], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
-  __shared__ GgTile tile_s;
+  __shared__ GgSched sched;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // 1024-byte aligned stage buffers (SWIZZLE_128B atoms)
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm) + 1023) & ~uintptr_t(1023));
@@ -107,69 +122,125 @@ __global__ void __launch_bounds__(kGgThreads, 1) grouped_gemm_kernel(const __gri
   if (tid == 0) {
     umma::prefetch_tmap(&a.tma_a);
     umma::prefetch_tmap(&a.tma_b);
-    for (int s = 0; s < kGgStages; ++s) {
+    for (int s = 0; s < S_; ++s) {
       umma::mbar_init(&full[s], 1);
       umma::mbar_init(&empty[s], 1);
     }
-    umma::mbar_init(&done, 1);
+    for (int b = 0; b < 2; ++b) {
+      umma::mbar_init(&tfull[b], 1);
+      umma::mbar_init(&tempty[b], 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) umma::tmem_alloc(&tmem_base, kGgBN);  // 128 f32 columns
+  if (warp == 1) umma::tmem_alloc(&tmem_base, Cfg::kTmemCols);
   pdl_trigger();
   pdl_wait();
-  if (tid == 0) tile_s = gg_tile(a, blockIdx.x);
+  if (warp == 2) {  // tile table (offsets / active come from the routing kernels)
+    const int nt = (a.N + BN - 1) / BN;
+    if (!a.offsets) {
+      if (lane == 0) sched.total = a.dense_experts * ((a.dense_rows + kGgBM - 1) / kGgBM) * nt;
+    } else {
+      const int na = min(a.active[0], kGgMaxActive);
+      int run = 0;
+      for (int i0 = 0; i0 < na; i0 += 32) {
+        const int i = i0 + lane;
+        int cnt = 0;
+        if (i < na) {
+          const int e = a.active[1 + i], off = a.offsets[e], n = a.offsets[e + 1] - off;
+          sched.e[i] = e;
+          sched.off[i] = off;
+          sched.n[i] = n;
+          cnt = ((n + kGgBM - 1) / kGgBM) * nt;
+        }
+        int x = cnt;  // inclusive warp scan
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (i < na) sched.base[i] = run + x - cnt;
+        run += __shfl_sync(0xffffffffu, x, 31);
+      }
+      if (lane == 0) {
+        sched.base[na] = run;
+        sched.total = run;
+        sched.na = na;
+      }
+    }
+  }
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
-  const GgTile T = tile_s;
   const uint32_t tmem = tmem_base;
   const int nk = a.K / kGgBK;
+  const int total = sched.total;
 
-  if (T.valid) {
-    if (warp == 0 && lane == 0) {
-      // ---------------- TMA producer
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kGgStages;
-        if (kb >= kGgStages) umma::mbar_wait(&empty[s], ((kb / kGgStages) - 1) & 1);
-        uint8_t* sa = base + (size_t)s * kGgStageBytes;
-        umma::mbar_expect_tx(&full[s], kGgStageBytes);
-        umma::tma_load_2d(sa, &a.tma_a, kb * kGgBK, T.row0, &full[s]);
-        umma::tma_load_3d(sa + kGgABytes, &a.tma_b, kb * kGgBK, T.n0, T.bslot, &full[s]);
-      }
-    } else if (warp == 1 && lane == 0) {
-      // ---------------- MMA issuer (one thread for the whole CTA)
-      constexpr uint32_t idesc = umma::idesc_bf16_f32(kGgBM, kGgBN);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kGgStages;
-        umma::mbar_wait(&full[s], (kb / kGgStages) & 1);
-        umma::fence_after();
-        const uint8_t* sa = base + (size_t)s * kGgStageBytes;
-        const uint8_t* sb = sa + kGgABytes;
-#pragma unroll
-        for (int k = 0; k < kGgBK / 16; ++k) {
-          // advance the start address by 16 elements (32 B) inside the 128 B swizzle atom
-          umma::mma_bf16(tmem, umma::sdesc_sw128(sa + k * 32), umma::sdesc_sw128(sb + k * 32), idesc,
-                         (kb | k) != 0);
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (ring continues across tiles)
+      uint32_t g = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const GgTile T = gg_tile<BN>(a, sched, tile);
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = (int)(g % S_);
+          if (g >= (uint32_t)S_) umma::mbar_wait(&empty[s], ((g / S_) - 1) & 1);
+          uint8_t* sa = base + (size_t)s * Cfg::kStageBytes;
+          umma::mbar_expect_tx(&full[s], Cfg::kStageBytes);
+          umma::tma_load_2d(sa, &a.tma_a, kb * kGgBK, T.row0, &full[s]);
+          umma::tma_load_3d(sa + kGgABytes, &a.tma_b, kb * kGgBK, T.n0, T.bslot, &full[s]);
         }
-        umma::mma_commit(&empty[s]);  // stage free once these MMAs have read it
       }
-      umma::mma_commit(&done);  // accumulator complete
-    } else if (warp >= 2) {
-      // ---------------- epilogue: TMEM -> registers -> global
-      umma::mbar_wait(&done, 0);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer (one thread for the whole CTA)
+      constexpr uint32_t idesc = umma::idesc_bf16_f32(kGgBM, BN);
+      uint32_t g = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+        const int b = it & 1;
+        if (it >= 2) umma::mbar_wait(&tempty[b], ((it >> 1) - 1) & 1);  // epilogue drained this buffer
+        umma::fence_after();
+        const uint32_t d = tmem + (uint32_t)(b * BN);
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = (int)(g % S_);
+          umma::mbar_wait(&full[s], (g / S_) & 1);
+          umma::fence_after();
+          const uint8_t* sa = base + (size_t)s * Cfg::kStageBytes;
+          const uint8_t* sb = sa + kGgABytes;
+#pragma unroll
+          for (int k = 0; k < kGgBK / 16; ++k) {
+            // advance the start address by 16 elements (32 B) inside the 128 B swizzle atom
+            umma::mma_bf16(d, umma::sdesc_sw128(sa + k * 32), umma::sdesc_sw128(sb + k * 32), idesc,
+                           (kb | k) != 0);
+          }
+          umma::mma_commit(&empty[s]);  // stage free once these MMAs have read it
+        }
+        umma::mma_commit(&tfull[b]);  // accumulator b complete
+      }
+    }
+  } else {
+    // ---------------- epilogue: TMEM -> registers -> global
+    const int q = warp & 3;       // TMEM lane quarter this warp may read
+    const int r = q * 32 + lane;  // tile row = TMEM lane
+    int it = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+      const int b = it & 1;
+      const GgTile T = gg_tile<BN>(a, sched, tile);
+      umma::mbar_wait(&tfull[b], (it >> 1) & 1);
       umma::fence_after();
-      const int q = warp & 3;               // TMEM lane quarter this warp may read
-      const int r = q * 32 + lane;          // tile row = TMEM lane
       const bool live = r < T.nrows;
-      const int row = T.row0 + r;           // row of A (permuted / dense)
+      const int row = T.row0 + r;  // row of A (permuted / dense)
+      const int orow = a.epi == kGgStoreF32Scatter && live && a.row_to_pair ? a.row_to_pair[row] : row;
 #pragma unroll 1
-      for (int c = 0; c < kGgBN / 16; ++c) {
-        float v[16];
-        umma::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 16), v);
-        if (!live) continue;
+      for (int c = 0; c < BN / 16; ++c) {
         const int n = T.n0 + c * 16;
+        if (n >= a.N) break;  // partial last n-tile (N % 128 == 0): warp-uniform
+        float v[16];
+        umma::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + c * 16), v);
+        if (!live) continue;
         if (a.epi == kGgSwigluBf16) {
-          const int f0 = (n / 16) * 8;      // 8 features: cols 0-7 gate, 8-15 up
+          const int f0 = (n / 16) * 8;  // 8 features: cols 0-7 gate, 8-15 up
           __nv_bfloat16* o = a.out_bf16 + (size_t)row * a.ldo + (size_t)T.e * a.out_expert_stride + f0;
           uint4 pk;
           uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
@@ -190,7 +261,6 @@ __global__ void __launch_bounds__(kGgThreads, 1) grouped_gemm_kernel(const __gri
             *reinterpret_cast<float4*>(o + j) = r4;
           }
         } else if (a.epi == kGgStoreF32Scatter) {
-          const int orow = a.row_to_pair ? a.row_to_pair[row] : row;
           float* o = a.out_f32 + (size_t)orow * a.ldo + (size_t)T.e * a.out_expert_stride + n;
 #pragma unroll
           for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
@@ -203,13 +273,16 @@ __global__ void __launch_bounds__(kGgThreads, 1) grouped_gemm_kernel(const __gri
           }
         }
       }
+      umma::fence_before();
+      __syncwarp();
+      if (lane == 0) umma::mbar_arrive(&tempty[b]);  // buffer b may be overwritten
     }
   }
   umma::fence_before();
   __syncthreads();
   if (warp == 1) {
     umma::fence_after();
-    umma::tmem_dealloc(tmem, kGgBN);
+    umma::tmem_dealloc(tmem, Cfg::kTmemCols);
   }
 }
 
@@ -265,7 +338,7 @@ extern "C" int mobile_grouped_gemm(const void* A, int rows_a, int K, const void*
                                    int max_tiles, int dense_rows, int dense_experts, int epi, float* out_f32,
                                    void* out_bf16, int ldo, int out_expert_stride, const int* row_to_pair,
                                    void* stream) {
-  if (K <= 0 || K % kGgBK || N <= 0 || N % kGgBN || rows_a <= 0 || n_slots <= 0) {
+  if (K <= 0 || K % kGgBK || N <= 0 || N % 128 || rows_a <= 0 || n_slots <= 0) {
     set_error("grouped_gemm: K=%d must be a multiple of 64 and N=%d of 128", K, N);
     return MOBILE_ERR_UNSUPPORTED;
   }
@@ -273,6 +346,7 @@ extern "C" int mobile_grouped_gemm(const void* A, int rows_a, int K, const void*
     set_error("grouped_gemm: operands must be 16-byte aligned");
     return MOBILE_ERR_INVALID;
   }
+  const int BN = N % 256 == 0 || N > 256 ? 256 : 128;  // partial last n-tile when N % 256 == 128
   GgArgs a{};
   {
     const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows_a};
@@ -283,7 +357,7 @@ extern "C" int mobile_grouped_gemm(const void* A, int rows_a, int K, const void*
   {
     const cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)N, (cuuint64_t)n_slots};
     const cuuint64_t strides[2] = {(cuuint64_t)K * 2, (cuuint64_t)b_expert_stride};
-    const cuuint32_t box[3] = {kGgBK, kGgBN, 1};
+    const cuuint32_t box[3] = {kGgBK, (cuuint32_t)BN, 1};
     if (int st = make_map(&a.tma_b, B_base, 3, dims, strides, box)) return st;
   }
   a.offsets = offsets;
@@ -300,10 +374,16 @@ extern "C" int mobile_grouped_gemm(const void* A, int rows_a, int K, const void*
   a.ldo = ldo;
   a.out_expert_stride = out_expert_stride;
   if (max_tiles <= 0) return MOBILE_OK;
-  const size_t smem = (size_t)kGgStages * kGgStageBytes + 1024;
-  if (int st = set_smem_once((const void*)grouped_gemm_kernel, smem)) return st;
-  return launch_pdl(grouped_gemm_kernel, dim3(max_tiles), dim3(kGgThreads), smem, (cudaStream_t)stream, 1,
-                    "grouped_gemm", a);
+  // persistent: at most one CTA per SM (max_tiles bounds the 128-wide tiles)
+  const int grid = max(1, min(max_tiles, sm_count()));
+  if (BN == 256) {
+    if (int st = set_smem_once((const void*)grouped_gemm_kernel<256>, GgCfg<256>::kSmem)) return st;
+    return launch_pdl(grouped_gemm_kernel<256>, dim3(grid), dim3(kGgThreads), GgCfg<256>::kSmem,
+                      (cudaStream_t)stream, 1, "grouped_gemm", a);
+  }
+  if (int st = set_smem_once((const void*)grouped_gemm_kernel<128>, GgCfg<128>::kSmem)) return st;
+  return launch_pdl(grouped_gemm_kernel<128>, dim3(grid), dim3(kGgThreads), GgCfg<128>::kSmem, (cudaStream_t)stream,
+                    1, "grouped_gemm", a);
 }
 
 extern "C" int mobile_gather_bf16(const float* src, const int* pairs, int div, int P, int d, void* X, void* stream) {

@@ -13,7 +13,8 @@ dev = torch.device("cuda")
 pk = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
 res = {}
 for name, T, k, E, d, I in (("mixtral_prefill2k", 2048, 2, 8, 4096, 14336), ("qwen_prefill512", 512, 4, 60, 2048, 1408),
-                            ("dseek_batch256", 256, 6, 64, 2048, 1408), ("dense_8k", 8192, 1, 1, 4096, 4096)):
+                            ("dseek_batch256", 256, 6, 64, 2048, 1408), ("dense_8k", 8192, 1, 1, 4096, 4096),
+                            ("dseek_decode64", 64, 3, 64, 2048, 1408), ("mixtral_decode8", 8, 2, 8, 4096, 14336)):
     g = torch.Generator(device=dev).manual_seed(0)
     P = T * k
     rows13 = 2 * I
@@ -47,6 +48,11 @@ for name, T, k, E, d, I in (("mixtral_prefill2k", 2048, 2, 8, 4096, 14336), ("qw
     tf = flops / (ms / 1e3) / 1e12
     res[name] = dict(ms=round(ms, 3), TFLOPs=round(tf, 1), frac_burst=round(tf / pk["bf16_tflops"], 3),
                      frac_sustained=round(tf / pk["bf16_tflops_sustained"], 3), GFLOP=round(flops / 1e9, 1))
+    # weight bytes of the experts that received rows (the decode-batch bound: a weight stream)
+    n_act = int(perm["active"][0].item())
+    wb = n_act * (rows13 * d + d * I) * 2
+    res[name].update(weight_GBs=round(wb / ms / 1e6, 1),
+                     weight_frac_hbm=round(wb / ms / 1e6 / pk["hbm_gbs"], 3))
     del W, X, U, Y
     torch.cuda.empty_cache()
 print(json.dumps(res, indent=1))
