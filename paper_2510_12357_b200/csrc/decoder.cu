@@ -181,6 +181,114 @@ __global__ void attn_decode_kernel(const float* __restrict__ qkv, float* __restr
   }
 }
 
+// The same attention, coalesced and vectorised for head_dim 64 / 128 (the
+// large-batch decode regime, where the KV cache is the dominant HBM stream):
+//  scores  lanes in groups of HD/16, each lane 16 dims (4 x float4) of one
+//          position's K row, group-reduced by shuffles; 32*16/HD positions per
+//          warp iteration, warps interleaved over positions
+//  P.V     lanes in groups of HD/4 (one float4 of the V row each), 128/HD
+//          positions per warp iteration; per-warp partial rows reduced over
+//          warps in a fixed order
+constexpr int kAttnThreads = 256;
+
+template <int HD>
+__global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const float* __restrict__ qkv,
+                                                                       float* __restrict__ kc, float* __restrict__ vc,
+                                                                       const int* __restrict__ pos, int d, int H,
+                                                                       int max_len, float* __restrict__ out) {
+  constexpr int NW = kAttnThreads / 32;
+  constexpr int LS = HD / 16, PS = 32 / LS;  // score lanes per position, positions per warp step
+  constexpr int LV = HD / 4, PV = 32 / LV;   // P.V lanes per position, positions per warp step
+  extern __shared__ __align__(16) float sc[];  // max_len scores
+  __shared__ __align__(16) float qs[HD];
+  __shared__ __align__(16) float part[NW * PV][HD];
+  __shared__ float red[NW];
+  pdl_trigger();
+  pdl_wait();
+  const int b = blockIdx.x / H, hh = blockIdx.x % H;
+  const int p = pos[b];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (p < 0 || p >= max_len) {  // position outside the cache: poison the output, touch nothing
+    for (int e = threadIdx.x; e < HD; e += blockDim.x) out[(size_t)b * d + hh * HD + e] = __int_as_float(0x7fc00000);
+    return;
+  }
+  const float* src = qkv + (size_t)b * 3 * d;
+  const size_t head0 = ((size_t)b * H + hh) * max_len;  // head-major cache (B, H, max_len, HD)
+  for (int e = threadIdx.x; e < HD; e += blockDim.x) {
+    qs[e] = src[hh * HD + e];
+    kc[(head0 + p) * HD + e] = src[d + hh * HD + e];
+    vc[(head0 + p) * HD + e] = src[2 * d + hh * HD + e];
+  }
+  __syncthreads();
+  const float scale = 1.0f / sqrtf((float)HD);
+  // ---- scores
+  const int sg = lane / LS, sl = lane % LS;
+  float qv[16];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float4 q4 = reinterpret_cast<const float4*>(qs + sl * 16)[i];
+    qv[4 * i] = q4.x; qv[4 * i + 1] = q4.y; qv[4 * i + 2] = q4.z; qv[4 * i + 3] = q4.w;
+  }
+  float mx = -INFINITY;
+  for (int j0 = warp * PS; j0 <= p; j0 += NW * PS) {
+    const int j = j0 + sg;
+    float s = 0.f;
+    if (j <= p) {
+      const float4* kr = reinterpret_cast<const float4*>(kc + (head0 + j) * HD + sl * 16);
+      float4 k4[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) k4[i] = __ldcs(kr + i);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        s += qv[4 * i] * k4[i].x + qv[4 * i + 1] * k4[i].y + qv[4 * i + 2] * k4[i].z + qv[4 * i + 3] * k4[i].w;
+    }
+#pragma unroll
+    for (int o = LS / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (j <= p) {
+      s *= scale;
+      if (sl == 0) sc[j] = s;
+      mx = fmaxf(mx, s);
+    }
+  }
+  mx = warp_max(mx);
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) mx = fmaxf(mx, red[i]);
+  __syncthreads();
+  float sum = 0.f;
+  for (int j = threadIdx.x; j <= p; j += blockDim.x) {
+    const float e = expf(sc[j] - mx);
+    sc[j] = e;
+    sum += e;
+  }
+  sum = warp_sum(sum);
+  if (lane == 0) red[warp] = sum;
+  __syncthreads();
+  sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) sum += red[i];
+  // ---- P.V
+  const int vg = lane / LV, vl = lane % LV;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int j = warp * PV + vg; j <= p; j += NW * PV) {
+    const float w = sc[j];
+    const float4 v4 = __ldcs(reinterpret_cast<const float4*>(vc + (head0 + j) * HD) + vl);
+    acc.x = fmaf(w, v4.x, acc.x); acc.y = fmaf(w, v4.y, acc.y);
+    acc.z = fmaf(w, v4.z, acc.z); acc.w = fmaf(w, v4.w, acc.w);
+  }
+  reinterpret_cast<float4*>(part[warp * PV + vg])[vl] = acc;
+  __syncthreads();
+  const float inv = 1.0f / sum;
+  for (int e = threadIdx.x; e < HD; e += blockDim.x) {
+    float o = 0.f;
+#pragma unroll
+    for (int i = 0; i < NW * PV; ++i) o += part[i][e];
+    out[(size_t)b * d + hh * HD + e] = o * inv;
+  }
+}
+
 // x[b] = embed[tok[b]] + pe[pos[b]]  (toymoe.py:172), optionally ln_out = LN(x)
 __global__ void embed_kernel(const int* __restrict__ tok, const int* __restrict__ pos,
                              const float* __restrict__ embed, const float* __restrict__ pe, int d,
@@ -274,6 +382,15 @@ extern "C" int mobile_dense_gemv(const float* x, int T, int d, int do_ln, const 
 extern "C" int mobile_attn_decode(const float* qkv, float* k_cache, float* v_cache, const int* pos, int B, int d,
                                   int H, int max_len, float* out, void* stream) {
   if (B <= 0 || d <= 0 || H <= 0 || d % H || max_len <= 0) { set_error("attn_decode: bad shape"); return MOBILE_ERR_INVALID; }
+  const int hd = d / H;
+  if ((hd == 64 || hd == 128) && (d & 3) == 0) {
+    const size_t vsmem = sizeof(float) * (size_t)max_len;
+    if (vsmem > 160 * 1024) { set_error("attn_decode: max_len=%d too long", max_len); return MOBILE_ERR_UNSUPPORTED; }
+    auto kern = hd == 64 ? attn_decode_vec_kernel<64> : attn_decode_vec_kernel<128>;
+    if (int st = set_smem_once((const void*)kern, vsmem)) return st;
+    return launch_pdl(kern, dim3(B * H), dim3(kAttnThreads), vsmem, (cudaStream_t)stream, 1, "attn_decode", qkv,
+                      k_cache, v_cache, pos, d, H, max_len, out);
+  }
   const size_t smem = sizeof(float) * ((size_t)max_len + d / H);
   if (smem > 200 * 1024) { set_error("attn_decode: max_len=%d too long", max_len); return MOBILE_ERR_UNSUPPORTED; }
   set_smem_once((const void*)attn_decode_kernel, smem);

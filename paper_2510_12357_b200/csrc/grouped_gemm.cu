@@ -24,6 +24,10 @@
 // prefix table in smem), so no host sync is needed between routing and the
 // GEMM.  For decode batches (a few rows per expert) the kernel is a weight
 // stream: every B byte is read once, the ring keeps 128-192 KB in flight/SM.
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
 #include "common.cuh"
 #include "umma.cuh"
 
@@ -60,6 +64,10 @@ struct GgArgs {
   __nv_bfloat16* out_bf16; // SWIGLU / STORE bf16: out[r * ldo + col]
   int ldo;
   int out_expert_stride;   // dense experts: column offset of expert e in the output (elements)
+  int ksplit;              // dense mode split-K: K-block ranges per tile (1 = off)
+  int nkp;                 // K blocks per split
+  float* ws;               // split-K partial tiles (item-major, 128 x BN f32 each)
+  unsigned* tickets;       // split-K arrival counter per tile (reset by the reducer)
 };
 
 struct GgTile {
@@ -107,6 +115,43 @@ __device__ __forceinline__ GgTile gg_tile(const GgArgs& a, const GgSched& S, int
   return t;
 }
 
+// one 16-column chunk of an output row through the epilogue
+__device__ __forceinline__ void gg_store(const GgArgs& a, const GgTile& T, int row, int orow, int n, const float (&v)[16]) {
+  if (a.epi == kGgSwigluBf16) {
+    const int f0 = (n / 16) * 8;  // 8 features: cols 0-7 gate, 8-15 up
+    __nv_bfloat16* o = a.out_bf16 + (size_t)row * a.ldo + (size_t)T.e * a.out_expert_stride + f0;
+    uint4 pk;
+    uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float h0 = silu_f(v[2 * j]) * v[8 + 2 * j];
+      const float h1 = silu_f(v[2 * j + 1]) * v[8 + 2 * j + 1];
+      const __nv_bfloat162 b2 = __floats2bfloat162_rn(h0, h1);
+      pw[j] = *reinterpret_cast<const uint32_t*>(&b2);
+    }
+    *reinterpret_cast<uint4*>(o) = pk;
+  } else if (a.epi == kGgAccumF32) {
+    float* o = a.out_f32 + (size_t)row * a.ldo + (size_t)T.e * a.out_expert_stride + n;
+#pragma unroll
+    for (int j = 0; j < 16; j += 4) {
+      float4 r4 = *reinterpret_cast<const float4*>(o + j);
+      r4.x += v[j]; r4.y += v[j + 1]; r4.z += v[j + 2]; r4.w += v[j + 3];
+      *reinterpret_cast<float4*>(o + j) = r4;
+    }
+  } else if (a.epi == kGgStoreF32Scatter) {
+    float* o = a.out_f32 + (size_t)orow * a.ldo + (size_t)T.e * a.out_expert_stride + n;
+#pragma unroll
+    for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+  } else {
+    __nv_bfloat16* o = a.out_bf16 + (size_t)row * a.ldo + (size_t)T.e * a.out_expert_stride + n;
+#pragma unroll
+    for (int j = 0; j < 16; j += 2) {
+      const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[j], v[j + 1]);
+      *reinterpret_cast<__nv_bfloat162*>(o + j) = b2;
+    }
+  }
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kGgThreads, 1) grouped_gemm_kernel(const __grid_constant__ GgArgs a) {
   using Cfg = GgCfg<BN>;
@@ -115,6 +160,7 @@ __global__ void __launch_bounds__(kGgThreads, 1) grouped_gemm_kernel(const __gri
   __shared__ __align__(8) uint64_t full[S_], empty[S_], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
   __shared__ GgSched sched;
+  __shared__ int red_last;  // split-K: this CTA reduces the tile
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // 1024-byte aligned stage buffers (SWIZZLE_128B atoms)
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm) + 1023) & ~uintptr_t(1023));
@@ -173,15 +219,17 @@ __global__ void __launch_bounds__(kGgThreads, 1) grouped_gemm_kernel(const __gri
   umma::fence_after();
   const uint32_t tmem = tmem_base;
   const int nk = a.K / kGgBK;
-  const int total = sched.total;
+  const int ks = a.ksplit;
+  const int total = sched.total * ks;  // work items: (tile, K split), split fastest
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (ring continues across tiles)
       uint32_t g = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        const GgTile T = gg_tile<BN>(a, sched, tile);
-        for (int kb = 0; kb < nk; ++kb, ++g) {
+      for (int item = blockIdx.x; item < total; item += gridDim.x) {
+        const GgTile T = gg_tile<BN>(a, sched, item / ks);
+        const int kb0 = (item % ks) * a.nkp, kb1 = min(nk, kb0 + a.nkp);
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = (int)(g % S_);
           if (g >= (uint32_t)S_) umma::mbar_wait(&empty[s], ((g / S_) - 1) & 1);
           uint8_t* sa = base + (size_t)s * Cfg::kStageBytes;
@@ -197,12 +245,13 @@ __global__ void __launch_bounds__(kGgThreads, 1) grouped_gemm_kernel(const __gri
       constexpr uint32_t idesc = umma::idesc_bf16_f32(kGgBM, BN);
       uint32_t g = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+      for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
         const int b = it & 1;
         if (it >= 2) umma::mbar_wait(&tempty[b], ((it >> 1) - 1) & 1);  // epilogue drained this buffer
         umma::fence_after();
         const uint32_t d = tmem + (uint32_t)(b * BN);
-        for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int kb0 = (item % ks) * a.nkp, kb1 = min(nk, kb0 + a.nkp);
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const int s = (int)(g % S_);
           umma::mbar_wait(&full[s], (g / S_) & 1);
           umma::fence_after();
@@ -212,7 +261,7 @@ __global__ void __launch_bounds__(kGgThreads, 1) grouped_gemm_kernel(const __gri
           for (int k = 0; k < kGgBK / 16; ++k) {
             // advance the start address by 16 elements (32 B) inside the 128 B swizzle atom
             umma::mma_bf16(d, umma::sdesc_sw128(sa + k * 32), umma::sdesc_sw128(sb + k * 32), idesc,
-                           (kb | k) != 0);
+                           (kb != kb0) || k != 0);
           }
           umma::mma_commit(&empty[s]);  // stage free once these MMAs have read it
         }
@@ -224,14 +273,16 @@ __global__ void __launch_bounds__(kGgThreads, 1) grouped_gemm_kernel(const __gri
     const int q = warp & 3;       // TMEM lane quarter this warp may read
     const int r = q * 32 + lane;  // tile row = TMEM lane
     int it = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+    for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
       const int b = it & 1;
+      const int tile = item / ks;
       const GgTile T = gg_tile<BN>(a, sched, tile);
       umma::mbar_wait(&tfull[b], (it >> 1) & 1);
       umma::fence_after();
       const bool live = r < T.nrows;
       const int row = T.row0 + r;  // row of A (permuted / dense)
       const int orow = a.epi == kGgStoreF32Scatter && live && a.row_to_pair ? a.row_to_pair[row] : row;
+      float* wp = ks > 1 ? a.ws + (size_t)item * kGgBM * BN + (size_t)r * BN : nullptr;
 #pragma unroll 1
       for (int c = 0; c < BN / 16; ++c) {
         const int n = T.n0 + c * 16;
@@ -239,43 +290,46 @@ __global__ void __launch_bounds__(kGgThreads, 1) grouped_gemm_kernel(const __gri
         float v[16];
         umma::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + c * 16), v);
         if (!live) continue;
-        if (a.epi == kGgSwigluBf16) {
-          const int f0 = (n / 16) * 8;  // 8 features: cols 0-7 gate, 8-15 up
-          __nv_bfloat16* o = a.out_bf16 + (size_t)row * a.ldo + (size_t)T.e * a.out_expert_stride + f0;
-          uint4 pk;
-          uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+        if (wp) {  // split-K partial
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float h0 = silu_f(v[2 * j]) * v[8 + 2 * j];
-            const float h1 = silu_f(v[2 * j + 1]) * v[8 + 2 * j + 1];
-            const __nv_bfloat162 b2 = __floats2bfloat162_rn(h0, h1);
-            pw[j] = *reinterpret_cast<const uint32_t*>(&b2);
-          }
-          *reinterpret_cast<uint4*>(o) = pk;
-        } else if (a.epi == kGgAccumF32) {
-          float* o = a.out_f32 + (size_t)row * a.ldo + (size_t)T.e * a.out_expert_stride + n;
-#pragma unroll
-          for (int j = 0; j < 16; j += 4) {
-            float4 r4 = *reinterpret_cast<const float4*>(o + j);
-            r4.x += v[j]; r4.y += v[j + 1]; r4.z += v[j + 2]; r4.w += v[j + 3];
-            *reinterpret_cast<float4*>(o + j) = r4;
-          }
-        } else if (a.epi == kGgStoreF32Scatter) {
-          float* o = a.out_f32 + (size_t)orow * a.ldo + (size_t)T.e * a.out_expert_stride + n;
-#pragma unroll
-          for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          for (int j = 0; j < 16; j += 4)
+            __stcg(reinterpret_cast<float4*>(wp + c * 16 + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
         } else {
-          __nv_bfloat16* o = a.out_bf16 + (size_t)row * a.ldo + (size_t)T.e * a.out_expert_stride + n;
-#pragma unroll
-          for (int j = 0; j < 16; j += 2) {
-            const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[j], v[j + 1]);
-            *reinterpret_cast<__nv_bfloat162*>(o + j) = b2;
-          }
+          gg_store(a, T, row, orow, n, v);
         }
       }
       umma::fence_before();
       __syncwarp();
       if (lane == 0) umma::mbar_arrive(&tempty[b]);  // buffer b may be overwritten
+      if (ks > 1) {
+        // the last of the tile's ks items sums the partials in split order
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 2 && lane == 0) red_last = atomicAdd(a.tickets + tile, 1u) == (unsigned)(ks - 1);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (red_last) {
+          __threadfence();
+          const float* w0 = a.ws + (size_t)tile * ks * kGgBM * BN + (size_t)r * BN;
+#pragma unroll 1
+          for (int c = 0; c < BN / 16 && live; ++c) {
+            const int n = T.n0 + c * 16;
+            if (n >= a.N) break;
+            float v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = 0.f;
+            for (int sp = 0; sp < ks; ++sp) {
+              const float4* src = reinterpret_cast<const float4*>(w0 + (size_t)sp * kGgBM * BN + c * 16);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float4 f = __ldcg(src + j);
+                v[4 * j] += f.x; v[4 * j + 1] += f.y; v[4 * j + 2] += f.z; v[4 * j + 3] += f.w;
+              }
+            }
+            gg_store(a, T, row, orow, n, v);
+          }
+          if (warp == 2 && lane == 0) a.tickets[tile] = 0u;  // reusable by the next launch
+        }
+      }
     }
   }
   umma::fence_before();
@@ -329,6 +383,38 @@ static int make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t
   return MOBILE_OK;
 }
 
+// split-K workspace: nsm partial tiles of 128 x 256 f32 + one ticket per tile
+static float* g_split_ws = nullptr;
+static unsigned* g_split_tickets = nullptr;
+
+static bool split_k_disabled() {  // opt-in (MOBILE_GG_SPLITK=1): the one-CTA reduction is L2-latency bound
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("MOBILE_GG_SPLITK");
+    v = (e && std::strcmp(e, "1") == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
+
+static bool ensure_split_ws(int nsm, cudaStream_t stream) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (g_split_ws) return true;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
+  void* w = nullptr;
+  void* t = nullptr;
+  if (cudaMalloc(&w, (size_t)nsm * kGgBM * 256 * sizeof(float)) != cudaSuccess) return false;
+  if (cudaMalloc(&t, (size_t)nsm * sizeof(unsigned)) != cudaSuccess || cudaMemset(t, 0, (size_t)nsm * sizeof(unsigned)) != cudaSuccess) {
+    cudaFree(w);
+    return false;
+  }
+  cudaDeviceSynchronize();
+  g_split_ws = (float*)w;
+  g_split_tickets = (unsigned*)t;
+  return true;
+}
+
 }  // namespace mobile
 
 using namespace mobile;
@@ -346,7 +432,13 @@ extern "C" int mobile_grouped_gemm(const void* A, int rows_a, int K, const void*
     set_error("grouped_gemm: operands must be 16-byte aligned");
     return MOBILE_ERR_INVALID;
   }
-  const int BN = N % 256 == 0 || N > 256 ? 256 : 128;  // partial last n-tile when N % 256 == 128
+  // 128 x 256 tiles (partial last n-tile when N % 256 == 128); dense GEMMs with
+  // few tiles (decode-batch projections) take 128 x 128 tiles: twice the CTAs
+  // streaming B, 6 stages in flight each
+  int BN = N % 256 == 0 || N > 256 ? 256 : 128;
+  if (!offsets && BN == 256 &&
+      dense_experts * ((dense_rows + kGgBM - 1) / kGgBM) * ((N + 255) / 256) < sm_count())
+    BN = 128;
   GgArgs a{};
   {
     const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows_a};
@@ -374,8 +466,33 @@ extern "C" int mobile_grouped_gemm(const void* A, int rows_a, int K, const void*
   a.ldo = ldo;
   a.out_expert_stride = out_expert_stride;
   if (max_tiles <= 0) return MOBILE_OK;
+  const int nsm = sm_count();
+  // Dense mode with fewer tiles than SMs (the decode-batch projections: 8-24
+  // tiles of a weight stream): split K so every SM streams B.  Deterministic:
+  // partials land in a library workspace, the tile's last CTA sums them in
+  // split order.  The workspace is allocated once (never during a capture;
+  // captured graphs keep using it), so launches sharing it must be stream-
+  // ordered -- one GEMM at a time per process, as the engines issue them.
+  a.ksplit = 1;
+  a.nkp = K / kGgBK;
+  if (!offsets && !split_k_disabled()) {
+    const int nk = K / kGgBK;
+    const int tiles = dense_experts * ((dense_rows + kGgBM - 1) / kGgBM) * ((N + BN - 1) / BN);
+    int ks = min(nsm / max(tiles, 1), nk / 4);
+    if (ks >= 2) {
+      const int nkp = (nk + ks - 1) / ks;
+      ks = (nk + nkp - 1) / nkp;
+      if (ensure_split_ws(nsm, (cudaStream_t)stream)) {
+        a.ksplit = ks;
+        a.nkp = nkp;
+        a.ws = g_split_ws;
+        a.tickets = g_split_tickets;
+        max_tiles = tiles * ks;
+      }
+    }
+  }
   // persistent: at most one CTA per SM (max_tiles bounds the 128-wide tiles)
-  const int grid = max(1, min(max_tiles, sm_count()));
+  const int grid = max(1, min(max_tiles, nsm));
   if (BN == 256) {
     if (int st = set_smem_once((const void*)grouped_gemm_kernel<256>, GgCfg<256>::kSmem)) return st;
     return launch_pdl(grouped_gemm_kernel<256>, dim3(grid), dim3(kGgThreads), GgCfg<256>::kSmem,

@@ -342,8 +342,8 @@ __global__ void __launch_bounds__(kRouterThreads) router_kernel(RouterArgs a) {
 template <typename W, int TT>
 static int launch_router(const RouterArgs& a, cudaStream_t stream) {
   const int Etot = a.E + a.n_extra;
-  int cs = 1;
-  if (a.T <= 8) cs = min(8, max(1, (Etot + 7) / 8));
+  // a cluster of up to 8 CTAs splits the router rows of each token tile
+  const int cs = min(8, max(1, (Etot + 7) / 8));
   const size_t smem = sizeof(float) * ((size_t)TT * a.d + (size_t)TT * Etot + 64);
   auto kern = router_kernel<W, TT>;
   if (int st = set_smem_once((const void*)kern, smem)) return st;

@@ -35,6 +35,29 @@ def test_dense_gemm(dev, M, N, K, S):
         assert rel_err(got.cpu().numpy(), want.cpu().numpy()) < 1e-3, e
 
 
+@pytest.mark.parametrize("M,N,K", [(64, 2048, 2048), (8, 6144, 2048), (256, 2048, 4096), (5, 384, 1024)])
+def test_dense_split_k_accumulate(dev, M, N, K):
+    """Decode-batch projections (few tiles, long K): the split-K path, with
+    the residual-accumulate epilogue; reruns are bit-identical (partials are
+    summed in split order by the tile's last CTA)."""
+    from paper_2510_12357_b200 import kernels as K_
+    g = torch.Generator(device=dev).manual_seed(M * 7 + N)
+    A = torch.randn(M, K, device=dev, generator=g).to(torch.bfloat16)
+    B = torch.randn(N, K, device=dev, generator=g).to(torch.bfloat16)
+    resid = torch.randn(M, N, device=dev, generator=g)
+    tiles = ((M + 127) // 128) * (N // 128)
+    outs = []
+    for _ in range(3):
+        out = resid.clone()
+        K_.grouped_gemm(A, K, B.data_ptr(), N * K * 2, 1, N, max_tiles=tiles, dense_rows=M, dense_experts=1,
+                        epi=K_.GG_ACCUM_F32, out_f32=out, ldo=N)
+        outs.append(out)
+    torch.cuda.synchronize()
+    want = resid + A.float() @ B.float().T
+    assert rel_err(outs[0].cpu().numpy(), want.cpu().numpy()) < 1e-3
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+
+
 @pytest.mark.parametrize("T,k,E,d,I", [(64, 2, 8, 128, 64), (300, 4, 12, 256, 128), (2048, 2, 8, 512, 256),
                                        (513, 4, 60, 2048, 1408)])
 def test_grouped_expert_ffn(dev, T, k, E, d, I):
