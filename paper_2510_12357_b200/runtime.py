@@ -36,16 +36,21 @@ from .policy import plan_from_targets
 
 KINDS = ("little", "big", "full")
 GEMV_MAX_BATCH = 4  # largest batch on the GEMV decode path (stream GEMV / persistent pass tile)
+GEMM_MIN_BATCH = 3  # resident bf16 decode switches to the GEMM path from here (profiles/r1_configs.json)
 MAX_BATCH = 1024
 
 
 class StepEngine:
     def __init__(self, dm: DeviceModel, batch: int, max_len: int, runtime=None, graphs: bool = True,
-                 persistent: bool | None = None, zero_sync: bool | None = None):
+                 persistent: bool | None = None, zero_sync: bool | None = None, gemm: bool | None = None):
         s = dm.spec
-        # B <= 8: the GEMV decode path (bulk-copy streaming / persistent pass);
-        # larger batches run the projections and the head as tcgen05 GEMMs
-        self.gemm_path = batch > GEMV_MAX_BATCH
+        # small batches: the GEMV decode path (persistent pass / bulk-copy
+        # streaming); larger ones run projections, experts and head as tcgen05
+        # GEMMs (default from GEMM_MIN_BATCH when the shapes allow it)
+        if gemm is None:
+            gemm = batch > GEMV_MAX_BATCH or (batch >= GEMM_MIN_BATCH and runtime is None and dm.moe.tc_ok
+                                              and persistent is not True)
+        self.gemm_path = bool(gemm)
         if self.gemm_path:
             if not dm.moe.tc_ok:
                 raise ValueError(f"StepEngine: batch {batch} > {GEMV_MAX_BATCH} needs the tcgen05 GEMM path "

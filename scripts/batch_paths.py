@@ -1,0 +1,43 @@
+"""Decode pass time per batch on the persistent GEMV kernel vs the GEMM path
+(chooses GEMM_MIN_BATCH).  python scripts/batch_paths.py [preset] [B...]"""
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2510_12357_b200.model import DeviceModel  # noqa: E402
+from paper_2510_12357_b200.presets import PRESETS  # noqa: E402
+from paper_2510_12357_b200.runtime import StepEngine  # noqa: E402
+from paper_2510_12357_b200.weights import DeviceWeights  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c4"
+batches = [int(b) for b in sys.argv[2:]] or [1, 2, 3, 4]
+spec = PRESETS[name]
+dm = DeviceModel(DeviceWeights.random(spec, torch.device("cuda"), seed=0))
+out = {}
+for B in batches:
+    for gemm in (False, True):
+        eng = StepEngine(dm, B, 560, gemm=gemm).build()
+        eng.sess.kc.normal_()
+        eng.sess.vc.normal_()
+        eng.pos.fill_(512)
+        torch.cuda.synchronize()
+        res = {}
+        for kd in ("little", "full"):
+            eng.graphs[kd].replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(eng.stream):
+                e0.record()
+                for _ in range(10):
+                    eng.graphs[kd].replay()
+                e1.record()
+            torch.cuda.synchronize()
+            res[kd] = round(e0.elapsed_time(e1) / 10, 3)
+        out[f"B{B}_{'gemm' if gemm else 'gemv'}"] = res
+        print(B, "gemm" if gemm else "gemv", res, flush=True)
+        del eng
+        torch.cuda.empty_cache()
+print(json.dumps(out))

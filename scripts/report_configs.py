@@ -22,7 +22,7 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 from paper_2510_12357_b200.model import DeviceModel  # noqa: E402
 from paper_2510_12357_b200.presets import NAMES, PRESETS  # noqa: E402
-from paper_2510_12357_b200.runtime import GEMV_MAX_BATCH, StepEngine  # noqa: E402
+from paper_2510_12357_b200.runtime import StepEngine  # noqa: E402
 from paper_2510_12357_b200.weights import DeviceWeights  # noqa: E402
 
 PK = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -62,8 +62,8 @@ for name in sys.argv[1:] or ["c2", "c3", "c4", "c5"]:
     res = {"model": NAMES[name], "init_s": round(time.time() - t0, 1), "decode": {}}
     ctx = PROMPT[name]
 
-    def engine(B):
-        e = StepEngine(dm, B, ctx + 48, persistent=True if B <= GEMV_MAX_BATCH else None).build()
+    def engine(B, gemm=None):
+        e = StepEngine(dm, B, ctx + 48, gemm=gemm).build()
         # B sequences at a common position: fill the caches with random K/V rows
         e.sess.kc.normal_()
         e.sess.vc.normal_()
