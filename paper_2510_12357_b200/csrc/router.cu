@@ -351,6 +351,15 @@ static int launch_router(const RouterArgs& a, cudaStream_t stream) {
                     "router launch", a);
 }
 
+template <typename W>
+static int launch_router_tt(const RouterArgs& a, int TT, cudaStream_t s) {
+  switch (TT) {
+    case 1: return launch_router<W, 1>(a, s);
+    case 2: return launch_router<W, 2>(a, s);
+    default: return launch_router<W, 4>(a, s);
+  }
+}
+
 // ---------------------------------------------------------------- topk rows
 // One warp per row; keys staged in shared memory; f32 or f64 input.
 template <typename F>
@@ -416,31 +425,21 @@ extern "C" int mobile_router_topk(const float* x, float* h2_out, const void* w_r
   if (k_max > E) { set_error("k (%d) exceeds number of experts (%d)", k_max, E); return MOBILE_ERR_K_EXCEEDS; }
   if (T == 0) return MOBILE_OK;
   if (d % 4 != 0 || (w_dtype == MOBILE_BF16 && d % 8 != 0)) { set_error("router: d=%d must be a multiple of 8", d); return MOBILE_ERR_UNSUPPORTED; }
+  // tokens per cluster: the kernel is latency-bound, so many small tiles beat
+  // fewer large ones (measured: 8/16-token tiles slow both batch-64 decode
+  // and 512-token prefill)
   const int TT = T == 1 ? 1 : (T == 2 ? 2 : 4);
   const bool fuse = perm_offsets && perm_pairs && perm_active && T <= TT && T * k_max <= 32;
   RouterArgs a{x, h2_out, w_router, T, d, E, n_extra, k_max, k_tok, replay, replay_mask, reuse_gates,
                gate_norm, logits_out, extra_out, idx_out, gates_out, flags,
                fuse ? perm_offsets : nullptr, fuse ? perm_pairs : nullptr, fuse ? perm_active : nullptr};
   cudaStream_t s = (cudaStream_t)stream;
-  if (perm_offsets && !fuse) {
-    int st = MOBILE_OK;
-    if (w_dtype == MOBILE_BF16) st = TT == 4 ? launch_router<__nv_bfloat16, 4>(a, s) : TT == 2 ? launch_router<__nv_bfloat16, 2>(a, s) : launch_router<__nv_bfloat16, 1>(a, s);
-    else if (w_dtype == MOBILE_F32) st = TT == 4 ? launch_router<float, 4>(a, s) : TT == 2 ? launch_router<float, 2>(a, s) : launch_router<float, 1>(a, s);
-    else { set_error("router: unsupported weight dtype %d", w_dtype); return MOBILE_ERR_UNSUPPORTED; }
-    if (st) return st;
-    return mobile_permute(idx_out, k_tok, T, k_max, E, perm_offsets, perm_pairs, perm_active, stream);
-  }
-  if (w_dtype == MOBILE_BF16) {
-    if (TT == 1) return launch_router<__nv_bfloat16, 1>(a, s);
-    if (TT == 2) return launch_router<__nv_bfloat16, 2>(a, s);
-    return launch_router<__nv_bfloat16, 4>(a, s);
-  } else if (w_dtype == MOBILE_F32) {
-    if (TT == 1) return launch_router<float, 1>(a, s);
-    if (TT == 2) return launch_router<float, 2>(a, s);
-    return launch_router<float, 4>(a, s);
-  }
-  set_error("router: unsupported weight dtype %d", w_dtype);
-  return MOBILE_ERR_UNSUPPORTED;
+  int st;
+  if (w_dtype == MOBILE_BF16) st = launch_router_tt<__nv_bfloat16>(a, TT, s);
+  else if (w_dtype == MOBILE_F32) st = launch_router_tt<float>(a, TT, s);
+  else { set_error("router: unsupported weight dtype %d", w_dtype); return MOBILE_ERR_UNSUPPORTED; }
+  if (st || !perm_offsets || fuse) return st;
+  return mobile_permute(idx_out, k_tok, T, k_max, E, perm_offsets, perm_pairs, perm_active, stream);
 }
 
 extern "C" int mobile_topk_rows(const void* rows, int dtype, int R, int E, int k, int* idx_out,
