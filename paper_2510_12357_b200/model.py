@@ -441,10 +441,19 @@ class DecodeSession:
             self.vc[layer, rows, :, pos:pos + n] = vn
             kh, vh = self.kc[layer, rows, :, :pos + n], self.vc[layer, rows, :, :pos + n]
         qh = q.view(Bn, n, H, hd).transpose(1, 2)
-        scores = (qh @ kh.transpose(-1, -2)) / math.sqrt(hd)
         if n > 1:
-            mask = torch.ones(n, pos + n, dtype=torch.bool, device=x.device).triu(1 + pos)
-            scores = scores.masked_fill(mask, float("-inf"))
+            # prompt chunk: fused attention (torch SDPA: flash on bf16 operands
+            # for bf16 models -- f32 accumulate, the weights' precision already
+            # bounds the error -- memory-efficient f32 otherwise), causal with
+            # the chunk's offset into the cache
+            dt = torch.bfloat16 if dw.wdtype == torch.bfloat16 else torch.float32
+            mask = None if pos == 0 else \
+                torch.ones(n, pos + n, dtype=torch.bool, device=x.device).tril(pos)
+            out = Fn.scaled_dot_product_attention(qh.to(dt), kh.to(dt), vh.to(dt), attn_mask=mask,
+                                                  is_causal=pos == 0)
+            out = out.float().transpose(1, 2).reshape(Bn * n, d)
+            return x + m._lin(out, dw.o[layer])
+        scores = (qh @ kh.transpose(-1, -2)) / math.sqrt(hd)
         attn = torch.softmax(scores, dim=-1)
         out = (attn @ vh).transpose(1, 2).reshape(Bn * n, d)
         return x + m._lin(out, dw.o[layer])
