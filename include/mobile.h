@@ -263,6 +263,39 @@ int mobile_advance(int* pos, int B, int* tok, const int* next_tok, void* stream)
  * pinned slot tables and routing lists). */
 int mobile_memcpy_async(void* dst, const void* src, size_t bytes, void* stream);
 
+/* ---- expert parallelism over peer memory (ep_p2p.cu) ---------------------
+ * Replaces the dispatch / combine all-to-alls of the expert-parallel layer
+ * (ep.py) with direct peer stores on an NVSwitch node.  Every
+ * rank owns a mailbox (mobile_ep_mailbox_create) whose CUDA IPC handle is
+ * exchanged once (mobile_ep_ipc_handle / _open); peers_dev is a device array
+ * of the G mailboxes as mapped in this process (this rank's own at [rank]).
+ * Per layer, with an epoch the caller increments per exchange:
+ *   home : mobile_ep_dispatch  -- plan (stable per-owner positions, dest_pos
+ *          (T*k_max) scratch, counts (G) scratch), row stores into the
+ *          owners' mailboxes, counts + release flag (system scope)
+ *   owner: mobile_ep_wait(which=0) -- acquire every source's flag, write
+ *          k_tok_out (G*cap) = 1 for the received rows; run the experts on
+ *          the mailbox rows; mobile_ep_return -- output rows back + flag
+ *   home : mobile_ep_wait(which=1); mobile_ep_collect -- Y (T*k_max, d) in
+ *          pair order (zero rows for unselected slots), then the combine.
+ * cap = rows a source may send one owner (T_max * k_max covers the worst case;
+ * overflow sets flags bit 0).  A wait that does not see its flags in 10 s
+ * traps (flags bit 1).  G <= 8. */
+size_t mobile_ep_mailbox_bytes(int G, int cap, int d);
+int mobile_ep_mailbox_create(int G, int cap, int d, void** mailbox);
+int mobile_ep_mailbox_destroy(void* mailbox);
+int mobile_ep_ipc_handle(void* mailbox, void* handle64);
+int mobile_ep_ipc_open(const void* handle64, void** ptr);
+int mobile_ep_ipc_close(void* ptr);
+int mobile_ep_dispatch(const float* rows, const int* idx, const int* k_tok, int T, int k_max, int d, const int* owner,
+                       const int* local_id, void* const* peers_dev, int G, int rank, int cap, unsigned epoch,
+                       int* dest_pos, int* counts, int* flags, void* stream);
+int mobile_ep_wait(void* mailbox, int G, int cap, int d, int which, unsigned epoch, int* k_tok_out, int* flags,
+                   void* stream);
+int mobile_ep_return(const float* out_rows, const void* mailbox, void* const* peers_dev, int G, int rank, int cap,
+                     int d, unsigned epoch, void* stream);
+int mobile_ep_collect(const void* mailbox, const int* dest_pos, int P, int G, int cap, int d, float* Y, void* stream);
+
 /* ---- expert cache core (memory.py:65-181 semantics) ----------------------
  * LRU of (layer, expert) keys with pins, in-flight protection, speculative
  * deferral, CapacityDeadlock.  Each resident entry owns a physical slot

@@ -21,6 +21,13 @@ so the layer output is bit-identical for G = 1, 2, 4, 8.
 The exchange is written against torch.distributed (NCCL over NVLink on the
 B200 box, gloo in the CPU tests); the expert compute is a callable so the
 host-side exchange logic can be tested on CPU with the oracle as the expert.
+
+`P2PExchange` / `P2PExpertParallelMoE` are the B200-native variant: the same
+semantics over peer memory (csrc/ep_p2p.cu) -- the home rank's kernels store
+pair rows straight into the owners' mailboxes (CUDA IPC-mapped, NVLink P2P on
+an NVSwitch node) and the owners store outputs straight back, with
+release/acquire flags at system scope instead of collectives: no host sync and
+no counts all-to-all per layer.
 """
 
 from __future__ import annotations
@@ -156,3 +163,130 @@ class ExpertParallelMoE:
         if R == 0:
             return torch.zeros(0, rows.shape[1], dtype=torch.float32, device=rows.device)
         return self.local.rows_ffn(layer, rows.float().contiguous(), ids.int().contiguous())
+
+
+# ----------------------------------------------------------------------------- peer-memory exchange
+class _DevView:
+    """A torch view of raw device memory (the IPC-mapped mailbox)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+class P2PExchange:
+    """Dispatch / combine over peer memory (ep_p2p.cu; include/mobile.h).
+
+    cap = rows one source may send one owner per exchange (T_max * k_max is
+    the worst case).  Collective setup (mailbox handles all-gathered once);
+    each exchange is kernels only, stream-ordered on the current stream."""
+
+    def __init__(self, E: int, d: int, cap: int, group=None, device=None):
+        import ctypes as C
+
+        from . import _native as N
+        self.N = N
+        self.group = group
+        self.G = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.E, self.d, self.cap = E, d, cap
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.dev = dev
+        box = C.c_void_p()
+        N.check(N.lib.mobile_ep_mailbox_create(self.G, cap, d, C.byref(box)), "ep mailbox")
+        self.box = box.value
+        handle = (C.c_ubyte * 64)()
+        N.check(N.lib.mobile_ep_ipc_handle(C.c_void_p(self.box), handle), "ep ipc handle")
+        handles = [bytes(handle)]
+        if self.G > 1:
+            handles = [None] * self.G
+            dist.all_gather_object(handles, bytes(handle), group=group)
+        self.opened = []
+        ptrs = []
+        for g in range(self.G):
+            if g == self.rank:
+                ptrs.append(self.box)
+                continue
+            p = C.c_void_p()
+            hb = (C.c_ubyte * 64).from_buffer_copy(handles[g])
+            N.check(N.lib.mobile_ep_ipc_open(hb, C.byref(p)), "ep ipc open")
+            ptrs.append(p.value)
+            self.opened.append(p.value)
+        self.peers = torch.tensor(ptrs, dtype=torch.int64, device=dev)
+        own, loc = owner_table(E, self.G, dev)
+        self.owner, self.local_id = own.int().contiguous(), loc.int().contiguous()
+        self.counts = torch.zeros(self.G, dtype=torch.int32, device=dev)
+        self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.k_in = torch.zeros(self.G * cap, dtype=torch.int32, device=dev)
+        self.epoch = 0
+        # views of this rank's mailbox (layout of ep_p2p.cu Box)
+        rows_b = (self.G * cap * d * 4 + 255) // 256 * 256
+        ids_b = (self.G * cap * 4 + 255) // 256 * 256
+        self.in_rows = torch.as_tensor(_DevView(self.box, (self.G * cap, d), "<f4"), device=dev)
+        self.in_ids = torch.as_tensor(_DevView(self.box + rows_b, (self.G * cap,), "<i4"), device=dev)
+        del ids_b
+
+    def _s(self):
+        return torch.cuda.current_stream().cuda_stream
+
+    def exchange(self, h2: torch.Tensor, idx: torch.Tensor, k_tok: torch.Tensor, expert_fn) -> torch.Tensor:
+        """h2 (T, d) rows of this rank's tokens, idx (T, k_max) selections ->
+        Y (T*k_max, d) expert outputs in pair order; expert_fn(rows, ids,
+        k_tok) runs this rank's experts on its mailbox rows."""
+        N, P_ = self.N, self.N.ptr
+        T, k_max = idx.shape
+        if T * k_max > self.cap:
+            raise ValueError(f"P2PExchange: {T * k_max} pairs exceed the mailbox capacity {self.cap}")
+        self.epoch += 1
+        ep = self.epoch
+        dest = torch.empty(T * k_max, dtype=torch.int32, device=self.dev)
+        N.check(N.lib.mobile_ep_dispatch(P_(h2), P_(idx), P_(k_tok), T, k_max, self.d, P_(self.owner),
+                                         P_(self.local_id), P_(self.peers), self.G, self.rank, self.cap, ep, P_(dest),
+                                         P_(self.counts), P_(self.flags), self._s()), "ep dispatch")
+        N.check(N.lib.mobile_ep_wait(self.box, self.G, self.cap, self.d, 0, ep, P_(self.k_in), P_(self.flags),
+                                     self._s()), "ep wait (in)")
+        out = expert_fn(self.in_rows, self.in_ids, self.k_in)
+        N.check(N.lib.mobile_ep_return(P_(out), self.box, P_(self.peers), self.G, self.rank, self.cap, self.d, ep,
+                                       self._s()), "ep return")
+        N.check(N.lib.mobile_ep_wait(self.box, self.G, self.cap, self.d, 1, ep, None, P_(self.flags), self._s()),
+                "ep wait (back)")
+        Y = torch.empty(T * k_max, self.d, dtype=torch.float32, device=self.dev)
+        N.check(N.lib.mobile_ep_collect(self.box, P_(dest), T * k_max, self.G, self.cap, self.d, P_(Y), self._s()),
+                "ep collect")
+        return Y
+
+    def close(self):
+        if getattr(self, "box", None) is None:
+            return
+        torch.cuda.synchronize()
+        for p in self.opened:
+            self.N.lib.mobile_ep_ipc_close(p)
+        self.opened = []
+        if self.G > 1:
+            dist.barrier(group=self.group)  # every peer unmapped this mailbox
+        self.N.lib.mobile_ep_mailbox_destroy(self.box)
+        self.box = None
+
+
+class P2PExpertParallelMoE(ExpertParallelMoE):
+    """ExpertParallelMoE with the peer-memory exchange (same decisions, gates
+    and combine on the home rank; the owner runs its experts on its mailbox)."""
+
+    def __init__(self, moe_full_router, local_moe, E: int, d: int, cap: int, group=None):
+        self.router_moe = moe_full_router
+        self.local = local_moe
+        self.x = P2PExchange(E, d, cap, group)
+
+    def forward(self, x, layer, k_tok, k_max, replay=None, replay_mask=None, reuse_gates=False, ln_out=None):
+        from . import kernels as K
+        rm = self.router_moe
+        sc = rm.route(x, layer, k_tok, k_max, replay=replay, replay_mask=replay_mask, reuse_gates=reuse_gates)
+        r = sc["router"]
+
+        def experts(rows, ids, k_in):
+            return self.local.rows_ffn(layer, rows, ids, k_in, clone=False)
+
+        Y = self.x.exchange(r["h2"], r["idx"], k_tok, experts)
+        Ys = rm.shared_rows(layer, r["h2"], sc) if rm.S else None
+        shared_logits = r["extra"] if rm.dw.n_gate_rows else None
+        return K.combine(x, Y, r["gates"], k_tok, Ys, rm.S, shared_logits, ln_out=ln_out)

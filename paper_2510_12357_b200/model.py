@@ -241,10 +241,14 @@ class MoBiLEMoE:
         return sc["Ys"]
 
     # ---- expert-parallel helpers (ep.py) ----
-    def rows_ffn(self, layer: int, rows: torch.Tensor, ids: torch.Tensor) -> torch.Tensor:
-        """Routed-expert FFN of R independent rows, row i through local expert ids[i] (k = 1)."""
+    def rows_ffn(self, layer: int, rows: torch.Tensor, ids: torch.Tensor, k_tok: torch.Tensor | None = None,
+                 clone: bool = True) -> torch.Tensor:
+        """Routed-expert FFN of R independent rows, row i through local expert
+        ids[i] (k = 1); rows with k_tok[i] = 0 are skipped (their output rows
+        are left as they were)."""
         R = rows.shape[0]
-        k_tok = torch.ones(R, dtype=torch.int32, device=rows.device)
+        if k_tok is None:
+            k_tok = torch.ones(R, dtype=torch.int32, device=rows.device)
         sc = self.scratch(R, 1)
         p = K.permute(ids.view(R, 1), k_tok, self.E, out=sc["perm"])
         loc = self.resident(layer)
@@ -252,7 +256,7 @@ class MoBiLEMoE:
             self._routed_tc(rows, p, R, 1, loc, sc)
         else:
             self._stream_ffn(rows, p, layer, R, 1, loc, sc, shared=False)
-        return sc["Y"][:R].clone()
+        return sc["Y"][:R].clone() if clone else sc["Y"][:R]
 
     def shared_rows(self, layer: int, h2: torch.Tensor, sc: dict) -> torch.Tensor:
         """Shared-expert outputs (T, S, d) for the tokens of a routed scratch."""
