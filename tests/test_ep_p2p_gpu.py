@@ -92,3 +92,52 @@ def test_p2p_ep_world2_one_gpu(cuda_ok, T):
     for rank, errs, exc in res:
         assert exc is None, (rank, exc)
         assert max(errs) < 2e-2, (rank, errs)
+
+
+@pytest.mark.parametrize("T,k_max,E,G", [(5, 3, 7, 2), (300, 4, 60, 8), (1, 2, 8, 3), (2048, 2, 8, 8)])
+def test_p2p_plan_matches_nccl_path_order(cuda_ok, T, k_max, E, G):
+    """ep_plan_kernel: each valid pair's (owner, position) equals the stable
+    (owner, pair id) order of EPExchange.plan; unselected slots (-1 ids,
+    k_tok < k_max) are skipped; per-owner counts match."""
+    import ctypes as C
+
+    from paper_2510_12357_b200 import _native as N
+    from paper_2510_12357_b200.ep import owner_table
+    rng = np.random.default_rng(T + E)
+    idx = np.stack([rng.permutation(E)[:k_max] for _ in range(T)]).astype(np.int32)
+    k_tok = rng.integers(1, k_max + 1, size=T).astype(np.int32)
+    idx[rng.random((T, k_max)) < 0.05] = -1
+    dev = torch.device("cuda")
+    own, loc = owner_table(E, G, dev)
+    P = T * k_max
+    cap = P
+    dest = torch.full((P,), -7, dtype=torch.int32, device=dev)
+    counts = torch.zeros(G, dtype=torch.int32, device=dev)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    box = C.c_void_p()
+    N.check(N.lib.mobile_ep_mailbox_create(G, cap, 8, C.byref(box)), "mailbox")
+    try:
+        peers = torch.tensor([box.value] * G, dtype=torch.int64, device=dev)  # every "peer" is this mailbox
+        rows = torch.zeros(T, 8, device=dev)
+        ti, tk = torch.tensor(idx, device=dev), torch.tensor(k_tok, device=dev)
+        own32, loc32 = own.int().contiguous(), loc.int().contiguous()  # alive until the kernels ran
+        N.check(N.lib.mobile_ep_dispatch(N.ptr(rows), N.ptr(ti), N.ptr(tk), T, k_max, 8, N.ptr(own32),
+                                         N.ptr(loc32), N.ptr(peers), G, 0, cap, 1, N.ptr(dest),
+                                         N.ptr(counts), N.ptr(flags), torch.cuda.current_stream().cuda_stream), "dispatch")
+        torch.cuda.synchronize()
+    finally:
+        N.lib.mobile_ep_mailbox_destroy(box)
+    d = dest.cpu().numpy()
+    owner = own.cpu().numpy()
+    want_pos, seen = {}, [0] * G
+    for p in range(P):
+        t, j = divmod(p, k_max)
+        e = idx[t, j]
+        if j < k_tok[t] and e >= 0:
+            g = owner[e]
+            want_pos[p] = g * cap + seen[g]
+            seen[g] += 1
+    for p in range(P):
+        assert d[p] == want_pos.get(p, -1), (p, d[p], want_pos.get(p, -1))
+    assert counts.cpu().tolist() == seen
+    assert int(flags.item()) == 0
