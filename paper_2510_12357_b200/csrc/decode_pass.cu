@@ -844,6 +844,45 @@ __device__ void attn_unit(const Plan& P, int l, const Item& it, int nc, const ch
     if (lane == 0) { part[0] = M; part[1] = S; }
 #pragma unroll
     for (int e = 0; e < PER; ++e) part[kAttnPart + lane + 32 * e] = acc[e];
+    // the head's last chunk to finish merges its nc chunks in chunk order and
+    // writes the final attention row: the o-projection then loads a plain row
+    // instead of every CTA merging every head after the barrier
+    __syncwarp();
+    unsigned last = 0;
+    unsigned* tk = P.sync + 64 + it.b * H + it.h;
+    if (lane == 0) {
+      __threadfence();
+      last = atomicAdd(tk, 1u) == (unsigned)(nc - 1) ? 1u : 0u;
+    }
+    if (__shfl_sync(0xffffffffu, last, 0)) {
+      __threadfence();
+      const float* base = P.attn_part + (size_t)(it.b * H + it.h) * P.nc_max * (hd + kAttnPart);
+      float mc = -INFINITY, sc = 0.f;
+      if (lane < nc) {
+        const float2 ms = __ldcg(reinterpret_cast<const float2*>(base + (size_t)lane * (hd + kAttnPart)));
+        mc = ms.x;
+        sc = ms.y;
+      }
+      const float Mh = warp_max(sc != 0.f ? mc : -INFINITY);
+      const float f = sc != 0.f ? expf(mc - Mh) : 0.f;
+      float Sh = 0.f;
+      for (int c = 0; c < nc; ++c) Sh += __shfl_sync(0xffffffffu, sc * f, c);
+      const float inv = 1.0f / Sh;
+      float O[PER];
+#pragma unroll
+      for (int e = 0; e < PER; ++e) O[e] = 0.f;
+      for (int c = 0; c < nc; ++c) {
+        const float fc = __shfl_sync(0xffffffffu, f, c);
+        if (fc != 0.f) {
+#pragma unroll
+          for (int e = 0; e < PER; ++e)
+            O[e] = fmaf(__ldcg(base + (size_t)c * (hd + kAttnPart) + kAttnPart + lane + 32 * e), fc, O[e]);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < PER; ++e) P.att[(size_t)it.b * d + it.h * hd + lane + 32 * e] = O[e] * inv;
+      if (lane == 0) *tk = 0u;  // ready for the next layer / launch
+    }
   }
   cbar();
 }
@@ -1727,7 +1766,7 @@ int mobile_dp_create(const mobile_dp_model* m, mobile_dp** out) {
     t.type = PT_GEMV; t.n_groups = 1; t.end_bar = 1;
     t.g[0] = dense_group(m->o, Wsz, d, d, EP_STORE);
     t.g[0].out = m->xa; t.g[0].out_ld = d; t.g[0].resid = m->x;
-    t.xkind0 = t.xkind = XK_ATTN; t.xsrc = m->att;
+    t.xkind0 = t.xkind = XK_PLAIN; t.xsrc = m->att;  // merged per head by its last attention chunk
     ts.push_back(t);
   }
   const int router_j = (int)ts.size();
