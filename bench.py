@@ -390,8 +390,11 @@ def cpu_leg(spec, steps, r):
     flags = injected_fallback_flags(1 + steps, r)
     if steps >= 1 and not any(flags[1:]):
         flags[1 + steps // 2] = True  # make the sample contain one replayed big pass
-    secs, fb = CB.time_decode(W, prompt, flags, 1, steps)
-    return {"value": round(steps / secs, 4), "unit": "tokens/s", "cores": CB.cores(), "kind": "port",
+    from threadpoolctl import threadpool_limits
+    n_cores = os.cpu_count() or 1
+    with threadpool_limits(limits=n_cores):
+        secs, fb = CB.time_decode(W, prompt, flags, 1, steps)
+    return {"value": round(steps / secs, 4), "unit": "tokens/s", "cores": n_cores, "kind": "port",
             "sample": f"{steps} decode tokens ({fb} fallback) of the same Qwen shape in fp32 NumPy "
                       f"(oracle KVDecoder), prompt 4, expert/attention matrices aliased to pools > LLC"}
 
@@ -409,14 +412,18 @@ def run_reference(args, ws, rank):
     W = CB.aliased_weights(os_)
     prompt = np.random.default_rng(1).integers(1, QWEN15_MOE.vocab_size, size=4).tolist()
     flags = injected_fallback_flags(args.warmup + args.steps, args.r)
-    secs, fb = CB.time_decode(W, prompt, flags, args.warmup, args.steps)
+    # every host core for the BLAS pool (torchrun sets OMP_NUM_THREADS=1 per rank)
+    from threadpoolctl import threadpool_limits
+    n_cores = os.cpu_count() or 1
+    with threadpool_limits(limits=n_cores):
+        secs, fb = CB.time_decode(W, prompt, flags, args.warmup, args.steps)
     v = args.steps / secs
     line = {"metric": METRIC, "value": round(v, 4), "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(secs / args.steps * 1e3, 2), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "impl": "reference",
             "data": "synthetic (random-init fp32 weights, random prompt)",
             "config": {"workload": WORKLOAD, "model": "Qwen1.5-MoE-A2.7B-shape", "global_batch": 1},
-            "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "cores": CB.cores(), "kind": "port",
+            "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "cores": n_cores, "kind": "port",
                              "sample": f"{args.steps} decode tokens ({fb} fallback), fp32 NumPy oracle KV decode, "
                                        f"prompt 4, matrices aliased to pools > LLC"},
             "e2e": {"value": round(v, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
