@@ -81,9 +81,10 @@ struct GgSched {
   int e[kGgMaxActive], off[kGgMaxActive], n[kGgMaxActive], base[kGgMaxActive + 1];
 };
 
-// tile id -> (expert, m-tile, n-tile): experts in active order, m-tiles of an
-// expert consecutive, n fastest within an m-tile (concurrent CTAs share A and
-// stream neighbouring B tiles of the same expert).
+// tile id -> (expert, m-tile, n-tile): experts in active order, then n-tiles,
+// m fastest: the CTAs that share a B (weight) tile run together, so an
+// expert's weights stream from HBM once however many 128-row m-tiles it has
+// (its A rows are small and stay in L2).
 template <int BN>
 __device__ __forceinline__ GgTile gg_tile(const GgArgs& a, const GgSched& S, int tile) {
   GgTile t;
@@ -94,9 +95,9 @@ __device__ __forceinline__ GgTile gg_tile(const GgArgs& a, const GgSched& S, int
     const int e = tile / per;
     const int r = tile - e * per;
     t.e = e;
-    t.row0 = (r / nt) * kGgBM;
+    t.row0 = (r % mt) * kGgBM;  // m fastest: the CTAs sharing a B tile run together (B read once from HBM)
     t.nrows = min(kGgBM, a.dense_rows - t.row0);
-    t.n0 = (r % nt) * BN;
+    t.n0 = (r / mt) * BN;
     t.bslot = a.slot ? a.slot[e] : e;
     return t;
   }
@@ -107,10 +108,11 @@ __device__ __forceinline__ GgTile gg_tile(const GgArgs& a, const GgSched& S, int
     else hi = mid - 1;
   }
   const int r = tile - S.base[lo];
+  const int mt = (S.n[lo] + kGgBM - 1) / kGgBM;
   t.e = S.e[lo];
-  t.row0 = S.off[lo] + (r / nt) * kGgBM;
+  t.row0 = S.off[lo] + (r % mt) * kGgBM;
   t.nrows = min(kGgBM, S.off[lo] + S.n[lo] - t.row0);
-  t.n0 = (r % nt) * BN;
+  t.n0 = (r / mt) * BN;
   t.bslot = a.slot ? a.slot[t.e] : t.e;
   return t;
 }
