@@ -18,8 +18,9 @@ spec = PRESETS[name]
 dm = DeviceModel(DeviceWeights.random(spec, torch.device("cuda"), seed=0))
 out = {}
 for B in batches:
-    for gemm in (False, True):
-        eng = StepEngine(dm, B, 560, gemm=gemm).build()
+    modes = [(False, None), (True, None)] + ([(False, False)] if B <= 4 else [])
+    for gemm, persistent in modes:
+        eng = StepEngine(dm, B, 560, gemm=gemm, persistent=persistent).build()
         eng.sess.kc.normal_()
         eng.sess.vc.normal_()
         eng.pos.fill_(512)
@@ -36,8 +37,9 @@ for B in batches:
                 e1.record()
             torch.cuda.synchronize()
             res[kd] = round(e0.elapsed_time(e1) / 10, 3)
-        out[f"B{B}_{'gemm' if gemm else 'gemv'}"] = res
-        print(B, "gemm" if gemm else "gemv", res, flush=True)
+        name_ = "gemm" if gemm else ("gemv" if persistent is None else "perop_gemv")
+        out[f"B{B}_{name_}"] = res
+        print(B, name_, res, flush=True)
         del eng
         torch.cuda.empty_cache()
 print(json.dumps(out))
