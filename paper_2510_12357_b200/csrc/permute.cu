@@ -138,6 +138,85 @@ __global__ void __launch_bounds__(1024) combine_kernel(const float* __restrict__
     ln_out[(size_t)t * d + i] = (x_out[(size_t)t * d + i] - mean) * inv;
 }
 
+// float4 variant (d % 4 == 0): the same per-element arithmetic and order,
+// 256 threads so several tokens' CTAs share an SM (prefill / batched decode)
+constexpr int kComb4Threads = 256;
+__global__ void __launch_bounds__(kComb4Threads) combine4_kernel(
+    const float4* __restrict__ x, const float4* __restrict__ Y, const float* __restrict__ gates,
+    const int* __restrict__ k_tok, int k_max, int d4, const float4* __restrict__ Ys, int n_shared,
+    const float* __restrict__ shared_logits, float4* __restrict__ x_out, float4* __restrict__ ln_out) {
+  __shared__ float red[kComb4Threads / 32];
+  __shared__ float sg[16];
+  const int t = blockIdx.x;
+  pdl_trigger();
+  pdl_wait();
+  const int kt = k_tok ? k_tok[t] : k_max;
+  if (threadIdx.x < kt && threadIdx.x < 8) sg[threadIdx.x] = gates[(size_t)t * k_max + threadIdx.x];
+  if (threadIdx.x < n_shared)
+    sg[8 + threadIdx.x] = shared_logits ? sigmoid_f(shared_logits[(size_t)t * n_shared + threadIdx.x]) : 1.0f;
+  __syncthreads();
+  float sum = 0.f;
+  for (int i = threadIdx.x; i < d4; i += kComb4Threads) {
+    float4 yv[8], ys[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) if (j < kt) yv[j] = Y[((size_t)t * k_max + j) * d4 + i];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) if (s < n_shared) ys[s] = Ys[((size_t)t * n_shared + s) * d4 + i];
+    const float4 xv = x[(size_t)t * d4 + i];
+    float m[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j < kt) {
+        m[0] = fmaf(sg[j], yv[j].x, m[0]); m[1] = fmaf(sg[j], yv[j].y, m[1]);
+        m[2] = fmaf(sg[j], yv[j].z, m[2]); m[3] = fmaf(sg[j], yv[j].w, m[3]);
+      }
+    }
+    for (int j = 8; j < kt; ++j) {
+      const float g = gates[(size_t)t * k_max + j];
+      const float4 y = Y[((size_t)t * k_max + j) * d4 + i];
+      m[0] = fmaf(g, y.x, m[0]); m[1] = fmaf(g, y.y, m[1]); m[2] = fmaf(g, y.z, m[2]); m[3] = fmaf(g, y.w, m[3]);
+    }
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      if (s < n_shared) {
+        const float g = sg[8 + s];
+        m[0] += g * ys[s].x; m[1] += g * ys[s].y; m[2] += g * ys[s].z; m[3] += g * ys[s].w;
+      }
+    }
+    const float4 v = make_float4(xv.x + m[0], xv.y + m[1], xv.z + m[2], xv.w + m[3]);
+    x_out[(size_t)t * d4 + i] = v;
+    sum += (v.x + v.y) + (v.z + v.w);
+  }
+  if (!ln_out) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int nw = kComb4Threads / 32;
+  sum = warp_sum(sum);
+  if (lane == 0) red[warp] = sum;
+  __syncthreads();
+  float mean = 0.f;
+#pragma unroll
+  for (int w = 0; w < nw; ++w) mean += red[w];
+  mean /= (float)(4 * d4);
+  __syncthreads();
+  float q = 0.f;
+  for (int i = threadIdx.x; i < d4; i += kComb4Threads) {
+    const float4 v = x_out[(size_t)t * d4 + i];
+    const float a = v.x - mean, b = v.y - mean, c = v.z - mean, e = v.w - mean;
+    q += (a * a + b * b) + (c * c + e * e);
+  }
+  q = warp_sum(q);
+  if (lane == 0) red[warp] = q;
+  __syncthreads();
+  float var = 0.f;
+#pragma unroll
+  for (int w = 0; w < nw; ++w) var += red[w];
+  const float inv = 1.0f / sqrtf(var / (float)(4 * d4) + 1e-5f);
+  for (int i = threadIdx.x; i < d4; i += kComb4Threads) {
+    const float4 v = x_out[(size_t)t * d4 + i];
+    ln_out[(size_t)t * d4 + i] = make_float4((v.x - mean) * inv, (v.y - mean) * inv, (v.z - mean) * inv, (v.w - mean) * inv);
+  }
+}
+
 }  // namespace mobile
 
 using namespace mobile;
@@ -156,6 +235,13 @@ extern "C" int mobile_combine(const float* x, const float* Y, const float* gates
   if (T < 0 || d <= 0 || k_max <= 0 || n_shared < 0) { set_error("combine: bad shape"); return MOBILE_ERR_INVALID; }
   if (T == 0) return MOBILE_OK;
   if (n_shared > 8) { set_error("combine: at most 8 shared experts"); return MOBILE_ERR_UNSUPPORTED; }
+  const bool al = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(x_out) |
+                    reinterpret_cast<uintptr_t>(ln_out) | reinterpret_cast<uintptr_t>(Y_shared)) & 15) == 0;
+  if (d % 4 == 0 && al)
+    return launch_pdl(combine4_kernel, dim3(T), dim3(kComb4Threads), 0, (cudaStream_t)stream, 1, "combine",
+                      reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(Y), gates, k_tok, k_max, d / 4,
+                      reinterpret_cast<const float4*>(Y_shared), Y_shared ? n_shared : 0, shared_logits,
+                      reinterpret_cast<float4*>(x_out), reinterpret_cast<float4*>(ln_out));
   const int threads = d >= 1024 ? 1024 : ((d + 31) / 32) * 32;
   return launch_pdl(combine_kernel, dim3(T), dim3(threads), 0, (cudaStream_t)stream, 1, "combine", x, Y, gates,
                     k_tok, k_max, d, Y_shared, Y_shared ? n_shared : 0, shared_logits, T, x_out, ln_out);
