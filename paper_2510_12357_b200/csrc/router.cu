@@ -339,11 +339,15 @@ __global__ void __launch_bounds__(kRouterThreads) router_kernel(RouterArgs a) {
   }
 }
 
+constexpr int kRouterClusterMaxT = 256;  // measured: clusters win up to batch 256, lose at 512-token prefill
+
 template <typename W, int TT>
 static int launch_router(const RouterArgs& a, cudaStream_t stream) {
   const int Etot = a.E + a.n_extra;
-  // a cluster of up to 8 CTAs splits the router rows of each token tile
-  const int cs = min(8, max(1, (Etot + 7) / 8));
+  // small T: a cluster of up to 8 CTAs splits the router rows of each token
+  // tile (latency); large T (prefill, big batches): the token tiles alone fill
+  // the GPU, so one CTA per tile computes every row (no cluster co-scheduling)
+  const int cs = a.T > kRouterClusterMaxT ? 1 : min(8, max(1, (Etot + 7) / 8));
   const size_t smem = sizeof(float) * ((size_t)TT * a.d + (size_t)TT * Etot + 64);
   auto kern = router_kernel<W, TT>;
   if (int st = set_smem_once((const void*)kern, smem)) return st;
