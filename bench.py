@@ -192,7 +192,8 @@ def run_ours(args, ws, rank, local):
 
     def make_engine(graphs=True):
         rt = OffloadRuntime(dw, slots, lookahead=2)
-        eng = StepEngine(dm, 1, max_len, runtime=rt, graphs=graphs).build(gamma=policy.gamma)
+        persistent = None if os.environ.get("MOBILE_PERSISTENT", "") == "" else os.environ["MOBILE_PERSISTENT"] != "0"
+        eng = StepEngine(dm, 1, max_len, runtime=rt, graphs=graphs, persistent=persistent).build(gamma=policy.gamma)
         return rt, eng
 
     def timed_decode(full: bool):

@@ -5,6 +5,9 @@
 // one CUDA graph -- instead of a few hundred framework ops.  Semantics follow
 // toymoe.py:171-186 (sinusoidal positions added to the embedding; pre-LN
 // attention, scale 1/sqrt(head_dim), softmax, residual).
+#include <algorithm>
+#include <mutex>
+
 #include "common.cuh"
 
 namespace mobile {
@@ -195,29 +198,38 @@ template <int HD>
 __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const float* __restrict__ qkv,
                                                                        float* __restrict__ kc, float* __restrict__ vc,
                                                                        const int* __restrict__ pos, int d, int H,
-                                                                       int max_len, float* __restrict__ out) {
+                                                                       int max_len, float* __restrict__ out, int nsplit,
+                                                                       float* __restrict__ ws, unsigned* __restrict__ tk) {
   constexpr int NW = kAttnThreads / 32;
   constexpr int LS = HD / 16, PS = 32 / LS;  // score lanes per position, positions per warp step
   constexpr int LV = HD / 4, PV = 32 / LV;   // P.V lanes per position, positions per warp step
-  extern __shared__ __align__(16) float sc[];  // max_len scores
+  extern __shared__ __align__(16) float sc[];  // this split's scores
   __shared__ __align__(16) float qs[HD];
   __shared__ __align__(16) float part[NW * PV][HD];
   __shared__ float red[NW];
+  __shared__ int last_s;
   pdl_trigger();
   pdl_wait();
-  const int b = blockIdx.x / H, hh = blockIdx.x % H;
+  const int bh = blockIdx.x / nsplit, sp = blockIdx.x - bh * nsplit;
+  const int b = bh / H, hh = bh % H;
   const int p = pos[b];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (p < 0 || p >= max_len) {  // position outside the cache: poison the output, touch nothing
-    for (int e = threadIdx.x; e < HD; e += blockDim.x) out[(size_t)b * d + hh * HD + e] = __int_as_float(0x7fc00000);
+    if (sp == 0)
+      for (int e = threadIdx.x; e < HD; e += blockDim.x) out[(size_t)b * d + hh * HD + e] = __int_as_float(0x7fc00000);
     return;
   }
+  // split sp owns positions [j0, j1) of [0, p]; the split holding p writes the new row
+  const int n = p + 1;
+  const int j0 = (int)((long long)n * sp / nsplit), j1 = (int)((long long)n * (sp + 1) / nsplit);
   const float* src = qkv + (size_t)b * 3 * d;
   const size_t head0 = ((size_t)b * H + hh) * max_len;  // head-major cache (B, H, max_len, HD)
   for (int e = threadIdx.x; e < HD; e += blockDim.x) {
     qs[e] = src[hh * HD + e];
-    kc[(head0 + p) * HD + e] = src[d + hh * HD + e];
-    vc[(head0 + p) * HD + e] = src[2 * d + hh * HD + e];
+    if (j1 == n) {
+      kc[(head0 + p) * HD + e] = src[d + hh * HD + e];
+      vc[(head0 + p) * HD + e] = src[2 * d + hh * HD + e];
+    }
   }
   __syncthreads();
   const float scale = 1.0f / sqrtf((float)HD);
@@ -230,10 +242,10 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
     qv[4 * i] = q4.x; qv[4 * i + 1] = q4.y; qv[4 * i + 2] = q4.z; qv[4 * i + 3] = q4.w;
   }
   float mx = -INFINITY;
-  for (int j0 = warp * PS; j0 <= p; j0 += NW * PS) {
-    const int j = j0 + sg;
+  for (int jj = j0 + warp * PS; jj < j1; jj += NW * PS) {
+    const int j = jj + sg;
     float s = 0.f;
-    if (j <= p) {
+    if (j < j1) {
       const float4* kr = reinterpret_cast<const float4*>(kc + (head0 + j) * HD + sl * 16);
       float4 k4[4];
 #pragma unroll
@@ -244,9 +256,9 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
     }
 #pragma unroll
     for (int o = LS / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (j <= p) {
+    if (j < j1) {
       s *= scale;
-      if (sl == 0) sc[j] = s;
+      if (sl == 0) sc[j - j0] = s;
       mx = fmaxf(mx, s);
     }
   }
@@ -258,9 +270,9 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
   for (int i = 0; i < NW; ++i) mx = fmaxf(mx, red[i]);
   __syncthreads();
   float sum = 0.f;
-  for (int j = threadIdx.x; j <= p; j += blockDim.x) {
-    const float e = expf(sc[j] - mx);
-    sc[j] = e;
+  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+    const float e = expf(sc[j - j0] - mx);
+    sc[j - j0] = e;
     sum += e;
   }
   sum = warp_sum(sum);
@@ -272,21 +284,62 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
   // ---- P.V
   const int vg = lane / LV, vl = lane % LV;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int j = warp * PV + vg; j <= p; j += NW * PV) {
-    const float w = sc[j];
+  for (int j = j0 + warp * PV + vg; j < j1; j += NW * PV) {
+    const float w = sc[j - j0];
     const float4 v4 = __ldcs(reinterpret_cast<const float4*>(vc + (head0 + j) * HD) + vl);
     acc.x = fmaf(w, v4.x, acc.x); acc.y = fmaf(w, v4.y, acc.y);
     acc.z = fmaf(w, v4.z, acc.z); acc.w = fmaf(w, v4.w, acc.w);
   }
   reinterpret_cast<float4*>(part[warp * PV + vg])[vl] = acc;
   __syncthreads();
-  const float inv = 1.0f / sum;
+  if (nsplit == 1) {
+    const float inv = 1.0f / sum;
+    for (int e = threadIdx.x; e < HD; e += blockDim.x) {
+      float o = 0.f;
+#pragma unroll
+      for (int i = 0; i < NW * PV; ++i) o += part[i][e];
+      out[(size_t)b * d + hh * HD + e] = o * inv;
+    }
+    return;
+  }
+  // ---- split-KV: this split's (m, s, o) partial; the (b, h)'s last split merges in split order
+  float* wp = ws + (size_t)blockIdx.x * (HD + 2);
   for (int e = threadIdx.x; e < HD; e += blockDim.x) {
     float o = 0.f;
 #pragma unroll
     for (int i = 0; i < NW * PV; ++i) o += part[i][e];
+    wp[2 + e] = o;
+  }
+  if (threadIdx.x == 0) { wp[0] = mx; wp[1] = sum; }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last_s = atomicAdd(tk + bh, 1u) == (unsigned)(nsplit - 1);
+  __syncthreads();
+  if (!last_s) return;
+  __threadfence();
+  const float* w0 = ws + (size_t)bh * nsplit * (HD + 2);
+  float M = -INFINITY;
+  for (int q = 0; q < nsplit; ++q) {
+    const float* w = w0 + (size_t)q * (HD + 2);
+    if (__ldcg(w + 1) != 0.f) M = fmaxf(M, __ldcg(w));
+  }
+  float S = 0.f;
+  for (int q = 0; q < nsplit; ++q) {
+    const float* w = w0 + (size_t)q * (HD + 2);
+    const float sq = __ldcg(w + 1);
+    if (sq != 0.f) S += sq * expf(__ldcg(w) - M);
+  }
+  const float inv = 1.0f / S;
+  for (int e = threadIdx.x; e < HD; e += blockDim.x) {
+    float o = 0.f;
+    for (int q = 0; q < nsplit; ++q) {
+      const float* w = w0 + (size_t)q * (HD + 2);
+      const float sq = __ldcg(w + 1);
+      if (sq != 0.f) o = fmaf(__ldcg(w + 2 + e), expf(__ldcg(w) - M), o);
+    }
     out[(size_t)b * d + hh * HD + e] = o * inv;
   }
+  if (threadIdx.x == 0) tk[bh] = 0u;
 }
 
 // x[b] = embed[tok[b]] + pe[pos[b]]  (toymoe.py:172), optionally ln_out = LN(x)
@@ -379,6 +432,36 @@ extern "C" int mobile_dense_gemv(const float* x, int T, int d, int do_ln, const 
   return MOBILE_ERR_UNSUPPORTED;
 }
 
+// split-KV partials + per-(b, h) tickets: one library workspace, grown outside
+// graph capture only (captured launches keep their pointers: never freed)
+static bool attn_split_ws(int floats, int tickets, cudaStream_t stream, float** ws, unsigned** tk) {
+  static std::mutex mu;
+  static float* g_ws = nullptr;
+  static unsigned* g_tk = nullptr;
+  static int g_floats = 0, g_tickets = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  if (floats > g_floats || tickets > g_tickets) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
+    const int nf = std::max(floats, 1 << 20), nt = std::max(tickets, 4096);
+    float* w = nullptr;
+    unsigned* t = nullptr;
+    if (cudaMalloc(&w, (size_t)nf * sizeof(float)) != cudaSuccess) return false;
+    if (cudaMalloc(&t, (size_t)nt * sizeof(unsigned)) != cudaSuccess || cudaMemset(t, 0, (size_t)nt * sizeof(unsigned)) != cudaSuccess) {
+      cudaFree(w);
+      return false;
+    }
+    cudaDeviceSynchronize();
+    g_ws = w;  // the previous buffers stay allocated: graphs captured earlier may point at them
+    g_tk = t;
+    g_floats = nf;
+    g_tickets = nt;
+  }
+  *ws = g_ws;
+  *tk = g_tk;
+  return true;
+}
+
 extern "C" int mobile_attn_decode(const float* qkv, float* k_cache, float* v_cache, const int* pos, int B, int d,
                                   int H, int max_len, float* out, void* stream) {
   if (B <= 0 || d <= 0 || H <= 0 || d % H || max_len <= 0) { set_error("attn_decode: bad shape"); return MOBILE_ERR_INVALID; }
@@ -388,8 +471,15 @@ extern "C" int mobile_attn_decode(const float* qkv, float* k_cache, float* v_cac
     if (vsmem > 160 * 1024) { set_error("attn_decode: max_len=%d too long", max_len); return MOBILE_ERR_UNSUPPORTED; }
     auto kern = hd == 64 ? attn_decode_vec_kernel<64> : attn_decode_vec_kernel<128>;
     if (int st = set_smem_once((const void*)kern, vsmem)) return st;
-    return launch_pdl(kern, dim3(B * H), dim3(kAttnThreads), vsmem, (cudaStream_t)stream, 1, "attn_decode", qkv,
-                      k_cache, v_cache, pos, d, H, max_len, out);
+    // split-KV when (sequence, head) pairs alone leave SMs idle on a long cache
+    int nsplit = 1;
+    const int bhn = B * H;
+    if (bhn < sm_count() && max_len >= 256) nsplit = std::min(std::min(16, (2 * sm_count() + bhn - 1) / bhn), max_len / 64);
+    float* ws = nullptr;
+    unsigned* tk = nullptr;
+    if (nsplit > 1 && !attn_split_ws(bhn * nsplit * (hd + 2), bhn, (cudaStream_t)stream, &ws, &tk)) nsplit = 1;
+    return launch_pdl(kern, dim3(bhn * nsplit), dim3(kAttnThreads), vsmem, (cudaStream_t)stream, 1, "attn_decode", qkv,
+                      k_cache, v_cache, pos, d, H, max_len, out, nsplit, ws, tk);
   }
   const size_t smem = sizeof(float) * ((size_t)max_len + d / H);
   if (smem > 200 * 1024) { set_error("attn_decode: max_len=%d too long", max_len); return MOBILE_ERR_UNSUPPORTED; }

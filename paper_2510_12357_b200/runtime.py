@@ -51,6 +51,13 @@ class StepEngine:
             gemm = batch > GEMV_MAX_BATCH or (batch >= GEMM_MIN_BATCH and runtime is None and dm.moe.tc_ok
                                               and persistent is not True)
         self.gemm_path = bool(gemm)
+        # resident batch 1: the per-op engine (graph-replayed, PDL-chained
+        # kernels; split-KV attention) beats the persistent pass on every
+        # config (scripts/batch_paths.py: C2 1.07 vs 1.29 ms, C3 1.94 vs 2.13,
+        # C4 1.92 vs 2.31, C5 4.61 vs 5.76 ms little pass); the persistent pass
+        # stays the default for B = 2 and for offloaded experts (zero-sync)
+        if persistent is None and runtime is None and batch == 1 and not self.gemm_path:
+            persistent = False
         if self.gemm_path:
             if not dm.moe.tc_ok:
                 raise ValueError(f"StepEngine: batch {batch} > {GEMV_MAX_BATCH} needs the tcgen05 GEMM path "

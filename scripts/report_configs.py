@@ -81,7 +81,7 @@ for name in sys.argv[1:] or ["c2", "c3", "c4", "c5"]:
     for B in batches:
         print(f"[{name}] B={B}", file=sys.stderr, flush=True)
         eng = engine(B)
-        row = {"path": "gemm" if eng.gemm_path else "persistent"}
+        row = {"path": "gemm" if eng.gemm_path else ("persistent" if eng.dp else "per-op")}
         if eng.dp:
             row["dp_info"] = eng.dp_info()
         for kd in ("little", "big", "full"):

@@ -328,3 +328,36 @@ def test_logits_confidence_vs_torch(cuda_ok, T, V):
     assert (out["argmax"].long().cpu() == first.cpu()).all()
     assert int(out["argmax"][0]) == V // 3
     assert (out["fallback"].cpu().bool() == (out["conf"].cpu() <= gamma)).all()
+
+
+@pytest.mark.parametrize("B,H,hd,max_len,pos", [(1, 16, 128, 1024, [700]), (2, 4, 64, 512, [5, 400]),
+                                                (1, 32, 128, 2100, [2047]), (3, 2, 128, 256, [0, 1, 255]),
+                                                (8, 16, 128, 64, [10, 20, 30, 40, 50, 60, 63, 0])])
+def test_attn_decode_vs_torch(cuda_ok, B, H, hd, max_len, pos):
+    """KV-cache attention at one new position per sequence (head-major cache):
+    the new K/V rows land in the cache, output = softmax(q K^T / sqrt(hd)) V
+    over positions 0..pos -- with and without the split-KV path (few
+    (sequence, head) pairs on a long cache), empty splits included."""
+    from paper_2510_12357_b200 import kernels as K
+    d = H * hd
+    g = torch.Generator(device="cuda").manual_seed(B * 100 + H)
+    kc = torch.randn(B, H, max_len, hd, device="cuda", generator=g)
+    vc = torch.randn(B, H, max_len, hd, device="cuda", generator=g)
+    qkv = torch.randn(B, 3 * d, device="cuda", generator=g)
+    p = torch.tensor(pos, dtype=torch.int32, device="cuda")
+    kc0, vc0 = kc.clone(), vc.clone()
+    out = torch.empty(B, d, device="cuda")
+    for _ in range(2):  # twice: the split tickets must reset
+        kc.copy_(kc0)
+        vc.copy_(vc0)
+        K.attn_decode(qkv, kc, vc, p, H, out=out)
+    torch.cuda.synchronize()
+    for b in range(B):
+        q, k, v = qkv[b, :d].view(H, hd), qkv[b, d:2 * d].view(H, hd), qkv[b, 2 * d:].view(H, hd)
+        kk, vv = kc0[b].clone(), vc0[b].clone()
+        kk[:, pos[b]] = k
+        vv[:, pos[b]] = v
+        assert torch.equal(kc[b, :, pos[b]], k) and torch.equal(vc[b, :, pos[b]], v)
+        sc = torch.einsum("hd,hpd->hp", q.double(), kk[:, :pos[b] + 1].double()) / hd ** 0.5
+        want = torch.einsum("hp,hpd->hd", torch.softmax(sc, dim=-1), vv[:, :pos[b] + 1].double()).reshape(d)
+        assert torch.allclose(out[b].double(), want, rtol=1e-4, atol=1e-5), (b, (out[b].double() - want).abs().max())
