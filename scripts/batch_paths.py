@@ -1,5 +1,6 @@
-"""Decode pass time per batch on the persistent GEMV kernel vs the GEMM path
-(chooses GEMM_MIN_BATCH).  python scripts/batch_paths.py [preset] [B...]"""
+"""Decode pass time per batch: persistent pass vs GEMM path vs per-op GEMV
+engine (the measurements behind StepEngine's defaults).
+    python scripts/batch_paths.py [preset] [B...]"""
 import json
 import sys
 from pathlib import Path
@@ -18,7 +19,7 @@ spec = PRESETS[name]
 dm = DeviceModel(DeviceWeights.random(spec, torch.device("cuda"), seed=0))
 out = {}
 for B in batches:
-    modes = [(False, None), (True, None)] + ([(False, False)] if B <= 4 else [])
+    modes = ([(False, True)] if B <= 4 else []) + [(True, None)] + ([(False, False)] if B <= 4 else [])
     for gemm, persistent in modes:
         eng = StepEngine(dm, B, 560, gemm=gemm, persistent=persistent).build()
         eng.sess.kc.normal_()
@@ -37,7 +38,7 @@ for B in batches:
                 e1.record()
             torch.cuda.synchronize()
             res[kd] = round(e0.elapsed_time(e1) / 10, 3)
-        name_ = "gemm" if gemm else ("gemv" if persistent is None else "perop_gemv")
+        name_ = "gemm" if gemm else ("persistent" if persistent else "perop_gemv")
         out[f"B{B}_{name_}"] = res
         print(B, name_, res, flush=True)
         del eng
