@@ -441,8 +441,9 @@ int mobile_dp_create(const mobile_dp_model* m, mobile_dp** out);
 void mobile_dp_destroy(mobile_dp* p);
 int mobile_dp_num_segments(const mobile_dp* p);
 int mobile_dp_info(const mobile_dp* p, int* out4); /* phases, stages, smem bytes, grid */
-/* optional device buffer (phases x grid x 3 u64): per phase and CTA the
- * globaltimer at [barrier passed, inputs ready, work done]; NULL = off */
+/* optional device buffer (phases x grid x 6 u64): per phase and CTA the
+ * globaltimer at [inputs visible, inputs built, work done, arrival issued,
+ * barrier observed, acquire fence done]; NULL = off */
 int mobile_dp_set_trace(mobile_dp* p, unsigned long long* trace);
 /* optional event log (grid x 2 roles x 1024 x 2 u64: globaltimer, code<<56 | phase<<32 | item); NULL = off */
 int mobile_dp_set_events(mobile_dp* p, unsigned long long* evt);

@@ -201,6 +201,22 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   return v;
 }
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// Acquire side of the grid barrier / flags: a relaxed poll observed the
+// released value, then an acquire-only fence (PTX 8.6).  Measured on B200: a
+// fence with RELEASE semantics (fence.acq_rel, red.release, __threadfence)
+// waits for every memory operation the SM has in flight -- including the
+// producer's 64 KB bulk copies -- so under the weight stream it costs 1-3 us;
+// fence.acquire does not (scripts/barrier_load_bench.cu).
+#ifndef MOBILE_DP_ACQ_FENCE
+#define MOBILE_DP_ACQ_FENCE 1
+#endif
+__device__ __forceinline__ void fence_acquire() {
+#if MOBILE_DP_ACQ_FENCE
+  asm volatile("fence.acquire.gpu;" ::: "memory");
+#else
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
+}
 __device__ __forceinline__ int ld_acquire_sys(const int* p) {
   int v;
   asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -248,6 +264,7 @@ __device__ __forceinline__ float reduce_rows16(float (&a)[16][TT], int t, int la
 }
 
 constexpr int kEvt = 1024;
+constexpr int kTraceSlots = 6;
 enum EvtCode { EV_W = 1, EV_X = 2, EV_FULL = 3, EV_UNIT = 4, EV_ARRIVE = 5, EV_PASS = 6, EV_READY = 7, EV_ROUTE = 8, EV_WAIT = 9, EV_RED = 10 };
 __device__ __forceinline__ void log_evt(const unsigned long long* base_, int role, int& n, int code, int p, int item) {
   unsigned long long* base = const_cast<unsigned long long*>(base_);
@@ -305,7 +322,7 @@ __device__ __forceinline__ Group grp_t(const Group& G0, int l) {
   return G;
 }
 
-__device__ void spin_until(const Plan& P, unsigned target, int p = -1) {
+__device__ void spin_until(const Plan& P, unsigned target, int p = -1, unsigned long long* tr = nullptr) {
   if (target == 0u) return;
   if (ld_relaxed(P.sync) < target) {
     const unsigned long long t0 = gtimer();
@@ -321,7 +338,9 @@ __device__ void spin_until(const Plan& P, unsigned target, int p = -1) {
       }
     }
   }
-  fence_acq_rel();
+  if (tr) tr[0] = gtimer();
+  fence_acquire();
+  if (tr) tr[1] = gtimer();
 }
 
 // ------------------------------------------------------------------ routing
@@ -965,7 +984,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
         }
       }
       __syncwarp();
-      fence_acq_rel();
+      fence_acquire();
       compute_route(P, l, rt_e, true);
       int* dst = reinterpret_cast<int*>(P.route_pub + l);
       const int* src = reinterpret_cast<const int*>(&rt_e);
@@ -1040,7 +1059,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
               }
               ok = __shfl_sync(0xffffffffu, ok, 0);
               if (!ok) return 2;
-              fence_acq_rel();
+              fence_acquire();
               compute_route(P, wl, rt_p, false);
             }
             rt_layer = wl;
@@ -1252,7 +1271,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
           }
           if (__shfl_sync(0xffffffffu, ok, 0)) {
             if (lane == 0) {
-              fence_acq_rel();
+              fence_acquire();
               asm volatile("fence.proxy.async.global;" ::: "memory");
               char* stg = smem + (size_t)s * stage_bytes + kWBytes;
               mbar_arrive_tx(&full[s], (uint32_t)(mt.nt * mt.xbytes));
@@ -1318,14 +1337,16 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
       for (int i = tid; i < (int)(sizeof(Tmpl) / 16); i += kCW * 32) dst[i] = src[i];
     }
     const Tmpl& T = cph;
+    // trace (debug): [0] inputs visible, [1] inputs built, [2] work done, [3] arrival
+    // issued, [4] barrier observed, [5] acquire fence done
+    unsigned long long* tr = P.trace ? P.trace + ((size_t)(p - first) * G + blockIdx.x) * kTraceSlots : nullptr;
     // ---- wait for the phase's inputs
     if (tid == 0) {
       const int dep = dep_of(P, p);
-      if (dep >= first) spin_until(P, bar_target(P, dep, first), p);
+      if (dep >= first) spin_until(P, bar_target(P, dep, first), p, tr ? tr + 4 : nullptr);
     }
     cbar();
     if (tid == 0) log_evt(P.evt, 1, cev, EV_PASS, p, 0);
-    unsigned long long* tr = P.trace ? P.trace + ((size_t)(p - first) * G + blockIdx.x) * 3 : nullptr;
     if (tr && tid == 0) tr[0] = gtimer();
     const int rot = rot_of(P, j, l);
     // ---- the layer's selection (one call site: inlined once)
@@ -1569,6 +1590,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
     if (tr && tid == 0) tr[2] = gtimer();
     if (tid == 0) log_evt(P.evt, 1, cev, EV_ARRIVE, p, 0);
     if (T.end_bar && tid == 0) red_release_add(P.sync, 1u);
+    if (tr && tid == 0) tr[3] = gtimer();
   }
   // exit ticket: the last CTA out resets the barrier for the next launch
   if (tid == 0) {

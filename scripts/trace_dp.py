@@ -23,7 +23,7 @@ dm = DeviceModel(DeviceWeights.random(spec, torch.device("cuda"), seed=0))
 eng = StepEngine(dm, 1, 600, graphs=False, persistent=True).build()
 info = eng.dp_info(kind)
 G, nph = info["grid"], info["phases"]
-trace = torch.zeros(nph * G * 3, dtype=torch.int64, device="cuda")
+trace = torch.zeros(nph * G * 6, dtype=torch.int64, device="cuda")
 prompt = np.random.default_rng(0).integers(1, spec.vocab_size, size=512).tolist()
 eng.prefill(prompt)
 for i in range(3):
@@ -33,7 +33,7 @@ torch.cuda.synchronize()
 with torch.cuda.stream(eng.stream):
     eng.run_pass(kind)
 torch.cuda.synchronize()
-t = trace.view(nph, G, 3).cpu().numpy().astype(np.float64)
+t = trace.view(nph, G, 6).cpu().numpy().astype(np.float64)
 t0 = t[0, :, 0].min()
 t = (t - t0) / 1e3  # us
 names = ["qkv", "attn", "o", "router+sgu", "gu+sd", "down"]
@@ -47,9 +47,14 @@ for p in range(nph):
     done = t[p, :, 2]
     done_max = done.max() if p < nph - 1 else float("nan")
     rows.append((p, kindname, round(start_max, 2), round(ready_max, 2), round(done_max, 2)))
-    d = per.setdefault(kindname, dict(n=0, bar=0.0, ready=0.0, work=0.0))
+    d = per.setdefault(kindname, dict(n=0, bar=0.0, ready=0.0, work=0.0, release=0.0, observe=0.0, acquire=0.0))
     d["n"] += 1
     d["bar"] += start_max - prev_done
+    if p > 0:  # the barrier this phase waited on: previous phase's arrivals
+        q = p - 1
+        d["release"] += float(np.max(t[q, :, 3] - t[q, :, 2]))          # slowest red.release issue
+        d["observe"] += float(np.median(t[p, :, 4]) - t[q, :, 3].max())  # last arrival -> median observer
+        d["acquire"] += float(np.max(t[p, :, 5] - t[p, :, 4]))         # slowest acquire fence
     d["ready"] += ready_max - start_max
     if p < nph - 1:
         d["work"] += done_max - ready_max
