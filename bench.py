@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--cap-gib", type=float, default=16.0)
     ap.add_argument("--reserved-gib", type=float, default=6.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-steps", type=int, default=6)
+    ap.add_argument("--cpu-steps", type=int, default=0, help="CPU-baseline tokens (default: --steps)")
     ap.add_argument("--layers", type=int, default=0, help="debug only: fewer layers (invalidates the number)")
     return ap.parse_args()
 
@@ -151,6 +151,15 @@ def ncu_traffic():
         return d.get("decode_pass_dram_bytes_per_launch")
     except Exception:
         return None
+
+
+def bench_config(args, ws, slots, routed_experts, layers):
+    """The workload's config block -- identical for both arms (same_config)."""
+    return {"workload": WORKLOAD, "model": "Qwen1.5-MoE-A2.7B-shape", "global_batch": ws,
+            "seq_len": args.prompt_len + args.warmup + args.steps, "context": args.prompt_len,
+            "parallelism": f"replicas{ws}" if ws > 1 else "single", "hbm_expert_slots": slots,
+            "routed_experts": routed_experts, "r_injected": args.r, "lookahead": 2, "gamma": 0.7,
+            "l2": "inputs > L2: ~4.7 GB of weights streamed per token (no flush)", "layers": layers}
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -279,7 +288,7 @@ def run_ours(args, ws, rank, local):
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_leg(spec, args.cpu_steps, args.r)
+        cpu = cpu_leg(args, args.cpu_steps or K_, 2)
 
     if rank == 0:
         line = {
@@ -287,12 +296,7 @@ def run_ours(args, ws, rank, local):
             "warmup": W_, "ms_per_step": round(dev_s / K_ * 1e3, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random-init bf16 weights on the device, random 512-token prompt)",
-            "config": {"workload": WORKLOAD, "model": "Qwen1.5-MoE-A2.7B-shape", "global_batch": ws,
-                       "seq_len": args.prompt_len + W_ + K_, "parallelism": f"replicas{ws}" if ws > 1 else "single",
-                       "hbm_expert_slots": slots, "routed_experts": spec.num_layers * spec.num_experts,
-                       "r_injected": args.r, "lookahead": 2, "gamma": 0.7,
-                       "l2": "inputs > L2: ~4.7 GB of weights streamed per token (no flush)",
-                       "layers": spec.num_layers},
+            "config": bench_config(args, ws, slots, spec.num_layers * spec.num_experts, spec.num_layers),
             "baseline_full_topk": {"value": round(base_value, 3), "unit": "tokens/s",
                                    "ms_per_step": round(base_s / K_ * 1e3, 3), "h2d_bytes": base["h2d_bytes"],
                                    "cache_hits": base["hits"], "transfers": base["transfers"]},
@@ -380,54 +384,48 @@ def kernels_per_pass(eng, kind):
     return s.num_layers * per_layer + 2
 
 
-def cpu_leg(spec, steps, r):
+def cpu_leg(args, steps, warmup):
+    """The oracle port of the same decode on this host's cores (oracle/ only:
+    the product package is never on this path)."""
+    from dataclasses import replace
+
     import numpy as np
 
     from oracle import cpu_baseline as CB
-    from paper_2510_12357_b200.policy import injected_fallback_flags
-    os_ = CB.oracle_spec_from(spec)
-    W = CB.aliased_weights(os_)
-    prompt = np.random.default_rng(1).integers(1, spec.vocab_size, size=4).tolist()
-    flags = injected_fallback_flags(1 + steps, r)
-    if steps >= 1 and not any(flags[1:]):
-        flags[1 + steps // 2] = True  # make the sample contain one replayed big pass
+    from oracle import moe_ref as R
+    spec = CB.C3_SPEC if not args.layers else replace(CB.C3_SPEC, num_layers=args.layers)
+    W = CB.aliased_weights(spec)
+    prompt = np.random.default_rng(1).integers(1, spec.vocab_size, size=1).tolist()
+    flags = R.injected_fallback_flags(warmup + steps, args.r)
     from threadpoolctl import threadpool_limits
     n_cores = os.cpu_count() or 1
     with threadpool_limits(limits=n_cores):
-        secs, fb = CB.time_decode(W, prompt, flags, 1, steps)
+        secs, fb = CB.time_decode(W, prompt, flags, warmup, steps, context=args.prompt_len - 1)
     return {"value": round(steps / secs, 4), "unit": "tokens/s", "cores": n_cores, "kind": "port",
-            "sample": f"{steps} decode tokens ({fb} fallback) of the same Qwen shape in fp32 NumPy "
-                      f"(oracle KVDecoder), prompt 4, expert/attention matrices aliased to pools > LLC"}
+            "sample": f"{steps} decode tokens ({fb} fallback, injected r={args.r}) of the same Qwen shape after "
+                      f"{warmup} warm-up tokens, context {args.prompt_len} (synthetic KV cache), fp32 NumPy oracle "
+                      f"KVDecoder on {n_cores} threads; expert/attention matrices aliased to pools > LLC"}
 
 
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args, ws, rank):
+    """The reference's CPU path of the same decode: the oracle port (the
+    reference package cannot build d=2048 models, toymoe.py:100-107), every
+    host core, the same metric / unit / config.  Imports oracle/ only."""
     if rank != 0:
         return
-    import numpy as np
-
     from oracle import cpu_baseline as CB
-    from paper_2510_12357_b200.policy import injected_fallback_flags
-    from paper_2510_12357_b200.presets import QWEN15_MOE
-    os_ = CB.oracle_spec_from(QWEN15_MOE)
-    W = CB.aliased_weights(os_)
-    prompt = np.random.default_rng(1).integers(1, QWEN15_MOE.vocab_size, size=4).tolist()
-    flags = injected_fallback_flags(args.warmup + args.steps, args.r)
-    # every host core for the BLAS pool (torchrun sets OMP_NUM_THREADS=1 per rank)
-    from threadpoolctl import threadpool_limits
-    n_cores = os.cpu_count() or 1
-    with threadpool_limits(limits=n_cores):
-        secs, fb = CB.time_decode(W, prompt, flags, args.warmup, args.steps)
-    v = args.steps / secs
-    line = {"metric": METRIC, "value": round(v, 4), "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(secs / args.steps * 1e3, 2), "higher_is_better": True,
+    slots = CB.c3_slots(int(args.cap_gib * 2**30), int(args.reserved_gib * 2**30))
+    spec = CB.C3_SPEC
+    cpu = cpu_leg(args, args.steps, args.warmup)
+    v = cpu["value"]
+    line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 / v, 2), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "impl": "reference",
-            "data": "synthetic (random-init fp32 weights, random prompt)",
-            "config": {"workload": WORKLOAD, "model": "Qwen1.5-MoE-A2.7B-shape", "global_batch": 1},
-            "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "cores": n_cores, "kind": "port",
-                             "sample": f"{args.steps} decode tokens ({fb} fallback), fp32 NumPy oracle KV decode, "
-                                       f"prompt 4, matrices aliased to pools > LLC"},
-            "e2e": {"value": round(v, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "data": "synthetic (random-init fp32 weights, synthetic 512-position KV context)",
+            "config": bench_config(args, ws, slots, spec.num_layers * spec.num_experts, spec.num_layers),
+            "cpu_baseline": cpu,
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 

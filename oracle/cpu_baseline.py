@@ -74,11 +74,47 @@ def oracle_spec_from(ms) -> R.OracleSpec:
                         pos_encoding=ms.pos_encoding)
 
 
-def time_decode(W: R.OracleWeights, prompt, flags, warmup: int, steps: int, gamma=0.7):
-    """MoBiLE KV decode on the CPU: returns (seconds for `steps` tokens, fallbacks)."""
+# The bench workload's shape (BASELINE.json configs[2], C3) restated on the
+# oracle side, so bench.py's CPU legs never import the product package:
+# Qwen1.5-MoE-A2.7B (d2048, 24 layers, 60 routed experts top-4 / little top-2,
+# one 5632-wide sigmoid-gated shared expert, V151936), unit-scale embeddings,
+# no additive position code (paper_2510_12357_b200/presets.py QWEN15_MOE).
+C3_SPEC = R.OracleSpec(num_layers=24, num_experts=60, k_big=4, k_little=2, hidden_dim=2048, vocab_size=151936,
+                       ffn_dim=1408, activation="swiglu", n_shared=1, shared_ffn_dim=5632, shared_gate="sigmoid",
+                       n_heads=16, embed_scale=1.0, pos_encoding="none")
+
+
+def c3_slots(cap_bytes: int, reserved_bytes: int, spec: R.OracleSpec = C3_SPEC) -> int:
+    """hbm_expert_slots (config.py:204-218) on the bf16 device sizes of `spec`
+    (expert = 3 d I, dense/layer = qkv+o + router + shared + shared gate)."""
+    d, per = spec.hidden_dim, 2
+    expert = 3 * d * spec.ffn_dim * per
+    dense = 4 * d * d * per + d * spec.num_experts * per + spec.n_shared * 3 * d * spec.shared_ffn_dim * per \
+        + (spec.n_shared * d * per if spec.shared_gate == "sigmoid" else 0)
+    return R.hbm_expert_slots(spec.num_layers, dense, cap_bytes, reserved_bytes, expert, spec.k_big)
+
+
+def synthetic_context(dec: R.KVDecoder, n: int, seed: int = 3) -> None:
+    """Fill the KV cache with `n` random positions (a bounded stand-in for
+    prefilling an n-token prompt: decode cost depends on the cache length,
+    not its contents)."""
+    rng = np.random.default_rng(seed)
+    d = dec.W.spec.hidden_dim
+    for l in range(dec.W.spec.num_layers):
+        dec.k_cache[l] = rng.standard_normal((n, d), dtype=np.float32)
+        dec.v_cache[l] = rng.standard_normal((n, d), dtype=np.float32)
+
+
+def time_decode(W: R.OracleWeights, prompt, flags, warmup: int, steps: int, gamma=0.7, context: int = 0):
+    """MoBiLE KV decode on the CPU: returns (seconds for `steps` tokens,
+    fallbacks).  `context` > 0: start from a synthetic cache of that many
+    positions instead of prefilling prompt[:-1]."""
     s = W.spec
     dec = R.KVDecoder(W)
-    dec.prefill(list(prompt[:-1]))
+    if context:
+        synthetic_context(dec, context)
+    else:
+        dec.prefill(list(prompt[:-1]))
     last = prompt[-1]
     fallbacks = 0
     t0 = None

@@ -115,3 +115,9 @@ def injected_fallback_flags(n_tokens: int, ratio: float) -> list[bool]:
         raise ValueError(f"fallback ratio outside [0, 1]: {ratio}")
     eps = 1e-9
     return [int((i + 1) * ratio + eps) > int(i * ratio + eps) for i in range(n_tokens)]
+
+
+def build_pregated_plan(*args, **kwargs):
+    """policy.py:119-153 (the modelled pre-gating competitor) is out of scope
+    (DESIGN.md §5): the name exists so `moesim` code importing it loads."""
+    raise NotImplementedError("build_pregated_plan: the pre-gating baseline (policy.py:119-153) is out of scope")

@@ -29,3 +29,6 @@ def cuda_ok():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return True
+
+# the staged reference suite runs only through tests/test_ref_compat.py (moesim alias)
+collect_ignore_glob = ["ref_compat/*"]

@@ -72,3 +72,15 @@ def test_on_demand_plan():
     assert plan.targets[0] == [ExpertId(0, 1)]
     with pytest.raises(ValueError, match="layer 1"):
         on_demand_selection([[ExpertId(0, 0)], []])
+
+
+def test_bench_reference_arm_restates_the_bench_workload():
+    """bench.py --impl reference imports only oracle/: its restated C3 shape
+    and slot count must be the product's (same_config on both arms)."""
+    from oracle import cpu_baseline as CB
+    from paper_2510_12357_b200 import HardwareSpec, hbm_expert_slots
+    from paper_2510_12357_b200.presets import QWEN15_MOE, with_byte_sizes
+    assert CB.C3_SPEC == CB.oracle_spec_from(QWEN15_MOE)
+    for cap, res in ((16, 6), (8, 2)):
+        hw = HardwareSpec(hbm_capacity=cap * 2**30, reserved=res * 2**30)
+        assert CB.c3_slots(cap * 2**30, res * 2**30) == hbm_expert_slots(with_byte_sizes(QWEN15_MOE), hw)
