@@ -256,6 +256,18 @@ int mobile_dense_gemv(const float* x, int T, int d, int do_ln, const void* w, in
                       const float* residual, float* y, void* stream);
 int mobile_attn_decode(const float* qkv, float* k_cache, float* v_cache, const int* pos, int B, int d,
                        int H, int max_len, float* out, void* stream);
+/* Split-KV variant (few (sequence, head) pairs on a long cache): positions are
+ * split over ~2 x SMs CTAs, each writes its (m, s, o) partial into the CALLER-
+ * OWNED workspace `ws` and takes a ticket; the (sequence, head)'s last split
+ * merges the partials in split order (deterministic).  mobile_attn_split_ws
+ * returns the sizes (0 = no split for this shape); tickets must be zeroed once
+ * and are left zero by every launch.  One workspace per concurrently running
+ * caller (stream / captured graph).  Without a workspace (or too small) the
+ * kernel runs unsplit.  mobile_attn_decode = mobile_attn_decode_ws without one. */
+int mobile_attn_split_ws(int B, int d, int H, int max_len, int* ws_floats, int* n_tickets);
+int mobile_attn_decode_ws(const float* qkv, float* k_cache, float* v_cache, const int* pos, int B, int d,
+                          int H, int max_len, float* out, float* ws, unsigned* tickets, int ws_floats,
+                          int n_tickets, void* stream);
 int mobile_embed(const int* tok, const int* pos, const float* embed, const float* pe, int B, int d, float* x,
                  float* ln_out, void* stream);
 int mobile_advance(int* pos, int B, int* tok, const int* next_tok, void* stream);

@@ -105,6 +105,8 @@ _SIGS = {
     "mobile_stream_head": ([P, I32, I32, P, I32, I32, F, F, P, P, P, P, P, P], I32),
     "mobile_dense_gemv": ([P, I32, I32, I32, P, I32, I32, P, P, P], I32),
     "mobile_attn_decode": ([P, P, P, P, I32, I32, I32, I32, P, P], I32),
+    "mobile_attn_split_ws": ([I32, I32, I32, I32, P, P], I32),
+    "mobile_attn_decode_ws": ([P, P, P, P, I32, I32, I32, I32, P, P, P, I32, I32, P], I32),
     "mobile_embed": ([P, P, P, P, I32, I32, P, P, P], I32),
     "mobile_advance": ([P, I32, P, P, P], I32),
     "mobile_memcpy_async": ([P, P, SZ, P], I32),

@@ -1103,7 +1103,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
     // full and the consumers wait on a barrier.  Routed units are skipped (their
     // address is only known after routing); it never blocks.
     int pp = first, pu = 0, pj = 0, pl = 0;
-    bool pfresh = true, pdone = false;
+    bool pfresh = true, pdone = P.pf_window < 0;  // < 0: no prefetch cursor at all
     unsigned long long pf_bytes = 0, w_static = 0;  // prefetched / issued-by-W static bytes
     const unsigned long long pf_window = (unsigned long long)P.pf_window;
     auto pf_step = [&]() -> bool {  // one unit; false = nothing left
@@ -1732,8 +1732,10 @@ int mobile_dp_create(const mobile_dp_model* m, mobile_dp** out) {
   P.reuse_gates = m->reuse_gates; P.max_len = m->max_len; P.L = L; P.V = m->V; P.nc_max = nc_max; P.TT = o->TT;
   P.logit_scale = m->logit_scale; P.gamma = m->gamma;
   P.hd = hd; P.npi = kWBytes / (2 * hd * 4);
-  P.pf_window = 0;  // measured: L2 prefetch ahead of the ring slows the pass (latency-bound)
-  if (const char* e = std::getenv("MOBILE_DP_PF_KB")) P.pf_window = std::max(0, std::atoi(e)) * 1024;
+  // measured: an L2 prefetch cursor ahead of (or trailing) the ring slows the
+  // pass (C3 little 2037 -> 1906 us without it); MOBILE_DP_PF_KB >= 0 enables it
+  P.pf_window = -1;
+  if (const char* e = std::getenv("MOBILE_DP_PF_KB")) P.pf_window = std::max(-1, std::atoi(e)) * 1024;
   P.tok = m->tok; P.pos = m->pos; P.embed = m->embed; P.pe = m->pe; P.kc = m->kc; P.vc = m->vc;
   P.q = m->q; P.att = m->att; P.Y = m->Y; P.Ys = m->Ys; P.states = m->states; P.extra = m->extra;
   P.replay = m->replay; P.idx_out = m->idx_out; P.gates_out = m->gates_out; P.active_out = m->active_out;

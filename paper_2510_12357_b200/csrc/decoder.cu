@@ -432,38 +432,33 @@ extern "C" int mobile_dense_gemv(const float* x, int T, int d, int do_ln, const 
   return MOBILE_ERR_UNSUPPORTED;
 }
 
-// split-KV partials + per-(b, h) tickets: one library workspace, grown outside
-// graph capture only (captured launches keep their pointers: never freed)
-static bool attn_split_ws(int floats, int tickets, cudaStream_t stream, float** ws, unsigned** tk) {
-  static std::mutex mu;
-  static float* g_ws = nullptr;
-  static unsigned* g_tk = nullptr;
-  static int g_floats = 0, g_tickets = 0;
-  std::lock_guard<std::mutex> lk(mu);
-  if (floats > g_floats || tickets > g_tickets) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
-    const int nf = std::max(floats, 1 << 20), nt = std::max(tickets, 4096);
-    float* w = nullptr;
-    unsigned* t = nullptr;
-    if (cudaMalloc(&w, (size_t)nf * sizeof(float)) != cudaSuccess) return false;
-    if (cudaMalloc(&t, (size_t)nt * sizeof(unsigned)) != cudaSuccess || cudaMemset(t, 0, (size_t)nt * sizeof(unsigned)) != cudaSuccess) {
-      cudaFree(w);
-      return false;
-    }
-    cudaDeviceSynchronize();
-    g_ws = w;  // the previous buffers stay allocated: graphs captured earlier may point at them
-    g_tk = t;
-    g_floats = nf;
-    g_tickets = nt;
+namespace mobile {
+// split-KV fan-out: ~2 x SMs CTAs when (sequence, head) pairs alone leave SMs
+// idle on a long cache, at least 64 cached positions per split
+static int attn_nsplit(int B, int H, int max_len) {
+  const int bhn = B * H;
+  if (bhn >= sm_count() || max_len < 256) return 1;
+  return std::min(std::min(16, (2 * sm_count() + bhn - 1) / bhn), max_len / 64);
+}
+}  // namespace mobile
+
+extern "C" int mobile_attn_split_ws(int B, int d, int H, int max_len, int* ws_floats, int* n_tickets) {
+  if (B <= 0 || d <= 0 || H <= 0 || d % H || max_len <= 0 || !ws_floats || !n_tickets) {
+    set_error("attn_split_ws: bad shape");
+    return MOBILE_ERR_INVALID;
   }
-  *ws = g_ws;
-  *tk = g_tk;
-  return true;
+  const int hd = d / H, ns = (hd == 64 || hd == 128) ? attn_nsplit(B, H, max_len) : 1;
+  *ws_floats = ns > 1 ? B * H * ns * (hd + 2) : 0;
+  *n_tickets = ns > 1 ? B * H : 0;
+  return MOBILE_OK;
 }
 
-extern "C" int mobile_attn_decode(const float* qkv, float* k_cache, float* v_cache, const int* pos, int B, int d,
-                                  int H, int max_len, float* out, void* stream) {
+// ws / tickets: caller-owned split-KV workspace (mobile_attn_split_ws sizes it;
+// tickets zeroed once, every launch leaves them zero).  One workspace per
+// concurrently running caller (stream / graph): two launches sharing one race.
+extern "C" int mobile_attn_decode_ws(const float* qkv, float* k_cache, float* v_cache, const int* pos, int B, int d,
+                                     int H, int max_len, float* out, float* ws, unsigned* tickets, int ws_floats,
+                                     int n_tickets, void* stream) {
   if (B <= 0 || d <= 0 || H <= 0 || d % H || max_len <= 0) { set_error("attn_decode: bad shape"); return MOBILE_ERR_INVALID; }
   const int hd = d / H;
   if ((hd == 64 || hd == 128) && (d & 3) == 0) {
@@ -471,21 +466,23 @@ extern "C" int mobile_attn_decode(const float* qkv, float* k_cache, float* v_cac
     if (vsmem > 160 * 1024) { set_error("attn_decode: max_len=%d too long", max_len); return MOBILE_ERR_UNSUPPORTED; }
     auto kern = hd == 64 ? attn_decode_vec_kernel<64> : attn_decode_vec_kernel<128>;
     if (int st = set_smem_once((const void*)kern, vsmem)) return st;
-    // split-KV when (sequence, head) pairs alone leave SMs idle on a long cache
-    int nsplit = 1;
+    int nsplit = attn_nsplit(B, H, max_len);
     const int bhn = B * H;
-    if (bhn < sm_count() && max_len >= 256) nsplit = std::min(std::min(16, (2 * sm_count() + bhn - 1) / bhn), max_len / 64);
-    float* ws = nullptr;
-    unsigned* tk = nullptr;
-    if (nsplit > 1 && !attn_split_ws(bhn * nsplit * (hd + 2), bhn, (cudaStream_t)stream, &ws, &tk)) nsplit = 1;
+    if (nsplit > 1 && (!ws || !tickets || ws_floats < bhn * nsplit * (hd + 2) || n_tickets < bhn)) nsplit = 1;
     return launch_pdl(kern, dim3(bhn * nsplit), dim3(kAttnThreads), vsmem, (cudaStream_t)stream, 1, "attn_decode", qkv,
-                      k_cache, v_cache, pos, d, H, max_len, out, nsplit, ws, tk);
+                      k_cache, v_cache, pos, d, H, max_len, out, nsplit, nsplit > 1 ? ws : nullptr,
+                      nsplit > 1 ? tickets : nullptr);
   }
   const size_t smem = sizeof(float) * ((size_t)max_len + d / H);
   if (smem > 200 * 1024) { set_error("attn_decode: max_len=%d too long", max_len); return MOBILE_ERR_UNSUPPORTED; }
   set_smem_once((const void*)attn_decode_kernel, smem);
   return launch_pdl(attn_decode_kernel, dim3(B * H), dim3(128), smem, (cudaStream_t)stream, 1, "attn_decode", qkv,
                     k_cache, v_cache, pos, d, H, max_len, out);
+}
+
+extern "C" int mobile_attn_decode(const float* qkv, float* k_cache, float* v_cache, const int* pos, int B, int d,
+                                  int H, int max_len, float* out, void* stream) {
+  return mobile_attn_decode_ws(qkv, k_cache, v_cache, pos, B, d, H, max_len, out, nullptr, nullptr, 0, 0, stream);
 }
 
 extern "C" int mobile_embed(const int* tok, const int* pos, const float* embed, const float* pe, int B, int d,

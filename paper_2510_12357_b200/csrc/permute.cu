@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(1024) combine_kernel(const float* __restrict__
   pdl_trigger();
   pdl_wait();
   const int kt = k_tok ? k_tok[t] : k_max;
-  if (threadIdx.x < kt) sg[threadIdx.x] = gates[(size_t)t * k_max + threadIdx.x];
+  if (threadIdx.x < kt && threadIdx.x < 8) sg[threadIdx.x] = gates[(size_t)t * k_max + threadIdx.x];  // later gates: global
   if (threadIdx.x < n_shared)
     sg[8 + threadIdx.x] = shared_logits ? sigmoid_f(shared_logits[(size_t)t * n_shared + threadIdx.x]) : 1.0f;
   __syncthreads();

@@ -204,15 +204,29 @@ def dense_gemv(x, w, *, do_ln=False, residual=None, out=None, stream=None):
     return out
 
 
-def attn_decode(qkv, k_cache, v_cache, pos, n_heads, out=None, stream=None):
+def attn_split_workspace(B, d, n_heads, max_len, device):
+    """Caller-owned split-KV workspace for attn_decode (decoder.cu): (partials,
+    tickets) sized by mobile_attn_split_ws, or None when the shape runs unsplit.
+    One per concurrently running caller (engine stream / captured graph)."""
+    import ctypes
+    nf, nt = ctypes.c_int(0), ctypes.c_int(0)
+    N.check(N.lib.mobile_attn_split_ws(B, d, n_heads, max_len, ctypes.byref(nf), ctypes.byref(nt)), "attn_split_ws")
+    if nf.value == 0:
+        return None
+    return (torch.empty(nf.value, dtype=torch.float32, device=device),
+            torch.zeros(nt.value, dtype=torch.int32, device=device))
+
+
+def attn_decode(qkv, k_cache, v_cache, pos, n_heads, out=None, stream=None, ws=None):
     B, d3 = qkv.shape
     d = d3 // 3
     max_len = k_cache.shape[2]  # head-major (B, H, max_len, head_dim)
     if out is None:
         out = torch.empty(B, d, device=qkv.device, dtype=torch.float32)
     _count()
-    N.check(N.lib.mobile_attn_decode(N.ptr(qkv), N.ptr(k_cache), N.ptr(v_cache), N.ptr(pos), B, d, n_heads, max_len,
-                                     N.ptr(out), _s(stream)), "attn_decode")
+    wp, tp, nf, nt = (N.ptr(ws[0]), N.ptr(ws[1]), ws[0].numel(), ws[1].numel()) if ws is not None else (None, None, 0, 0)
+    N.check(N.lib.mobile_attn_decode_ws(N.ptr(qkv), N.ptr(k_cache), N.ptr(v_cache), N.ptr(pos), B, d, n_heads,
+                                        max_len, N.ptr(out), wp, tp, nf, nt, _s(stream)), "attn_decode")
     return out
 
 

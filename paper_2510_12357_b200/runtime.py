@@ -82,6 +82,8 @@ class StepEngine:
         self.qkv = torch.empty(B, 3 * d, dtype=f32, device=dev)
         self.att = torch.empty(B, d, dtype=f32, device=dev)
         self.xa = torch.empty(B, d, dtype=f32, device=dev)
+        # this engine's own split-KV workspace (its stream and graphs only)
+        self.attn_ws = K.attn_split_workspace(B, d, s.n_heads, max_len, dev)
         self.k = {"little": s.k_little, "big": s.k_big, "full": s.k_big}
         self.k_tok = {kd: torch.full((B,), self.k[kd], dtype=i32, device=dev) for kd in KINDS}
         # zero-initialised: the graph warm-up replays states["little"] before any real pass
@@ -123,7 +125,7 @@ class StepEngine:
         wc = self.dm.moe.wcode
         K.stream_gemv([K.sg_group(w_base=dw.qkv[l].data_ptr(), K=d, rows=3 * d, x=self.ln, dense_T=B,
                                   out=self.qkv)], wc, B)
-        K.attn_decode(self.qkv, self.sess.kc[l], self.sess.vc[l], self.pos, s.n_heads, out=self.att)
+        K.attn_decode(self.qkv, self.sess.kc[l], self.sess.vc[l], self.pos, s.n_heads, out=self.att, ws=self.attn_ws)
         K.stream_gemv([K.sg_group(w_base=dw.o[l].data_ptr(), K=d, rows=d, x=self.att, dense_T=B, out=self.xa,
                                   residual=x_in)], wc, B)
         return self.xa
@@ -141,7 +143,8 @@ class StepEngine:
         dw, d, B = self.dm.dw, self.spec.hidden_dim, self.B
         K.gather_bf16(self.ln, None, 1, B, self.xb)
         self._dense_gemm(dw.qkv[l], 3 * d, self.qkv, K.GG_STORE_F32)
-        K.attn_decode(self.qkv, self.sess.kc[l], self.sess.vc[l], self.pos, self.spec.n_heads, out=self.att)
+        K.attn_decode(self.qkv, self.sess.kc[l], self.sess.vc[l], self.pos, self.spec.n_heads, out=self.att,
+                      ws=self.attn_ws)
         K.gather_bf16(self.att, None, 1, B, self.xb)
         self.xa.copy_(x_in)
         self._dense_gemm(dw.o[l], d, self.xa, K.GG_ACCUM_F32)

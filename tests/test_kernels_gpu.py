@@ -347,17 +347,21 @@ def test_attn_decode_vs_torch(cuda_ok, B, H, hd, max_len, pos):
     p = torch.tensor(pos, dtype=torch.int32, device="cuda")
     kc0, vc0 = kc.clone(), vc.clone()
     out = torch.empty(B, d, device="cuda")
-    for _ in range(2):  # twice: the split tickets must reset
-        kc.copy_(kc0)
-        vc.copy_(vc0)
-        K.attn_decode(qkv, kc, vc, p, H, out=out)
-    torch.cuda.synchronize()
-    for b in range(B):
-        q, k, v = qkv[b, :d].view(H, hd), qkv[b, d:2 * d].view(H, hd), qkv[b, 2 * d:].view(H, hd)
-        kk, vv = kc0[b].clone(), vc0[b].clone()
-        kk[:, pos[b]] = k
-        vv[:, pos[b]] = v
-        assert torch.equal(kc[b, :, pos[b]], k) and torch.equal(vc[b, :, pos[b]], v)
-        sc = torch.einsum("hd,hpd->hp", q.double(), kk[:, :pos[b] + 1].double()) / hd ** 0.5
-        want = torch.einsum("hp,hpd->hd", torch.softmax(sc, dim=-1), vv[:, :pos[b] + 1].double()).reshape(d)
-        assert torch.allclose(out[b].double(), want, rtol=1e-4, atol=1e-5), (b, (out[b].double() - want).abs().max())
+    ws = K.attn_split_workspace(B, d, H, max_len, torch.device("cuda"))
+    for w in (ws, None):  # the split path (caller-owned workspace) and the unsplit one
+        for _ in range(2):  # twice: the split tickets must reset
+            kc.copy_(kc0)
+            vc.copy_(vc0)
+            K.attn_decode(qkv, kc, vc, p, H, out=out, ws=w)
+        torch.cuda.synchronize()
+        if w is not None:
+            assert int(w[1].abs().sum()) == 0
+        for b in range(B):
+            q, k, v = qkv[b, :d].view(H, hd), qkv[b, d:2 * d].view(H, hd), qkv[b, 2 * d:].view(H, hd)
+            kk, vv = kc0[b].clone(), vc0[b].clone()
+            kk[:, pos[b]] = k
+            vv[:, pos[b]] = v
+            assert torch.equal(kc[b, :, pos[b]], k) and torch.equal(vc[b, :, pos[b]], v)
+            sc = torch.einsum("hd,hpd->hp", q.double(), kk[:, :pos[b] + 1].double()) / hd ** 0.5
+            want = torch.einsum("hp,hpd->hd", torch.softmax(sc, dim=-1), vv[:, :pos[b] + 1].double()).reshape(d)
+            assert torch.allclose(out[b].double(), want, rtol=1e-4, atol=1e-5), (b, (out[b].double() - want).abs().max())
