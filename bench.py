@@ -56,6 +56,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=0, help="CPU-baseline tokens (default: --steps)")
     ap.add_argument("--layers", type=int, default=0, help="debug only: fewer layers (invalidates the number)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config (C2/C4/C5) block")
+    ap.add_argument("--no-ep", action="store_true", help="skip the expert-parallel (C4 batched) block")
+    ap.add_argument("--ep-batch", type=int, default=64, help="sequences per rank in the expert-parallel block")
+    ap.add_argument("--configs", default="c1,c2,c4,c5", help="configs of the per-config block")
     return ap.parse_args()
 
 
@@ -205,11 +209,13 @@ def run_ours(args, ws, rank, local):
         eng = StepEngine(dm, 1, max_len, runtime=rt, graphs=graphs, persistent=persistent).build(gamma=policy.gamma)
         return rt, eng
 
-    def timed_decode(full: bool):
+    def timed_decode(full: bool, natural: bool = False):
+        """natural: the confidence rule decides the fallbacks (policy.py:69-79)
+        instead of the injected flags"""
         rt, eng = make_engine()
         eng.prefill(prompt)
         for i in range(W_):
-            eng.step(flags[i], full=full, next_token=stream[i])
+            eng.step(None if natural else flags[i], full=full, next_token=stream[i])
         torch.cuda.synchronize()
         barrier(ws)
         launches0 = K.LAUNCHES[0]
@@ -222,7 +228,7 @@ def run_ours(args, ws, rank, local):
             w0 = time.perf_counter()
             fb = 0
             for i in range(W_, W_ + K_):
-                _, f = eng.step(flags[i], full=full, next_token=stream[i])
+                _, f = eng.step(None if natural else flags[i], full=full, next_token=stream[i])
                 fb += f
             ev1.record(eng.stream)
             torch.cuda.synchronize()
@@ -241,6 +247,7 @@ def run_ours(args, ws, rank, local):
 
     mob = timed_decode(full=False)
     base = timed_decode(full=True)
+    nat = timed_decode(full=False, natural=True)
 
     # isolated PCIe H2D peak (pinned, 1 GiB) for the copy-engine roofline
     hbuf = torch.empty(2**30, dtype=torch.uint8, pin_memory=True)
@@ -278,6 +285,7 @@ def run_ours(args, ws, rank, local):
 
     dev_s = max_over_ranks(ws, mob["dev_s"], dev)
     base_s = max_over_ranks(ws, base["dev_s"], dev)
+    nat_s = max_over_ranks(ws, nat["dev_s"], dev)
     e2e_s = max_over_ranks(ws, e2e_s, dev)
     wall_s = max_over_ranks(ws, mob["wall_s"], dev)
     value = ws * K_ / dev_s
@@ -285,6 +293,12 @@ def run_ours(args, ws, rank, local):
 
     P = peaks()
     achieved = roof["little"]["gbs"]
+    ep = None
+    if not args.no_ep:
+        ep = ep_block(args, ws, rank, dev, P)
+    per_config = None
+    if rank == 0 and not args.no_configs:
+        per_config = config_sweep(args, dev, P)
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -301,6 +315,13 @@ def run_ours(args, ws, rank, local):
                                    "ms_per_step": round(base_s / K_ * 1e3, 3), "h2d_bytes": base["h2d_bytes"],
                                    "cache_hits": base["hits"], "transfers": base["transfers"]},
             "speedup_vs_full_topk": round(value / base_value, 4),
+            "mobile_natural_r": {"value": round(ws * K_ / nat_s, 3),
+                                 "unit": "tokens/s", "fallbacks": nat["fallbacks"],
+                                 "r_observed": round(nat["fallbacks"] / K_, 4),
+                                 "speedup_vs_full_topk": round(base_s / nat_s, 4),
+                                 "note": "same decode with the fallbacks decided by the confidence rule "
+                                         "(max p <= gamma = 0.7) on random-init weights instead of the injected "
+                                         "paper ratio"},
             "mobile": {"fallbacks": mob["fallbacks"], "h2d_bytes": mob["h2d_bytes"], "transfers": mob["transfers"],
                        "cache_hits": mob["hits"], "cache_coalesced": mob["coalesced"],
                        "wall_ms_per_step": round(mob["wall_s"] / K_ * 1e3, 3)},
@@ -324,6 +345,8 @@ def run_ours(args, ws, rank, local):
             "e2e_incl_prefill": {"value": round(K_ / e2e_s * ws, 3), "unit": "tokens/s",
                                  "note": "wall clock of StepEngine.decode(prompt host list, K) on a cold expert "
                                          "cache, incl. the %d-token prefill" % args.prompt_len},
+            "ep": ep,
+            "configs": per_config,
             "gpu_launches": mob["launches"] + mob["graph_kernels"] * (K_ + mob["fallbacks"]),
             "clocks": mob["clocks"],
             "init_s": round(t_init, 1),
@@ -405,6 +428,267 @@ def cpu_leg(args, steps, warmup):
             "sample": f"{steps} decode tokens ({fb} fallback, injected r={args.r}) of the same Qwen shape after "
                       f"{warmup} warm-up tokens, context {args.prompt_len} (synthetic KV cache), fp32 NumPy oracle "
                       f"KVDecoder on {n_cores} threads; expert/attention matrices aliased to pools > LLC"}
+
+
+# ----------------------------------------------------------------------------- expert parallelism
+def ep_block(args, ws, rank, dev, P):
+    """BASELINE.json C4 (DeepSeek-MoE-16B shape) batched decode, EXPERT-
+    PARALLEL over the ws ranks of this launch (ep.EPStepEngine): routed
+    experts in contiguous blocks per rank (64 / ws), everything else
+    replicated, each rank decoding its own --ep-batch sequences at context
+    512; rows exchanged every layer through IPC-mapped peer mailboxes
+    (NVLink on a multi-GPU node; at ws = 1 through the rank's own mailbox).
+    Pass times are graph replays timed with CUDA events on the engine stream
+    (10 each, max over ranks); the exchange legs (dispatch + wait, owner
+    experts, return + collect) come from one eager pass with CUDA events
+    around each leg.  tokens/s is the whole job: ws x batch per step."""
+    import math
+
+    import torch
+
+    from paper_2510_12357_b200.ep import EPStepEngine, ExchangeTimer, partition
+    from paper_2510_12357_b200.model import DeviceModel, MoBiLEMoE
+    from paper_2510_12357_b200.presets import DEEPSEEK_MOE_16B as spec
+    from paper_2510_12357_b200.weights import DeviceWeights
+
+    B, ctx, r = args.ep_batch, 512, 0.11
+    group = None
+    dw = DeviceWeights.random(spec, dev, seed=0)
+    dm = DeviceModel(dw)
+    lo, hi = partition(spec.num_experts, ws)[rank]
+    local = MoBiLEMoE(dw.shard_experts(lo, hi))
+    eng = EPStepEngine(dm, local, B, ctx + 48, group=group).build()
+    g = torch.Generator(device=dev).manual_seed(100 + rank)
+    eng.sess.kc.normal_(generator=g)
+    eng.sess.vc.normal_(generator=g)
+    eng.pos.fill_(ctx)
+    eng.tok.copy_(torch.randint(1, spec.vocab_size, (B,), device=dev, dtype=torch.int32, generator=g))
+    for kd in ("little", "big", "full"):
+        eng.graphs[kd].replay()
+    torch.cuda.synchronize()
+
+    def time_pass(kd, reps=10):
+        barrier(ws)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(eng.stream):
+            e0.record()
+            for _ in range(reps):
+                eng.graphs[kd].replay()
+            e1.record()
+        torch.cuda.synchronize()
+        return max_over_ranks(ws, e0.elapsed_time(e1) / reps, dev)
+
+    ms = {kd: time_pass(kd) for kd in ("little", "big", "full")}
+    # exchange legs: one eager little pass with events around every leg
+    eng.use_graphs, eng.ex_timer = False, ExchangeTimer()
+    barrier(ws)
+    with torch.cuda.stream(eng.stream):
+        eng._whole_pass("little")
+    legs = eng.ex_timer.summary_ms()
+    eng.use_graphs, eng.ex_timer = True, None
+    legs = {k: (round(max_over_ranks(ws, v, dev), 3) if k != "exchanges" else v) for k, v in legs.items()}
+    p_any = 1.0 - (1.0 - r) ** B
+    t_mob = ms["little"] + p_any * ms["big"]  # conservative: the big pass over the whole batch
+    eng.close()
+    del eng, local, dm, dw
+    torch.cuda.empty_cache()
+    return {"workload": f"C4 DeepSeek-MoE-16B shape, batched decode, {B} sequences per rank, context {ctx}, "
+                        f"expert-parallel over {ws} rank(s) (experts {lo}-{hi - 1} on rank {rank})",
+            "parallelism": f"ep{ws}", "batch_per_rank": B, "n_gpus": ws,
+            "pass_ms": {k: round(v, 3) for k, v in ms.items()},
+            "mobile_tokens_s": round(ws * B / t_mob * 1e3, 1),
+            "full_topk_tokens_s": round(ws * B / ms["full"] * 1e3, 1),
+            "speedup_vs_full_topk": round(ms["full"] / t_mob, 4), "r": r, "p_any_fallback": round(p_any, 4),
+            "exchange_ms_per_little_pass": legs,
+            "note": "pass times max over ranks; MoBiLE = little + P(any row falls back) x big (whole-batch replay); "
+                    "exchange legs from an eager pass (CUDA events on the engine stream)"}
+
+
+# ----------------------------------------------------------------------------- other configs
+R_PAPER = {"c2": 0.21, "c3": 0.11, "c4": 0.11, "c5": 0.11}  # PAPER.md: OLMoE 0.21, Qwen 0.11
+CTX = {"c2": 512, "c3": 512, "c4": 512, "c5": 2048}
+BATCHES = {"c2": (1,), "c4": (1, 64), "c5": (1,)}
+
+
+def config_sweep(args, dev, P):
+    """BASELINE.json configs C2 / C4 / C5 at 1 GPU, experts HBM-resident,
+    random-init bf16 weights: decode passes (little / replayed big / full
+    top-k; graph replays timed with CUDA events on the engine stream, 10
+    replays each, inputs >> L2) as MoBiLE tokens/s at the paper's fallback
+    ratio vs full-top-k tokens/s, each pass's HBM roofline fraction; C5 also a
+    2048-token prefill with its expert GEMMs' tensor roofline fraction; and the
+    oracle port's decode on the host cores beside each (CPU legs import
+    oracle/ only)."""
+    import math
+    import numpy as np
+    import torch
+
+    from paper_2510_12357_b200.model import DeviceModel
+    from paper_2510_12357_b200.presets import NAMES, PRESETS
+    from paper_2510_12357_b200.runtime import StepEngine
+    from paper_2510_12357_b200.weights import DeviceWeights
+
+    hbm, tens = P.get("hbm_gbs", 6543.1), P.get("bf16_tflops", 1403.0)
+    out = {}
+    for name in [c for c in args.configs.split(",") if c]:
+        if name == "c1":
+            out[name] = c1_line()
+            continue
+        spec = PRESETS[name]
+        t0 = time.time()
+        dw = DeviceWeights.random(spec, dev, seed=0)
+        dm = DeviceModel(dw)
+        ctx, r = CTX[name], R_PAPER[name]
+        res = {"model": NAMES[name], "context": ctx, "r": r, "decode": {}}
+        eb, d, L = dw.elem_bytes, spec.hidden_dim, spec.num_layers
+
+        def pass_bytes(k, B):
+            experts = min(spec.num_experts, B * k) * dw.expert_bytes
+            per_layer = (4 * d * d + (spec.num_experts + dw.n_gate_rows) * d) * eb + experts \
+                + spec.n_shared * dw.shared_bytes + B * 2 * ctx * d * 4
+            return L * per_layer + spec.vocab_size * d * eb
+
+        def engine(B):
+            e = StepEngine(dm, B, ctx + 48).build()
+            e.sess.kc.normal_()
+            e.sess.vc.normal_()
+            e.pos.fill_(ctx)
+            e.tok.copy_(torch.randint(1, spec.vocab_size, (B,), device=dev, dtype=torch.int32))
+            for kd in ("little", "big", "full"):
+                e.graphs[kd].replay()
+            torch.cuda.synchronize()
+            return e
+
+        def time_pass(e, kd, reps=10):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(e.stream):
+                e0.record()
+                for _ in range(reps):
+                    e.graphs[kd].replay()
+                e1.record()
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / reps / 1e3
+
+        for B in BATCHES[name]:
+            eng = engine(B)
+            row = {"engine": "gemm" if eng.gemm_path else ("persistent" if eng.dp else "per-op")}
+            for kd in ("little", "big", "full"):
+                t = time_pass(eng, kd)
+                nb = pass_bytes(eng.k[kd], B)
+                row[kd] = {"ms": round(t * 1e3, 3), "bytes": nb, "gbs": round(nb / t / 1e9, 1),
+                           "hbm_frac": round(nb / t / 1e9 / hbm, 4)}
+            del eng
+            torch.cuda.empty_cache()
+            # batched MoBiLE: the big pass replays only the rows that fell back
+            p_any = 1.0 - (1.0 - r) ** B
+            b_fb = max(1, math.ceil(r * B / p_any - 1e-9))
+            if b_fb == B:
+                t_big = row["big"]["ms"]
+            else:
+                e2 = engine(b_fb)
+                t_big = round(time_pass(e2, "big") * 1e3, 3)
+                del e2
+                torch.cuda.empty_cache()
+            t_mob = row["little"]["ms"] + p_any * t_big
+            row.update({"big_rows": b_fb, "big_rows_ms": t_big, "p_any_fallback": round(p_any, 4),
+                        "mobile_tokens_s": round(B * 1e3 / t_mob, 2),
+                        "full_topk_tokens_s": round(B * 1e3 / row["full"]["ms"], 2),
+                        "speedup_vs_full_topk": round(row["full"]["ms"] / t_mob, 4)})
+            res["decode"][f"B{B}"] = row
+        if name == "c5":  # 2k-token prefill (per-op engine: attention + tcgen05 grouped-GEMM experts)
+            pe = StepEngine(dm, 1, ctx + 8, persistent=False)
+            prompt = np.random.default_rng(1).integers(1, spec.vocab_size, size=ctx).tolist()
+            pe.prefill(prompt)
+            torch.cuda.synchronize()
+            w0 = time.perf_counter()
+            pe.prefill(prompt)
+            torch.cuda.synchronize()
+            tp = time.perf_counter() - w0
+            I = spec.ffn
+            flops = 2.0 * ctx * L * spec.k_big * 3 * d * I
+            res["prefill"] = {"tokens": ctx, "ms": round(tp * 1e3, 2), "tokens_s": round(ctx / tp, 1),
+                              "expert_gemm_tflop": round(flops / 1e12, 2),
+                              "roofline": {"bound": "tensor", "achieved": round(flops / tp / 1e12, 1),
+                                           "peak": tens, "unit": "TFLOP/s", "frac": round(flops / tp / 1e12 / tens, 4),
+                                           "note": "expert GEMM FLOPs / whole-prefill wall time (attention, "
+                                                   "projections and routing included in the time)"}}
+            del pe
+        res["init_s"] = round(time.time() - t0, 1)
+        del dm, dw
+        torch.cuda.empty_cache()
+        if not args.no_cpu_baseline:
+            res["cpu_baseline"] = cpu_config_leg(name, r)
+        out[name] = res
+    return out
+
+
+def c1_line(n_tokens=24):
+    """C1 (the reference's own tiny config, configs[0]): the UNMODIFIED
+    reference `moesim.toymoe.generate` (toymoe.py:246-303, staged into
+    oracle/_ref by oracle/stage_ref.py) on the host cores next to this
+    package's drop-in `generate` on the GPU, identical spec / prompt / policy;
+    tokens and accept/fallback decisions must be identical."""
+    import sys as _sys
+
+    ref_dir = ROOT / "oracle" / "_ref"
+    if not (ref_dir / "moesim" / "toymoe.py").is_file():
+        return {"unavailable": "oracle/_ref not staged (python oracle/stage_ref.py in the build container)"}
+    _sys.path.insert(0, str(ref_dir))
+    try:
+        import moesim.config as RC
+        import moesim.toymoe as RT
+    finally:
+        _sys.path.remove(str(ref_dir))
+    import paper_2510_12357_b200 as M
+    import torch
+
+    kw = dict(num_layers=2, num_experts=16, k_big=4, k_little=2, hidden_dim=256, vocab_size=256, seed=0)
+    prompt = [3, 17, 42, 5]
+    rm = RT.build_model(RC.ModelSpec(**kw))
+    RT.generate(rm, prompt, RC.PolicySpec(), 2)  # warm-up
+    w0 = time.perf_counter()
+    rt, rd = RT.generate(rm, prompt, RC.PolicySpec(), n_tokens)
+    t_ref = time.perf_counter() - w0
+    om = M.build_model(M.ModelSpec(**kw))
+    M.generate(om, prompt, M.PolicySpec(), 2)  # warm-up
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    ot, od = M.generate(om, prompt, M.PolicySpec(), n_tokens)
+    torch.cuda.synchronize()
+    t_ours = time.perf_counter() - w0
+    same = ot == rt and [d.accepted_by for d in od] == [d.accepted_by for d in rd] and \
+        [d.little_selections for d in od] == [d.little_selections for d in rd]
+    n = len(rd)
+    return {"model": "tiny (SPEC.md): L2 E16 K4 k2 d256 V256, fp64 reference", "tokens": n, "prompt": len(prompt),
+            "reference": {"value": round(n / t_ref, 2), "unit": "tokens/s", "impl": "moesim.toymoe.generate "
+                          "(unmodified, oracle/_ref)", "cores": os.cpu_count() or 1},
+            "ours": {"value": round(n / t_ours, 2), "unit": "tokens/s",
+                     "impl": "paper_2510_12357_b200.generate (drop-in API, libmobile kernels)"},
+            "fallbacks": sum(d.accepted_by != "Little" for d in rd),
+            "identical_tokens_and_decisions": bool(same),
+            "note": "wall clock of generate(prompt, max_len) on both sides; the reference recomputes the whole "
+                    "prefix per token (no KV cache) and so does the drop-in API"}
+
+
+def cpu_config_leg(name, r, steps=2, warmup=1):
+    """The oracle port's KV decode of config `name` on the host cores (oracle/
+    only; matrices aliased to pools larger than the LLC, bounded RAM)."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+
+    from oracle import cpu_baseline as CB
+    from oracle import moe_ref as R
+    spec = CB.SPECS[name]
+    W = CB.aliased_weights(spec, expert_pool=4 if name == "c5" else 64)
+    flags = R.injected_fallback_flags(warmup + steps, r)
+    n_cores = os.cpu_count() or 1
+    with threadpool_limits(limits=n_cores):
+        secs, fb = CB.time_decode(W, [1], flags, warmup, steps, context=CTX[name])
+    return {"value": round(steps / secs, 4), "unit": "tokens/s", "cores": n_cores, "kind": "port",
+            "sample": f"{steps} decode tokens ({fb} fallback, injected r={r}) after {warmup} warm-up, context "
+                      f"{CTX[name]} (synthetic KV cache), fp32 NumPy oracle KVDecoder"}
 
 
 # ----------------------------------------------------------------------------- reference arm

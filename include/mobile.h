@@ -281,7 +281,10 @@ int mobile_memcpy_async(void* dst, const void* src, size_t bytes, void* stream);
  * rank owns a mailbox (mobile_ep_mailbox_create) whose CUDA IPC handle is
  * exchanged once (mobile_ep_ipc_handle / _open); peers_dev is a device array
  * of the G mailboxes as mapped in this process (this rank's own at [rank]).
- * Per layer, with an epoch the caller increments per exchange:
+ * Per layer, with an epoch that advances per exchange: the effective epoch is
+ * `epoch` + *epoch_dev when epoch_dev is non-NULL -- a device counter bumped
+ * by mobile_ep_advance at the start of each exchange, so a CUDA graph of the
+ * exchange replays correctly (every rank runs every exchange, in lockstep):
  *   home : mobile_ep_dispatch  -- plan (stable per-owner positions, dest_pos
  *          (T*k_max) scratch, counts (G) scratch), row stores into the
  *          owners' mailboxes, counts + release flag (system scope)
@@ -301,11 +304,12 @@ int mobile_ep_ipc_open(const void* handle64, void** ptr);
 int mobile_ep_ipc_close(void* ptr);
 int mobile_ep_dispatch(const float* rows, const int* idx, const int* k_tok, int T, int k_max, int d, const int* owner,
                        const int* local_id, void* const* peers_dev, int G, int rank, int cap, unsigned epoch,
-                       int* dest_pos, int* counts, int* flags, void* stream);
-int mobile_ep_wait(void* mailbox, int G, int cap, int d, int which, unsigned epoch, int* k_tok_out, int* flags,
-                   void* stream);
+                       const unsigned* epoch_dev, int* dest_pos, int* counts, int* flags, void* stream);
+int mobile_ep_wait(void* mailbox, int G, int cap, int d, int which, unsigned epoch, const unsigned* epoch_dev,
+                   int* k_tok_out, int* flags, void* stream);
 int mobile_ep_return(const float* out_rows, const void* mailbox, void* const* peers_dev, int G, int rank, int cap,
-                     int d, unsigned epoch, void* stream);
+                     int d, unsigned epoch, const unsigned* epoch_dev, void* stream);
+int mobile_ep_advance(unsigned* epoch_dev, void* stream);
 int mobile_ep_collect(const void* mailbox, const int* dest_pos, int P, int G, int cap, int d, float* Y, void* stream);
 
 /* ---- expert cache core (memory.py:65-181 semantics) ----------------------

@@ -84,6 +84,18 @@ C3_SPEC = R.OracleSpec(num_layers=24, num_experts=60, k_big=4, k_little=2, hidde
                        n_heads=16, embed_scale=1.0, pos_encoding="none")
 
 
+# The other BASELINE.json configs on the oracle side (presets.py OLMOE /
+# DEEPSEEK_MOE_16B / MIXTRAL_8X7B), for bench.py's per-config CPU legs.
+C2_SPEC = R.OracleSpec(num_layers=16, num_experts=64, k_big=8, k_little=4, hidden_dim=2048, vocab_size=50304,
+                       ffn_dim=1024, activation="swiglu", n_heads=16, embed_scale=1.0, pos_encoding="none")
+C4_SPEC = R.OracleSpec(num_layers=27, num_experts=64, k_big=6, k_little=3, hidden_dim=2048, vocab_size=102400,
+                       ffn_dim=1408, activation="swiglu", n_shared=2, shared_ffn_dim=1408, n_heads=16,
+                       embed_scale=1.0, pos_encoding="none")
+C5_SPEC = R.OracleSpec(num_layers=32, num_experts=8, k_big=2, k_little=1, hidden_dim=4096, vocab_size=32000,
+                       ffn_dim=14336, activation="swiglu", n_heads=32, embed_scale=1.0, pos_encoding="none")
+SPECS = {"c2": C2_SPEC, "c3": C3_SPEC, "c4": C4_SPEC, "c5": C5_SPEC}
+
+
 def c3_slots(cap_bytes: int, reserved_bytes: int, spec: R.OracleSpec = C3_SPEC) -> int:
     """hbm_expert_slots (config.py:204-218) on the bf16 device sizes of `spec`
     (expert = 3 d I, dense/layer = qkv+o + router + shared + shared gate)."""

@@ -94,9 +94,10 @@ _SIGS = {
     "mobile_ep_ipc_handle": ([P, P], I32),
     "mobile_ep_ipc_open": ([P, P], I32),
     "mobile_ep_ipc_close": ([P], I32),
-    "mobile_ep_dispatch": ([P, P, P, I32, I32, I32, P, P, P, I32, I32, I32, C.c_uint, P, P, P, P], I32),
-    "mobile_ep_wait": ([P, I32, I32, I32, I32, C.c_uint, P, P, P], I32),
-    "mobile_ep_return": ([P, P, P, I32, I32, I32, I32, C.c_uint, P], I32),
+    "mobile_ep_dispatch": ([P, P, P, I32, I32, I32, P, P, P, I32, I32, I32, C.c_uint, P, P, P, P, P], I32),
+    "mobile_ep_wait": ([P, I32, I32, I32, I32, C.c_uint, P, P, P, P], I32),
+    "mobile_ep_return": ([P, P, P, I32, I32, I32, I32, C.c_uint, P, P], I32),
+    "mobile_ep_advance": ([P, P], I32),
     "mobile_ep_collect": ([P, P, I32, I32, I32, I32, P, P], I32),
     "mobile_stream_gemv": ([P, I32, I32, I32, P], I32),
     "mobile_stream_head_ws_bytes": ([], SZ),

@@ -137,9 +137,10 @@ __global__ void ep_send_kernel(const float* __restrict__ rows, const int* __rest
 
 // 3. counts, then the epoch flag, into every owner's mailbox
 __global__ void ep_post_kernel(const int* __restrict__ counts, void* const* __restrict__ peers, int rank, int G, int cap,
-                               int d, unsigned epoch) {
+                               int d, unsigned epoch, const unsigned* epoch_dev) {
   pdl_trigger();
   pdl_wait();
+  if (epoch_dev) epoch += *epoch_dev;
   const int g = threadIdx.x;
   if (g >= G) return;
   const Box b = layout(G, cap, d);
@@ -152,9 +153,10 @@ __global__ void ep_post_kernel(const int* __restrict__ counts, void* const* __re
 // 4. wait until every source posted this epoch; owner side also derives the
 //    per-row validity (k_tok = 1 for rows below the source's count)
 __global__ void ep_wait_kernel(void* mailbox, int G, int cap, int d, int which, unsigned epoch, int* k_tok_out,
-                               int* flags) {
+                               int* flags, const unsigned* epoch_dev) {
   pdl_trigger();
   pdl_wait();
+  if (epoch_dev) epoch += *epoch_dev;
   const Box b = layout(G, cap, d);
   char* box = reinterpret_cast<char*>(mailbox);
   const unsigned* fl = reinterpret_cast<const unsigned*>(box + (which == 0 ? b.in_flag : b.back_flag));
@@ -196,14 +198,25 @@ __global__ void ep_return_kernel(const float* __restrict__ out_rows, const void*
   __threadfence_system();
 }
 
-__global__ void ep_post_back_kernel(void* const* __restrict__ peers, int rank, int G, int cap, int d, unsigned epoch) {
+__global__ void ep_post_back_kernel(void* const* __restrict__ peers, int rank, int G, int cap, int d, unsigned epoch,
+                                    const unsigned* epoch_dev) {
   pdl_trigger();
   pdl_wait();
+  if (epoch_dev) epoch += *epoch_dev;
   const int s = threadIdx.x;
   if (s >= G) return;
   const Box b = layout(G, cap, d);
   __threadfence_system();
   st_release_sys_u32(reinterpret_cast<unsigned*>(reinterpret_cast<char*>(peers[s]) + b.back_flag) + rank, epoch);
+}
+
+// graph-replayable exchanges: the epoch lives in device memory, advanced by
+// one kernel at the start of every exchange (ranks advance in lockstep: every
+// rank runs every exchange)
+__global__ void ep_advance_kernel(unsigned* epoch_dev) {
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0) *epoch_dev += 1u;
 }
 
 // 6. home: Y[p] = the owner's output row of pair p (zero for unselected slots)
@@ -271,7 +284,8 @@ extern "C" int mobile_ep_ipc_close(void* ptr) {
 
 extern "C" int mobile_ep_dispatch(const float* rows, const int* idx, const int* k_tok, int T, int k_max, int d,
                                   const int* owner, const int* local_id, void* const* peers_dev, int G, int rank, int cap,
-                                  unsigned epoch, int* dest_pos, int* counts, int* flags, void* stream) {
+                                  unsigned epoch, const unsigned* epoch_dev, int* dest_pos, int* counts, int* flags,
+                                  void* stream) {
   if (T < 0 || k_max < 1 || d < 1 || G < 1 || G > 8 || rank < 0 || rank >= G || cap < 1) {
     set_error("ep_dispatch: bad arguments");
     return MOBILE_ERR_INVALID;
@@ -283,23 +297,30 @@ extern "C" int mobile_ep_dispatch(const float* rows, const int* idx, const int* 
   if (P > 0)
     if (int st = launch_pdl(ep_send_kernel, dim3(P), dim3(128), 0, s, 1, "ep_send", rows, idx, dest_pos, P, k_max, d,
                             local_id, peers_dev, rank, G, cap)) return st;
-  return launch_pdl(ep_post_kernel, dim3(1), dim3(32), 0, s, 1, "ep_post", counts, peers_dev, rank, G, cap, d, epoch);
+  return launch_pdl(ep_post_kernel, dim3(1), dim3(32), 0, s, 1, "ep_post", counts, peers_dev, rank, G, cap, d, epoch,
+                    epoch_dev);
 }
 
-extern "C" int mobile_ep_wait(void* mailbox, int G, int cap, int d, int which, unsigned epoch, int* k_tok_out, int* flags,
-                              void* stream) {
+extern "C" int mobile_ep_wait(void* mailbox, int G, int cap, int d, int which, unsigned epoch, const unsigned* epoch_dev,
+                              int* k_tok_out, int* flags, void* stream) {
   if (G < 1 || G > 8 || (which != 0 && which != 1)) { set_error("ep_wait: bad arguments"); return MOBILE_ERR_INVALID; }
   return launch_pdl(ep_wait_kernel, dim3(1), dim3(256), 0, (cudaStream_t)stream, 1, "ep_wait", mailbox, G, cap, d, which,
-                    epoch, k_tok_out, flags);
+                    epoch, k_tok_out, flags, epoch_dev);
 }
 
 extern "C" int mobile_ep_return(const float* out_rows, const void* mailbox, void* const* peers_dev, int G, int rank, int cap,
-                                int d, unsigned epoch, void* stream) {
+                                int d, unsigned epoch, const unsigned* epoch_dev, void* stream) {
   if (G < 1 || G > 8 || rank < 0 || rank >= G) { set_error("ep_return: bad arguments"); return MOBILE_ERR_INVALID; }
   cudaStream_t s = (cudaStream_t)stream;
   if (int st = launch_pdl(ep_return_kernel, dim3(G * cap), dim3(128), 0, s, 1, "ep_return", out_rows, mailbox, peers_dev,
                           rank, G, cap, d)) return st;
-  return launch_pdl(ep_post_back_kernel, dim3(1), dim3(32), 0, s, 1, "ep_post_back", peers_dev, rank, G, cap, d, epoch);
+  return launch_pdl(ep_post_back_kernel, dim3(1), dim3(32), 0, s, 1, "ep_post_back", peers_dev, rank, G, cap, d, epoch,
+                    epoch_dev);
+}
+
+extern "C" int mobile_ep_advance(unsigned* epoch_dev, void* stream) {
+  if (!epoch_dev) { set_error("ep_advance: null epoch"); return MOBILE_ERR_INVALID; }
+  return launch_pdl(ep_advance_kernel, dim3(1), dim3(32), 0, (cudaStream_t)stream, 1, "ep_advance", epoch_dev);
 }
 
 extern "C" int mobile_ep_collect(const void* mailbox, const int* dest_pos, int P, int G, int cap, int d, float* Y,

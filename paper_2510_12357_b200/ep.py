@@ -37,6 +37,8 @@ from dataclasses import dataclass
 import torch
 import torch.distributed as dist
 
+from .runtime import StepEngine
+
 
 def partition(E: int, G: int) -> list[tuple[int, int]]:
     """Contiguous expert blocks [lo, hi) per rank, the first E % G ranks one larger."""
@@ -218,7 +220,8 @@ class P2PExchange:
         self.counts = torch.zeros(self.G, dtype=torch.int32, device=dev)
         self.flags = torch.zeros(1, dtype=torch.int32, device=dev)
         self.k_in = torch.zeros(self.G * cap, dtype=torch.int32, device=dev)
-        self.epoch = 0
+        self.epoch_dev = torch.zeros(1, dtype=torch.int32, device=dev)  # advanced on the device per exchange
+        self._bufs: dict = {}
         # views of this rank's mailbox (layout of ep_p2p.cu Box)
         rows_b = (self.G * cap * d * 4 + 255) // 256 * 256
         ids_b = (self.G * cap * 4 + 255) // 256 * 256
@@ -229,30 +232,47 @@ class P2PExchange:
     def _s(self):
         return torch.cuda.current_stream().cuda_stream
 
-    def exchange(self, h2: torch.Tensor, idx: torch.Tensor, k_tok: torch.Tensor, expert_fn) -> torch.Tensor:
+    def exchange(self, h2: torch.Tensor, idx: torch.Tensor, k_tok: torch.Tensor, expert_fn,
+                 timer: "ExchangeTimer | None" = None) -> torch.Tensor:
         """h2 (T, d) rows of this rank's tokens, idx (T, k_max) selections ->
         Y (T*k_max, d) expert outputs in pair order; expert_fn(rows, ids,
-        k_tok) runs this rank's experts on its mailbox rows."""
+        k_tok) runs this rank's experts on its mailbox rows.  Kernels only,
+        stream-ordered, no host sync; the epoch lives in device memory
+        (advanced by the first kernel), so the exchange can be captured in a
+        CUDA graph and replayed.  `timer` (eager only) records CUDA events
+        around the dispatch / owner experts / return legs."""
         N, P_ = self.N, self.N.ptr
         T, k_max = idx.shape
         if T * k_max > self.cap:
             raise ValueError(f"P2PExchange: {T * k_max} pairs exceed the mailbox capacity {self.cap}")
-        self.epoch += 1
-        ep = self.epoch
-        dest = torch.empty(T * k_max, dtype=torch.int32, device=self.dev)
+        key = (T, k_max)
+        if key not in self._bufs:
+            self._bufs[key] = (torch.empty(T * k_max, dtype=torch.int32, device=self.dev),
+                               torch.empty(T * k_max, self.d, dtype=torch.float32, device=self.dev))
+        dest, Y = self._bufs[key]
+        s = self._s()
+        if timer is not None:
+            timer.mark("start")
+        N.check(N.lib.mobile_ep_advance(P_(self.epoch_dev), s), "ep advance")
         N.check(N.lib.mobile_ep_dispatch(P_(h2), P_(idx), P_(k_tok), T, k_max, self.d, P_(self.owner),
-                                         P_(self.local_id), P_(self.peers), self.G, self.rank, self.cap, ep, P_(dest),
-                                         P_(self.counts), P_(self.flags), self._s()), "ep dispatch")
-        N.check(N.lib.mobile_ep_wait(self.box, self.G, self.cap, self.d, 0, ep, P_(self.k_in), P_(self.flags),
-                                     self._s()), "ep wait (in)")
+                                         P_(self.local_id), P_(self.peers), self.G, self.rank, self.cap, 0,
+                                         P_(self.epoch_dev), P_(dest), P_(self.counts), P_(self.flags), s),
+                "ep dispatch")
+        N.check(N.lib.mobile_ep_wait(self.box, self.G, self.cap, self.d, 0, 0, P_(self.epoch_dev), P_(self.k_in),
+                                     P_(self.flags), s), "ep wait (in)")
+        if timer is not None:
+            timer.mark("dispatched")
         out = expert_fn(self.in_rows, self.in_ids, self.k_in)
-        N.check(N.lib.mobile_ep_return(P_(out), self.box, P_(self.peers), self.G, self.rank, self.cap, self.d, ep,
-                                       self._s()), "ep return")
-        N.check(N.lib.mobile_ep_wait(self.box, self.G, self.cap, self.d, 1, ep, None, P_(self.flags), self._s()),
-                "ep wait (back)")
-        Y = torch.empty(T * k_max, self.d, dtype=torch.float32, device=self.dev)
-        N.check(N.lib.mobile_ep_collect(self.box, P_(dest), T * k_max, self.G, self.cap, self.d, P_(Y), self._s()),
+        if timer is not None:
+            timer.mark("experts")
+        N.check(N.lib.mobile_ep_return(P_(out), self.box, P_(self.peers), self.G, self.rank, self.cap, self.d, 0,
+                                       P_(self.epoch_dev), s), "ep return")
+        N.check(N.lib.mobile_ep_wait(self.box, self.G, self.cap, self.d, 1, 0, P_(self.epoch_dev), None,
+                                     P_(self.flags), s), "ep wait (back)")
+        N.check(N.lib.mobile_ep_collect(self.box, P_(dest), T * k_max, self.G, self.cap, self.d, P_(Y), s),
                 "ep collect")
+        if timer is not None:
+            timer.mark("returned")
         return Y
 
     def close(self):
@@ -266,6 +286,35 @@ class P2PExchange:
             dist.barrier(group=self.group)  # every peer unmapped this mailbox
         self.N.lib.mobile_ep_mailbox_destroy(self.box)
         self.box = None
+
+
+class ExchangeTimer:
+    """CUDA events around the legs of eager exchanges (dispatch + wait,
+    owner experts, return + wait + collect), summed per leg."""
+
+    LEGS = (("start", "dispatched", "dispatch"), ("dispatched", "experts", "owner_experts"),
+            ("experts", "returned", "return"))
+
+    def __init__(self):
+        self.events: list[dict] = []
+        self.cur: dict | None = None
+
+    def mark(self, name: str):
+        if name == "start":
+            self.cur = {}
+            self.events.append(self.cur)
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.cur[name] = e
+
+    def summary_ms(self) -> dict:
+        torch.cuda.synchronize()
+        out = {leg: 0.0 for _, _, leg in self.LEGS}
+        for ev in self.events:
+            for a, b, leg in self.LEGS:
+                out[leg] += ev[a].elapsed_time(ev[b])
+        out["exchanges"] = len(self.events)
+        return out
 
 
 class P2PExpertParallelMoE(ExpertParallelMoE):
@@ -283,10 +332,56 @@ class P2PExpertParallelMoE(ExpertParallelMoE):
         sc = rm.route(x, layer, k_tok, k_max, replay=replay, replay_mask=replay_mask, reuse_gates=reuse_gates)
         r = sc["router"]
 
-        def experts(rows, ids, k_in):
-            return self.local.rows_ffn(layer, rows, ids, k_in, clone=False)
+        def experts(rows, ids, k_in):  # one kernel choice for any row count: G-invariant outputs
+            return self.local.rows_ffn(layer, rows, ids, k_in, clone=False, force_tc=self.local.tc_ok)
 
         Y = self.x.exchange(r["h2"], r["idx"], k_tok, experts)
         Ys = rm.shared_rows(layer, r["h2"], sc) if rm.S else None
         shared_logits = r["extra"] if rm.dw.n_gate_rows else None
         return K.combine(x, Y, r["gates"], k_tok, Ys, rm.S, shared_logits, ln_out=ln_out)
+
+
+
+class EPStepEngine(StepEngine):
+    """Expert-parallel decode engine: a StepEngine whose
+    routed experts are sharded over the ranks of `group` and exchanged over
+    peer memory every layer.
+
+    Each rank decodes its own B sequences (data-parallel over the batch):
+    embed, attention, router, top-k / replay, shared experts, combine and the
+    head run on the home rank with the single-GPU kernels; only the routed
+    expert rows travel (P2PExchange: dispatch into the owners' mailboxes, the
+    owner's experts on the tcgen05 grouped GEMM for any row count, outputs
+    back, combine in selection order).  Every output row is a function of its
+    own input row alone, so a rank's tokens, router logits, selections and
+    confidences are bit-identical for any G (tests/test_ep_engine_gpu.py).
+    The exchange is kernels only with a device-side epoch, so each pass kind
+    is captured in one CUDA graph like the single-GPU engine.
+
+    `dm` holds the replicated weights (its routed experts are not read);
+    `local` is a MoBiLEMoE over this rank's expert block
+    (DeviceWeights.shard_experts)."""
+
+    def __init__(self, dm, local, batch: int, max_len: int, group=None, graphs: bool = True, gemm=None):
+        super().__init__(dm, batch, max_len, graphs=graphs, persistent=False, gemm=gemm)
+        s = dm.spec
+        self.ep_local = local
+        self.xch = P2PExchange(s.num_experts, s.hidden_dim, batch * s.k_big, group, dm.device)
+        self.ex_timer: ExchangeTimer | None = None  # eager mode: CUDA events around the exchange legs
+
+    def _experts(self, l: int, kind: str, sc: dict, loc) -> torch.Tensor:
+        from . import kernels as K
+        rm, local = self.dm.moe, self.ep_local
+        r = sc["router"]
+        k_tok = self.k_tok[kind]
+
+        def experts(rows, ids, k_in):
+            return local.rows_ffn(l, rows, ids, k_in, clone=False, force_tc=local.tc_ok)
+
+        Y = self.xch.exchange(r["h2"], r["idx"], k_tok, experts, timer=None if self.use_graphs else self.ex_timer)
+        Ys = rm.shared_rows(l, r["h2"], sc) if rm.S else None
+        shared_logits = r["extra"] if rm.dw.n_gate_rows else None
+        return K.combine(self.xa, Y, r["gates"], k_tok, Ys, rm.S, shared_logits, x_out=sc["x_out"], ln_out=self.ln)
+
+    def close(self):
+        self.xch.close()

@@ -242,17 +242,19 @@ class MoBiLEMoE:
 
     # ---- expert-parallel helpers (ep.py) ----
     def rows_ffn(self, layer: int, rows: torch.Tensor, ids: torch.Tensor, k_tok: torch.Tensor | None = None,
-                 clone: bool = True) -> torch.Tensor:
+                 clone: bool = True, force_tc: bool = False) -> torch.Tensor:
         """Routed-expert FFN of R independent rows, row i through local expert
         ids[i] (k = 1); rows with k_tok[i] = 0 are skipped (their output rows
-        are left as they were)."""
+        are left as they were).  force_tc: the tcgen05 path for any R (each
+        output row then depends only on its input row: expert-parallel owners
+        use it so the layer output does not depend on how rows are spread)."""
         R = rows.shape[0]
         if k_tok is None:
             k_tok = torch.ones(R, dtype=torch.int32, device=rows.device)
         sc = self.scratch(R, 1)
         p = K.permute(ids.view(R, 1), k_tok, self.E, out=sc["perm"])
         loc = self.resident(layer)
-        if R >= TC_MIN_TOKENS and self.tc_ok:
+        if (R >= TC_MIN_TOKENS or force_tc) and self.tc_ok:
             self._routed_tc(rows, p, R, 1, loc, sc)
         else:
             self._stream_ffn(rows, p, layer, R, 1, loc, sc, shared=False)
@@ -338,12 +340,31 @@ class DeviceModel:
         self.head_ws: dict = {}
 
     # ------------------------------------------------------------- pieces
-    def _lin(self, h: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
-        """h @ w.T for an out-major (tiled) weight (N, d)."""
+    def _lin(self, h: torch.Tensor, w: torch.Tensor, resid: torch.Tensor | None = None) -> torch.Tensor:
+        """(resid +) h @ w.T for an out-major weight (N, d), on libmobile kernels:
+        up to 8 rows the bulk-copy GEMV (f32 activations); more rows of a bf16
+        model the tcgen05 grouped GEMM in dense mode (bf16 operands, f32
+        accumulate, the residual accumulated in its epilogue).  Only the f32
+        toy weights (the reference-parity configs) with more than 8 rows use
+        torch's matmul."""
         w = self.dw.plain(w)
-        if w.dtype == torch.float32:
-            return Fn.linear(h, w)
-        return Fn.linear(h.to(w.dtype), w).to(torch.float32)
+        n, d = h.shape
+        n_out = w.shape[0]
+        if n <= 8:
+            return K.dense_gemv(h.contiguous(), w, residual=resid)
+        if w.dtype == torch.bfloat16 and d % 128 == 0 and n_out % 128 == 0:
+            xb = torch.empty(n, d, dtype=torch.bfloat16, device=h.device)
+            K.gather_bf16(h.contiguous(), None, 1, n, xb)
+            if resid is not None:
+                out, epi = resid.clone(), K.GG_ACCUM_F32
+            else:
+                out, epi = torch.empty(n, n_out, dtype=torch.float32, device=h.device), K.GG_STORE_F32
+            K.grouped_gemm(xb, d, w.data_ptr(), w.numel() * w.element_size(), 1, n_out,
+                           max_tiles=(n + 127) // 128 * (n_out // 128), dense_rows=n, dense_experts=1, epi=epi,
+                           out_f32=out, ldo=n_out)
+            return out
+        y = Fn.linear(h, w) if w.dtype == torch.float32 else Fn.linear(h.to(w.dtype), w).to(torch.float32)
+        return y if resid is None else resid + y
 
     def attention_full(self, x: torch.Tensor, layer: int) -> torch.Tensor:
         """toymoe.py:178-186 over all n positions (causal), n_heads generalised."""
@@ -359,7 +380,7 @@ class DeviceModel:
         scores = scores.masked_fill(mask, float("-inf"))
         attn = torch.softmax(scores, dim=-1)
         out = (attn @ vh).transpose(0, 1).reshape(n, d)
-        return x + self._lin(out, dw.o[layer])
+        return self._lin(out, dw.o[layer], resid=x)
 
     def stream_head_ws(self) -> K.StreamHeadWorkspace:
         if getattr(self, "_sh_ws", None) is None:
@@ -456,11 +477,11 @@ class DecodeSession:
             out = Fn.scaled_dot_product_attention(qh.to(dt), kh.to(dt), vh.to(dt), attn_mask=mask,
                                                   is_causal=pos == 0)
             out = out.float().transpose(1, 2).reshape(Bn * n, d)
-            return x + m._lin(out, dw.o[layer])
+            return m._lin(out, dw.o[layer], resid=x)
         scores = (qh @ kh.transpose(-1, -2)) / math.sqrt(hd)
         attn = torch.softmax(scores, dim=-1)
         out = (attn @ vh).transpose(1, 2).reshape(Bn * n, d)
-        return x + m._lin(out, dw.o[layer])
+        return m._lin(out, dw.o[layer], resid=x)
 
     def run(self, tokens: torch.Tensor, k_tok: torch.Tensor, k_max: int, *, rows=None, replay=None,
             replay_mask=None, reuse_gates=False, advance=True, expert_hook=None, layer_hook=None, timer=None):

@@ -1,0 +1,177 @@
+"""Expert parallelism is G-invariant on the device.
+
+The expert-parallel layer (P2PExpertParallelMoE) and decode engine
+(EPStepEngine) run the owners' experts with ONE kernel choice for any row
+count (tcgen05 grouped GEMM), so every output row depends only on its own
+input row; routing, gating, shared experts and the combine run on the home
+rank.  A rank's outputs must therefore be BIT-IDENTICAL whether its tokens
+are served by a world of 1 (every expert local) or a world of 2 (half the
+experts on the peer, rows exchanged through IPC-mapped mailboxes).
+
+World 2 runs as two processes sharing the box's one GPU (CUDA IPC; gloo only
+carries the one-time handle exchange); in each process the same tokens also
+go through a world-1 exchange (a one-rank group over all experts) and the
+two results are compared with torch.equal.  T (tokens per rank) in
+{1, 8, 64}.  The engine test decodes little / forced-fallback big / full
+passes from CUDA graphs (device-side exchange epoch) and compares router
+logits, selections, confidences and argmax tokens per step."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from tests.helpers import QWEN_MINI, matched
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _layer_case(rank, world, groups, T):
+    from paper_2510_12357_b200.ep import P2PExpertParallelMoE, partition
+    from paper_2510_12357_b200.model import MoBiLEMoE
+    _, ms, dm = matched(QWEN_MINI, "bfloat16")
+    lo, hi = partition(ms.num_experts, world)[rank]
+    ep2 = P2PExpertParallelMoE(dm.moe, MoBiLEMoE(dm.dw.shard_experts(lo, hi)), ms.num_experts, ms.hidden_dim,
+                               cap=T * ms.k_big, group=groups["world"])
+    ep1 = P2PExpertParallelMoE(dm.moe, MoBiLEMoE(dm.dw.shard_experts(0, ms.num_experts)), ms.num_experts,
+                               ms.hidden_dim, cap=T * ms.k_big, group=groups["self"])
+    bad = []
+    try:
+        for layer in range(ms.num_layers):
+            for rep in range(2):
+                rng = np.random.default_rng(1000 + 37 * rank + 5 * layer + rep)
+                x = torch.tensor(rng.normal(size=(T, ms.hidden_dim)), dtype=torch.float32, device="cuda")
+                k_tok = torch.tensor(rng.choice([ms.k_little, ms.k_big], size=T), dtype=torch.int32, device="cuda")
+                o2 = ep2.forward(x, layer, k_tok, ms.k_big).clone()
+                o1 = ep1.forward(x, layer, k_tok, ms.k_big).clone()
+                torch.cuda.synchronize()
+                if not torch.equal(o1, o2):
+                    bad.append((layer, rep, (o1 - o2).abs().max().item()))
+        assert int(ep2.x.flags.item()) == 0 and int(ep1.x.flags.item()) == 0
+    finally:
+        ep2.x.close()
+        ep1.x.close()
+    return bad
+
+
+def _engine_case(rank, world, groups, B, steps=4):
+    from paper_2510_12357_b200.ep import EPStepEngine, partition
+    from paper_2510_12357_b200.model import MoBiLEMoE
+    _, ms, dm = matched(QWEN_MINI, "bfloat16")
+    lo, hi = partition(ms.num_experts, world)[rank]
+    max_len = 32
+    e2 = EPStepEngine(dm, MoBiLEMoE(dm.dw.shard_experts(lo, hi)), B, max_len, group=groups["world"]).build()
+    e1 = EPStepEngine(dm, MoBiLEMoE(dm.dw.shard_experts(0, ms.num_experts)), B, max_len,
+                      group=groups["self"]).build()
+    # identical synthetic context in both engines (B sequences at position 6)
+    g = torch.Generator(device="cuda").manual_seed(77 + rank)
+    kc = torch.randn(e1.sess.kc.shape, device="cuda", generator=g)
+    vc = torch.randn(e1.sess.vc.shape, device="cuda", generator=g)
+    rng = np.random.default_rng(77 + rank)
+    bad = []
+    try:
+        for e in (e2, e1):
+            e.sess.kc.copy_(kc)
+            e.sess.vc.copy_(vc)
+            e.pos.fill_(6)
+        for i in range(steps):
+            tok = torch.tensor(rng.integers(1, ms.vocab_size, size=B), dtype=torch.int32, device="cuda")
+            outs = []
+            for e in (e2, e1):
+                e.tok.copy_(tok)
+                for kd in ("little", "big", "full"):  # big replays this step's little-pass logits
+                    e.run_pass(kd)
+                e.stream.synchronize()
+                outs.append({kd: (e.states[kd].clone(), e.idx[kd].clone(), e.head[kd]["conf"].clone(),
+                                  e.head[kd]["argmax"].clone()) for kd in ("little", "big", "full")})
+                e.pos.add_(1)
+            torch.cuda.synchronize()
+            for kd in outs[0]:
+                for a, b, name in zip(outs[0][kd], outs[1][kd], ("states", "idx", "conf", "argmax")):
+                    if not torch.equal(a, b):
+                        bad.append((i, kd, name))
+        assert int(e2.xch.flags.item()) == 0 and int(e1.xch.flags.item()) == 0
+    finally:
+        e2.close()
+        e1.close()
+    return bad
+
+
+def _worker(rank, world, port, case, arg, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        selfs = [dist.new_group([r]) for r in range(world)]  # collective: every rank creates every group
+        groups = {"world": dist.group.WORLD, "self": selfs[rank]}
+        fn = _layer_case if case == "layer" else _engine_case
+        q.put((rank, fn(rank, world, groups, arg), None))
+    except Exception as exc:  # noqa: BLE001
+        import traceback
+        q.put((rank, None, traceback.format_exc()[-3000:]))
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn(case, arg, world=2):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, arg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=900) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+    return res
+
+
+@pytest.mark.parametrize("T", [1, 8, 64])
+def test_ep_layer_bit_identical_world1_vs_world2(cuda_ok, T):
+    for rank, bad, exc in _spawn("layer", T):
+        assert exc is None, (rank, exc)
+        assert bad == [], (rank, bad)
+
+
+@pytest.mark.parametrize("B", [1, 8])
+def test_ep_engine_bit_identical_world1_vs_world2(cuda_ok, B):
+    for rank, bad, exc in _spawn("engine", B):
+        assert exc is None, (rank, exc)
+        assert bad == [], (rank, bad)
+
+
+def test_ep_engine_world1_matches_single_gpu_engine(cuda_ok):
+    """In-process world 1: the EP engine (owner experts on the tcgen05 path,
+    bf16 activations) against the single-GPU engine on the same tokens at the
+    bf16 bar (2e-2 of the row's largest router logit / confidence)."""
+    from paper_2510_12357_b200.ep import EPStepEngine
+    from paper_2510_12357_b200.model import MoBiLEMoE
+    from paper_2510_12357_b200.runtime import StepEngine
+    _, ms, dm = matched(QWEN_MINI, "bfloat16")
+    ep = EPStepEngine(dm, MoBiLEMoE(dm.dw.shard_experts(0, ms.num_experts)), 1, 32).build()
+    ref = StepEngine(dm, 1, 32, persistent=False).build()
+    try:
+        prompt = [3, 17, 42, 5]
+        ep.prefill(prompt)
+        ref.prefill(prompt)
+        for i, nxt in enumerate([11, 12, 13]):
+            ep.step(forced_fallback=(i == 1), next_token=nxt)
+            ref.step(forced_fallback=(i == 1), next_token=nxt)
+            torch.cuda.synchronize()
+            a, b = ep.states["little"], ref.states["little"]
+            assert (a - b).abs().max().item() <= 2e-2 * b.abs().max().item()
+            ca, cb = ep.head["little"]["conf"], ref.head["little"]["conf"]
+            assert (ca - cb).abs().max().item() <= 2e-2 * cb.abs().max().item()
+    finally:
+        ep.close()

@@ -84,3 +84,12 @@ def test_bench_reference_arm_restates_the_bench_workload():
     for cap, res in ((16, 6), (8, 2)):
         hw = HardwareSpec(hbm_capacity=cap * 2**30, reserved=res * 2**30)
         assert CB.c3_slots(cap * 2**30, res * 2**30) == hbm_expert_slots(with_byte_sizes(QWEN15_MOE), hw)
+
+
+def test_oracle_bench_specs_match_presets():
+    """bench.py's CPU legs build the config shapes on the oracle side
+    (oracle/cpu_baseline.SPECS, no product import); they must equal presets.py."""
+    from oracle import cpu_baseline as CB
+    from paper_2510_12357_b200.presets import PRESETS
+    for name, spec in CB.SPECS.items():
+        assert CB.oracle_spec_from(PRESETS[name]) == spec, name
