@@ -72,7 +72,12 @@ def dist_init(args):
         import torch
         import torch.distributed as dist
         backend = "nccl" if args.impl == "ours" else "gloo"
-        if backend == "nccl":
+        if os.environ.get("MOBILE_BENCH_SHARE_GPU") == "1":
+            # functional test of the multi-rank path on a 1-GPU box: every rank on
+            # cuda:0 (the EP mailboxes map through CUDA IPC), gloo for the host
+            # collectives (NCCL refuses two ranks on one GPU); numbers meaningless
+            backend, local = "gloo", 0
+        if args.impl == "ours":
             torch.cuda.set_device(local)
         dist.init_process_group(backend)
     return ws, rank, local
@@ -89,6 +94,8 @@ def max_over_ranks(ws, v: float, device=None) -> float:
         return v
     import torch
     import torch.distributed as dist
+    if dist.get_backend() == "gloo":
+        device = "cpu"
     t = torch.tensor([v], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -721,6 +728,8 @@ def main():
         run_reference(args, ws, rank)
         return
     ws, rank, local = dist_init(args)
+    if os.environ.get("MOBILE_BENCH_SHARE_GPU") == "1":
+        local = 0
     run_ours(args, ws, rank, local)
     if ws > 1:
         import torch.distributed as dist

@@ -717,20 +717,21 @@ __device__ void load_x(const Plan& P, int xkind, const float* xsrc, float* xdst,
     block_ln_rows(xbuf, B, d, red);
   } else if (xkind == XK_COMBINE_LN) {
     // x_out = xa + sum_j g_j Y_j (selection order) + sum_s sigma_s Ys_s   (toymoe.py:204, 207)
-    // Every source row of a chunk is loaded before any arithmetic (one L2 round trip per chunk).
+    // Every thread loads the shared-gate logits it needs together with the
+    // source rows of its column (no separate round trip + CTA barrier for the
+    // gates: a dependent L2 load costs ~1 us under the weight stream).
     const int l = combine_layer, k = P.k, S = P.S;
-    __shared__ float sg[kMaxB][kMaxGate];
-    if (tid < B * S) {
-      const int b = tid / S, s = tid - b * S;
-      sg[b][s] = P.n_gate ? sigmoid_f(__ldcg(P.extra + ((size_t)l * B + b) * P.n_gate + s)) : 1.0f;
-    }
-    cbar();
     const float4* Y4 = reinterpret_cast<const float4*>(P.Y);
     const float4* Ys4 = reinterpret_cast<const float4*>(P.Ys);
     const float4* X4 = reinterpret_cast<const float4*>(xsrc);
     float4* xd = reinterpret_cast<float4*>(xdst);
+    constexpr int NT = kCW * 32;
     for (int b = 0; b < B; ++b) {
-      for (int i = tid; i < nv; i += kCW * 32) {
+      float glog[kMaxGate];
+#pragma unroll
+      for (int s2 = 0; s2 < kMaxGate; ++s2)
+        glog[s2] = (s2 < S && P.n_gate) ? __ldcg(P.extra + ((size_t)l * B + b) * P.n_gate + s2) : 0.f;
+      for (int i = tid; i < nv; i += NT) {
         float4 yv[8], ys[kMaxGate];
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -751,7 +752,7 @@ __device__ void load_x(const Plan& P, int xkind, const float* xsrc, float* xdst,
 #pragma unroll
         for (int s2 = 0; s2 < kMaxGate; ++s2) {
           if (s2 < S) {
-            const float g = sg[b][s2];
+            const float g = P.n_gate ? sigmoid_f(glog[s2]) : 1.0f;
             m[0] += g * ys[s2].x; m[1] += g * ys[s2].y; m[2] += g * ys[s2].z; m[3] += g * ys[s2].w;
           }
         }
@@ -1941,7 +1942,19 @@ int mobile_dp_launch(mobile_dp* o, int segment, void* stream) {
   }
   void* kern = pick_kernel(o->w_dtype, o->TT);
   void* args[] = {(void*)&o->plan, (void*)&first, (void*)&last, (void*)&o->nst, (void*)&o->stage_bytes, (void*)&o->xbuf_off};
-  cudaError_t e = cudaLaunchKernel(kern, dim3(o->grid), dim3(kThreads), args, o->smem, (cudaStream_t)stream);
+  // cooperative launch: the grid barriers need every CTA co-resident, which a
+  // cooperative launch guarantees (or refuses) instead of assuming it
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(o->grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = o->smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelExC(&cfg, kern, args);
   if (e != cudaSuccess) return cuda_status(e, "decode_pass launch");
   return MOBILE_OK;
 }

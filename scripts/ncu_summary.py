@@ -13,7 +13,13 @@ for r in rows[1:]:
     if r[mi] != "gpu__time_duration.sum" or (flt and flt not in r[ki]):
         continue
     k = r[ki].split("(")[0][:60]
-    agg[k][0] += float(r[vi].replace(",", ""))
+    try:
+        val = float(r[vi].replace(",", ""))
+    except ValueError:  # "n/a": a launch ncu could not measure
+        continue
+    if val != val:  # "nan" (a launch ncu could not measure)
+        continue
+    agg[k][0] += val
     agg[k][1] += 1
 tot = sum(v[0] for v in agg.values())
 for k, (t, n) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
