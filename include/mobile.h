@@ -133,31 +133,12 @@ int mobile_probs_check(const void* probs, int dtype, int V, double* out, void* s
 int mobile_permute(const int* idx, const int* k_tok, int T, int k_max, int E, int* offsets,
                    int* sorted_pairs, int* active, void* stream);
 
-/* ---- expert FFN (grouped, weight-streaming) -----------------------------
- * toymoe.py:202-204 generalised.  Expert e's weights live at
- *   w13 = w13_base + slot[e] * expert_stride   ((2I or I) x d, out-major;
- *         SwiGLU rows are interleaved in groups of 16: 8 gate rows, 8 up rows)
- *   w2  = w2_base  + slot[e] * expert_stride   (d x I, out-major)
- * `slot` may be NULL (identity).  `max_active` bounds active[0] (host-known
- * upper bound, sizes the grid).  `tok_div` maps pair id -> token (k_max).
- *   gate_up: U[p, :I] = act(h2[p / tok_div] . W13)      (f32)
- *   down:    Y[p, :d] = U[p] . W2                        (f32)
- */
-int mobile_expert_gate_up(const float* h2, const int* offsets, const int* sorted_pairs,
-                          const int* active, int max_active, int max_tokens_per_expert, int tok_div,
-                          int d, int I, const void* w13_base, long long expert_stride,
-                          const int* slot, int w_dtype, int activation, float* U, void* stream);
-int mobile_expert_down(const float* U, const int* offsets, const int* sorted_pairs,
-                       const int* active, int max_active, int max_tokens_per_expert, int d, int I,
-                       const void* w2_base, long long expert_stride, const int* slot, int w_dtype,
-                       float* Y, void* stream);
-
 /* ---- bulk-copy streaming GEMV (decode engine) -----------------------------
  * One launch computes several groups of weight-row dot products, streaming
  * weights through shared memory with cp.async.bulk on an mbarrier ring.
  * Weights are row-major (out-major); rows are streamed in tiles of 16 rows x
  * 4 KB of K (one contiguous copy when the row fits, else one copy per row).
- * Group semantics (per pair p of expert e, see mobile_expert_gate_up):
+ * Group semantics (per pair p of expert e; pairs grouped by mobile_permute):
  *   epi 0 STORE : out[p, r] = (residual[p, r] +) x[p / x_div] . W_e[r]
  *   epi 1 RELU  : out[p, r] = max(x[p / x_div] . W_e[r], 0)
  *   epi 2 SWIGLU: rows in 16-row groups [8 gate | 8 up] ->

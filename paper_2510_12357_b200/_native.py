@@ -83,8 +83,6 @@ _SIGS = {
     "mobile_logits_confidence": ([P, I32, I32, F, F, P, P, P, P], I32),
     "mobile_probs_check": ([P, I32, I32, P, P], I32),
     "mobile_permute": ([P, P, I32, I32, I32, P, P, P, P], I32),
-    "mobile_expert_gate_up": ([P, P, P, P, I32, I32, I32, I32, I32, P, I64, P, I32, I32, P, P], I32),
-    "mobile_expert_down": ([P, P, P, P, I32, I32, I32, I32, P, I64, P, I32, P, P], I32),
     "mobile_combine": ([P, P, P, P, I32, I32, I32, P, I32, P, P, P, P], I32),
     "mobile_grouped_gemm": ([P, I32, I32, P, I64, I32, I32, P, P, P, I32, I32, I32, I32, P, P, I32, I32, P, P], I32),
     "mobile_gather_bf16": ([P, P, I32, I32, I32, P, P], I32),

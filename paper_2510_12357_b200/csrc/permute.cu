@@ -246,3 +246,19 @@ extern "C" int mobile_combine(const float* x, const float* Y, const float* gates
   return launch_pdl(combine_kernel, dim3(T), dim3(threads), 0, (cudaStream_t)stream, 1, "combine", x, Y, gates,
                     k_tok, k_max, d, Y_shared, Y_shared ? n_shared : 0, shared_logits, T, x_out, ln_out);
 }
+
+namespace mobile {
+// SM count of the current device (grids are sized in multiples of it)
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n = v > 0 ? v : 148;
+  }
+  return n;
+}
+}  // namespace mobile
+
+extern "C" int mobile_num_sms(void) { return mobile::sm_count(); }

@@ -141,23 +141,6 @@ def permute(idx, k_tok, E, out=None, stream=None):
     return out
 
 
-def expert_gate_up(h2, offsets, sorted_pairs, active, max_active, max_tok, tok_div, d, I, w13_base_ptr,
-                   expert_stride, slot, w_dtype, activation, U, stream=None):
-    _count()
-    N.check(N.lib.mobile_expert_gate_up(
-        N.ptr(h2), N.ptr(offsets), N.ptr(sorted_pairs), N.ptr(active), int(max_active), int(max_tok),
-        int(tok_div), d, I, w13_base_ptr, int(expert_stride), N.ptr(slot), w_dtype, activation, N.ptr(U),
-        _s(stream)), "expert_gate_up")
-
-
-def expert_down(U, offsets, sorted_pairs, active, max_active, max_tok, d, I, w2_base_ptr, expert_stride, slot,
-                w_dtype, Y, stream=None):
-    _count()
-    N.check(N.lib.mobile_expert_down(
-        N.ptr(U), N.ptr(offsets), N.ptr(sorted_pairs), N.ptr(active), int(max_active), int(max_tok), d, I,
-        w2_base_ptr, int(expert_stride), N.ptr(slot), w_dtype, N.ptr(Y), _s(stream)), "expert_down")
-
-
 def combine(x, Y, gates, k_tok, Y_shared=None, n_shared=0, shared_logits=None, x_out=None, ln_out=None,
             stream=None):
     T, d = x.shape

@@ -35,7 +35,7 @@ torch.backends.cudnn.allow_tf32 = False
 _ACT = {"relu": N.ACT_RELU, "swiglu": N.ACT_SWIGLU}
 # expert FFN implementation: "stream" (bulk-copy TMA streaming, default) or
 # "warp" (register-streaming warp kernels); both are libmobile sm_100a kernels
-FFN_IMPL = os.environ.get("MOBILE_FFN", "stream")
+FFN_IMPL = os.environ.get("MOBILE_FFN", "stream")  # "stream_only": never the tcgen05 path (tests)
 # prefill / batched (T > TC_MIN_TOKENS): grouped expert GEMM on tcgen05 tensor cores
 TC_MIN_TOKENS = int(os.environ.get("MOBILE_TC_MIN_TOKENS", "5"))
 _GATE = {"selected_softmax": N.GATE_SELECTED_SOFTMAX, "softmax_all": N.GATE_SOFTMAX_ALL}
@@ -142,11 +142,9 @@ class MoBiLEMoE:
         Decode (T < TC_MIN_TOKENS): bulk-copy streaming GEMV launches (gate-up
         of routed + shared experts in one launch, then down of both) and the
         combine.  Prefill / batched: the tcgen05 grouped GEMM.
-        FFN_IMPL="warp" selects the register-streaming warp kernels."""
+        FFN_IMPL="stream_only" keeps the streaming path for any T (tests)."""
         T = x.shape[0]
         loc = loc if loc is not None else self.resident(layer)
-        if FFN_IMPL == "warp":
-            return self._experts_warp(x, layer, sc, k_tok, k_max, loc, timer, ln_out)
         r = sc["router"]
         if T >= TC_MIN_TOKENS and self.tc_ok and FFN_IMPL != "stream_only":
             self._routed_tc(r["h2"], sc["perm"], T, k_max, loc, sc)
@@ -278,36 +276,6 @@ class MoBiLEMoE:
                                   max_active=self.S, out=sc["Ys"], prefetch=True)], self.wcode, T)
         del k_max
         return sc["Ys"]
-
-    def _experts_warp(self, x, layer, sc, k_tok, k_max, loc, timer, ln_out):
-        T = x.shape[0]
-        dw, E, d = self.dw, self.E, self.d
-        r, p = sc["router"], sc["perm"]
-        max_active = min(E, T * k_max)
-        if timer is not None:
-            timer.start()
-        K.expert_gate_up(r["h2"], p["offsets"], p["sorted_pairs"], p["active"], max_active, T, k_max, d, self.I,
-                         loc.w13_base, loc.stride, loc.slot, self.wcode, self.act, sc["U"])
-        if timer is not None:
-            timer.stop(("routed", T, k_max))
-        K.expert_down(sc["U"], p["offsets"], p["sorted_pairs"], p["active"], max_active, T, d, self.I,
-                      loc.w2_base, loc.stride, loc.slot, self.wcode, sc["Y"])
-        Ys = None
-        if self.S:
-            base = dw.shared[layer].data_ptr()
-            sb = dw.shared_bytes
-            if timer is not None:
-                timer.start()
-            K.expert_gate_up(r["h2"], sc["s_offsets"], sc["s_pairs"], sc["s_active"], self.S, T, self.S, d, self.Is,
-                             base, sb, None, self.wcode, self.act, sc["Us"])
-            if timer is not None:
-                timer.stop(("shared", T, self.S))
-            K.expert_down(sc["Us"], sc["s_offsets"], sc["s_pairs"], sc["s_active"], self.S, T, d, self.Is,
-                          base + dw.s_w13_elems * dw.elem_bytes, sb, None, self.wcode, sc["Ys"])
-            Ys = sc["Ys"]
-        shared_logits = r["extra"] if dw.n_gate_rows else None
-        K.combine(x, sc["Y"], r["gates"], k_tok, Ys, self.S, shared_logits, x_out=sc["x_out"], ln_out=ln_out)
-        return sc["x_out"]
 
     def forward(self, x: torch.Tensor, layer: int, k_tok: torch.Tensor, k_max: int, *, replay=None,
                 replay_mask=None, reuse_gates=False, experts: ExpertLocation | None = None,

@@ -34,7 +34,7 @@ for name, spec in (("qwen", QWEN15_MOE), ("olmoe", OLMOE)):
         k_tok = torch.full((1,), k, dtype=torch.int32, device=dev)
         scs = [moe.route(x, l, k_tok, k) for l in range(L)]
         scs = [dict(sc) for sc in scs]  # route() returns views of shared scratch: rebuild per layer
-        for impl in ("stream", "warp"):
+        for impl in ("stream",):
             M.FFN_IMPL = impl
             try:
                 sc0 = moe.route(x, 0, k_tok, k)
