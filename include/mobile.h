@@ -211,6 +211,8 @@ int mobile_grouped_gemm(const void* A, int rows_a, int K, const void* B_base, lo
 /* X[r, :] = bf16(src[pairs[r] / div, :]) (pairs NULL: row r) -- the expert-
  * sorted activation matrix for mobile_grouped_gemm. */
 int mobile_gather_bf16(const float* src, const int* pairs, int div, int P, int d, void* X, void* stream);
+/* the same gather from bf16 source rows (expert-parallel mailbox rows) */
+int mobile_gather_rows_bf16(const void* src, const int* pairs, int div, int P, int d, void* X, void* stream);
 
 /* ---- combine -------------------------------------------------------------
  * toymoe.py:192, 204, 207:  moe = sum_j gates[t,j] * Y[t*k_max + j] (selection
@@ -274,6 +276,9 @@ int mobile_memcpy_async(void* dst, const void* src, size_t bytes, void* stream);
  *          the mailbox rows; mobile_ep_return -- output rows back + flag
  *   home : mobile_ep_wait(which=1); mobile_ep_collect -- Y (T*k_max, d) in
  *          pair order (zero rows for unselected slots), then the combine.
+ * rows_bf16 = 1: the dispatched rows are stored as bf16 (half the link bytes;
+ * the owner's tcgen05 experts consume bf16 activations), packed at d * 2
+ * bytes per row inside the mailbox's row area; 0: f32 rows.
  * cap = rows a source may send one owner (T_max * k_max covers the worst case;
  * overflow sets flags bit 0).  A wait that does not see its flags in 10 s
  * traps (flags bit 1).  G <= 8. */
@@ -285,7 +290,8 @@ int mobile_ep_ipc_open(const void* handle64, void** ptr);
 int mobile_ep_ipc_close(void* ptr);
 int mobile_ep_dispatch(const float* rows, const int* idx, const int* k_tok, int T, int k_max, int d, const int* owner,
                        const int* local_id, void* const* peers_dev, int G, int rank, int cap, unsigned epoch,
-                       const unsigned* epoch_dev, int* dest_pos, int* counts, int* flags, void* stream);
+                       const unsigned* epoch_dev, int rows_bf16, int* dest_pos, int* counts, int* flags,
+                       void* stream);
 int mobile_ep_wait(void* mailbox, int G, int cap, int d, int which, unsigned epoch, const unsigned* epoch_dev,
                    int* k_tok_out, int* flags, void* stream);
 int mobile_ep_return(const float* out_rows, const void* mailbox, void* const* peers_dev, int G, int rank, int cap,

@@ -85,6 +85,7 @@ _SIGS = {
     "mobile_permute": ([P, P, I32, I32, I32, P, P, P, P], I32),
     "mobile_combine": ([P, P, P, P, I32, I32, I32, P, I32, P, P, P, P], I32),
     "mobile_grouped_gemm": ([P, I32, I32, P, I64, I32, I32, P, P, P, I32, I32, I32, I32, P, P, I32, I32, P, P], I32),
+    "mobile_gather_rows_bf16": ([P, P, I32, I32, I32, P, P], I32),
     "mobile_gather_bf16": ([P, P, I32, I32, I32, P, P], I32),
     "mobile_ep_mailbox_bytes": ([I32, I32, I32], SZ),
     "mobile_ep_mailbox_create": ([I32, I32, I32, P], I32),
@@ -92,7 +93,7 @@ _SIGS = {
     "mobile_ep_ipc_handle": ([P, P], I32),
     "mobile_ep_ipc_open": ([P, P], I32),
     "mobile_ep_ipc_close": ([P], I32),
-    "mobile_ep_dispatch": ([P, P, P, I32, I32, I32, P, P, P, I32, I32, I32, C.c_uint, P, P, P, P, P], I32),
+    "mobile_ep_dispatch": ([P, P, P, I32, I32, I32, P, P, P, I32, I32, I32, C.c_uint, P, I32, P, P, P, P], I32),
     "mobile_ep_wait": ([P, I32, I32, I32, I32, C.c_uint, P, P, P, P], I32),
     "mobile_ep_return": ([P, P, P, I32, I32, I32, I32, C.c_uint, P, P], I32),
     "mobile_ep_advance": ([P, P], I32),

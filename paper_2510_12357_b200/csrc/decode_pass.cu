@@ -860,6 +860,13 @@ __device__ void attn_unit(const Plan& P, int l, const Item& it, int nc, const ch
 #pragma unroll
       for (int e = 0; e < PER; ++e) acc[e] += q[kAttnPart + lane + 32 * e] * f;
     }
+    if (nc == 1) {  // one unit per head: the final row directly (no partial, ticket or merge)
+      const float inv = 1.0f / S;
+#pragma unroll
+      for (int e = 0; e < PER; ++e) P.att[(size_t)it.b * d + it.h * hd + lane + 32 * e] = acc[e] * inv;
+      cbar();
+      return;
+    }
     float* part = P.attn_part + ((size_t)(it.b * H + it.h) * P.nc_max + it.c) * (hd + kAttnPart);
     if (lane == 0) { part[0] = M; part[1] = S; }
 #pragma unroll
@@ -1716,7 +1723,8 @@ int mobile_dp_create(const mobile_dp_model* m, mobile_dp** out) {
   o->smem = (size_t)o->xbuf_off + xbuf;
 
   // ---- workspace: sync words, attention partials, head partials
-  const int nc_max = std::min(32, std::max(1, G / std::max(1, B * m->H)));
+  int nc_max = std::min(32, std::max(1, G / std::max(1, B * m->H)));
+  if (const char* e = std::getenv("MOBILE_DP_ATTN_NC")) nc_max = std::max(1, std::min(nc_max, std::atoi(e)));
   const size_t sync_bytes = (4 * (64 + (size_t)B * m->H) + 511) / 256 * 256;
   const size_t attn_bytes = 4 * (size_t)B * m->H * nc_max * (hd + kAttnPart);
   const size_t head_bytes = 4 * (size_t)G * kMaxB * 3;

@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kPlanThreads) ep_plan_kernel(const int* __rest
 // 2. rows -> the owners' mailboxes (peer stores), one CTA per pair
 __global__ void ep_send_kernel(const float* __restrict__ rows, const int* __restrict__ idx, const int* __restrict__ dest_pos,
                                int P, int k_max, int d, const int* __restrict__ local_id, void* const* __restrict__ peers,
-                               int rank, int G, int cap) {
+                               int rank, int G, int cap, int rows_bf16) {
   pdl_trigger();
   pdl_wait();
   const int p = blockIdx.x;
@@ -123,8 +123,16 @@ __global__ void ep_send_kernel(const float* __restrict__ rows, const int* __rest
   const int g = dp / cap, pos = dp - g * cap;
   const Box b = layout(G, cap, d);
   char* box = reinterpret_cast<char*>(peers[g]);
-  float* dst = reinterpret_cast<float*>(box + b.in_rows) + ((size_t)rank * cap + pos) * d;
   const float* src = rows + (size_t)(p / k_max) * d;
+  if (rows_bf16) {  // the owner's tensor-core experts consume bf16 rows: half the link bytes
+    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(box + b.in_rows) + ((size_t)rank * cap + pos) * d;
+    for (int i = threadIdx.x * 2; i < d; i += blockDim.x * 2)
+      *reinterpret_cast<__nv_bfloat162*>(dst + i) = __floats2bfloat162_rn(src[i], src[i + 1]);
+    if (threadIdx.x == 0) reinterpret_cast<int*>(box + b.in_ids)[(size_t)rank * cap + pos] = local_id[idx[p]];
+    __threadfence_system();
+    return;
+  }
+  float* dst = reinterpret_cast<float*>(box + b.in_rows) + ((size_t)rank * cap + pos) * d;
   if ((d & 3) == 0) {
     for (int i = threadIdx.x; i < d / 4; i += blockDim.x)
       reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(src)[i];
@@ -284,19 +292,20 @@ extern "C" int mobile_ep_ipc_close(void* ptr) {
 
 extern "C" int mobile_ep_dispatch(const float* rows, const int* idx, const int* k_tok, int T, int k_max, int d,
                                   const int* owner, const int* local_id, void* const* peers_dev, int G, int rank, int cap,
-                                  unsigned epoch, const unsigned* epoch_dev, int* dest_pos, int* counts, int* flags,
-                                  void* stream) {
+                                  unsigned epoch, const unsigned* epoch_dev, int rows_bf16, int* dest_pos, int* counts,
+                                  int* flags, void* stream) {
   if (T < 0 || k_max < 1 || d < 1 || G < 1 || G > 8 || rank < 0 || rank >= G || cap < 1) {
     set_error("ep_dispatch: bad arguments");
     return MOBILE_ERR_INVALID;
   }
+  if (rows_bf16 && (d & 1)) { set_error("ep_dispatch: bf16 rows need an even d"); return MOBILE_ERR_UNSUPPORTED; }
   cudaStream_t s = (cudaStream_t)stream;
   const int P = T * k_max;
   if (int st = launch_pdl(ep_plan_kernel, dim3(1), dim3(kPlanThreads), 0, s, 1, "ep_plan", idx, k_tok, P, k_max, owner, G,
                           cap, dest_pos, counts, flags)) return st;
   if (P > 0)
     if (int st = launch_pdl(ep_send_kernel, dim3(P), dim3(128), 0, s, 1, "ep_send", rows, idx, dest_pos, P, k_max, d,
-                            local_id, peers_dev, rank, G, cap)) return st;
+                            local_id, peers_dev, rank, G, cap, rows_bf16)) return st;
   return launch_pdl(ep_post_kernel, dim3(1), dim3(32), 0, s, 1, "ep_post", counts, peers_dev, rank, G, cap, d, epoch,
                     epoch_dev);
 }

@@ -356,6 +356,24 @@ __global__ void gather_bf16_kernel(const float* __restrict__ src, const int* __r
     *reinterpret_cast<__nv_bfloat162*>(o + i) = __floats2bfloat162_rn(s[i], s[i + 1]);
 }
 
+// the same gather from bf16 rows (expert-parallel mailboxes hold bf16 rows)
+__global__ void gather_rows_bf16_kernel(const __nv_bfloat16* __restrict__ src, const int* __restrict__ pairs, int div,
+                                        int P, int d, __nv_bfloat16* __restrict__ X) {
+  pdl_trigger();
+  pdl_wait();
+  const int r = blockIdx.x;
+  if (r >= P) return;
+  const int srow = pairs ? pairs[r] / div : r;
+  const __nv_bfloat16* s = src + (size_t)srow * d;
+  __nv_bfloat16* o = X + (size_t)r * d;
+  if ((d & 7) == 0) {
+    for (int i = threadIdx.x; i < d / 8; i += blockDim.x)
+      reinterpret_cast<uint4*>(o)[i] = reinterpret_cast<const uint4*>(s)[i];
+  } else {
+    for (int i = threadIdx.x; i < d; i += blockDim.x) o[i] = s[i];
+  }
+}
+
 // ---------------------------------------------------------------- host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -503,6 +521,13 @@ extern "C" int mobile_grouped_gemm(const void* A, int rows_a, int K, const void*
   if (int st = set_smem_once((const void*)grouped_gemm_kernel<128>, GgCfg<128>::kSmem)) return st;
   return launch_pdl(grouped_gemm_kernel<128>, dim3(grid), dim3(kGgThreads), GgCfg<128>::kSmem, (cudaStream_t)stream,
                     1, "grouped_gemm", a);
+}
+
+extern "C" int mobile_gather_rows_bf16(const void* src, const int* pairs, int div, int P, int d, void* X, void* stream) {
+  if (P <= 0) return MOBILE_OK;
+  return launch_pdl(gather_rows_bf16_kernel, dim3(P), dim3(256), 0, (cudaStream_t)stream, 1, "gather_rows_bf16",
+                    reinterpret_cast<const __nv_bfloat16*>(src), pairs, div > 0 ? div : 1, P, d,
+                    reinterpret_cast<__nv_bfloat16*>(X));
 }
 
 extern "C" int mobile_gather_bf16(const float* src, const int* pairs, int div, int P, int d, void* X, void* stream) {

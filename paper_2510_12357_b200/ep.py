@@ -183,7 +183,9 @@ class P2PExchange:
     the worst case).  Collective setup (mailbox handles all-gathered once);
     each exchange is kernels only, stream-ordered on the current stream."""
 
-    def __init__(self, E: int, d: int, cap: int, group=None, device=None):
+    def __init__(self, E: int, d: int, cap: int, group=None, device=None, bf16_rows: bool = False):
+        """bf16_rows: dispatch the rows as bf16 (half the link bytes) -- for
+        owners whose experts run on the tcgen05 path (bf16 activations)."""
         import ctypes as C
 
         from . import _native as N
@@ -225,7 +227,11 @@ class P2PExchange:
         # views of this rank's mailbox (layout of ep_p2p.cu Box)
         rows_b = (self.G * cap * d * 4 + 255) // 256 * 256
         ids_b = (self.G * cap * 4 + 255) // 256 * 256
-        self.in_rows = torch.as_tensor(_DevView(self.box, (self.G * cap, d), "<f4"), device=dev)
+        self.bf16_rows = bool(bf16_rows)
+        if self.bf16_rows:  # bf16 rows packed at d * 2 bytes in the row area (no bf16 typestr: int16 view)
+            self.in_rows = torch.as_tensor(_DevView(self.box, (self.G * cap, d), "<i2"), device=dev).view(torch.bfloat16)
+        else:
+            self.in_rows = torch.as_tensor(_DevView(self.box, (self.G * cap, d), "<f4"), device=dev)
         self.in_ids = torch.as_tensor(_DevView(self.box + rows_b, (self.G * cap,), "<i4"), device=dev)
         del ids_b
 
@@ -256,7 +262,8 @@ class P2PExchange:
         N.check(N.lib.mobile_ep_advance(P_(self.epoch_dev), s), "ep advance")
         N.check(N.lib.mobile_ep_dispatch(P_(h2), P_(idx), P_(k_tok), T, k_max, self.d, P_(self.owner),
                                          P_(self.local_id), P_(self.peers), self.G, self.rank, self.cap, 0,
-                                         P_(self.epoch_dev), P_(dest), P_(self.counts), P_(self.flags), s),
+                                         P_(self.epoch_dev), int(self.bf16_rows), P_(dest), P_(self.counts),
+                                         P_(self.flags), s),
                 "ep dispatch")
         N.check(N.lib.mobile_ep_wait(self.box, self.G, self.cap, self.d, 0, 0, P_(self.epoch_dev), P_(self.k_in),
                                      P_(self.flags), s), "ep wait (in)")
@@ -324,7 +331,7 @@ class P2PExpertParallelMoE(ExpertParallelMoE):
     def __init__(self, moe_full_router, local_moe, E: int, d: int, cap: int, group=None):
         self.router_moe = moe_full_router
         self.local = local_moe
-        self.x = P2PExchange(E, d, cap, group)
+        self.x = P2PExchange(E, d, cap, group, bf16_rows=local_moe.tc_ok)
 
     def forward(self, x, layer, k_tok, k_max, replay=None, replay_mask=None, reuse_gates=False, ln_out=None):
         from . import kernels as K
@@ -366,7 +373,7 @@ class EPStepEngine(StepEngine):
         super().__init__(dm, batch, max_len, graphs=graphs, persistent=False, gemm=gemm)
         s = dm.spec
         self.ep_local = local
-        self.xch = P2PExchange(s.num_experts, s.hidden_dim, batch * s.k_big, group, dm.device)
+        self.xch = P2PExchange(s.num_experts, s.hidden_dim, batch * s.k_big, group, dm.device, bf16_rows=local.tc_ok)
         self.ex_timer: ExchangeTimer | None = None  # eager mode: CUDA events around the exchange legs
 
     def _experts(self, l: int, kind: str, sc: dict, loc) -> torch.Tensor:

@@ -304,7 +304,12 @@ def logits_confidence(logits, logit_scale, gamma, out, stream=None):
 
 
 def gather_bf16(src, pairs, div, P, X, stream=None):
+    """X[r] = bf16(src[pairs[r] / div]) (src f32, or bf16 rows: a plain copy)."""
     _count()
+    if src.dtype == torch.bfloat16:
+        N.check(N.lib.mobile_gather_rows_bf16(N.ptr(src), N.ptr(pairs), int(div), int(P), src.shape[1], N.ptr(X),
+                                              _s(stream)), "gather_rows_bf16")
+        return X
     N.check(N.lib.mobile_gather_bf16(N.ptr(src), N.ptr(pairs), int(div), int(P), src.shape[1], N.ptr(X), _s(stream)),
             "gather_bf16")
     return X

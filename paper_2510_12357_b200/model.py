@@ -252,7 +252,9 @@ class MoBiLEMoE:
         sc = self.scratch(R, 1)
         p = K.permute(ids.view(R, 1), k_tok, self.E, out=sc["perm"])
         loc = self.resident(layer)
-        if (R >= TC_MIN_TOKENS or force_tc) and self.tc_ok:
+        if rows.dtype == torch.bfloat16 and not self.tc_ok:
+            raise ValueError("rows_ffn: bf16 rows need the tcgen05 expert path (bf16 SwiGLU shapes)")
+        if (R >= TC_MIN_TOKENS or force_tc or rows.dtype == torch.bfloat16) and self.tc_ok:
             self._routed_tc(rows, p, R, 1, loc, sc)
         else:
             self._stream_ffn(rows, p, layer, R, 1, loc, sc, shared=False)

@@ -122,7 +122,7 @@ def test_p2p_plan_matches_nccl_path_order(cuda_ok, T, k_max, E, G):
         ti, tk = torch.tensor(idx, device=dev), torch.tensor(k_tok, device=dev)
         own32, loc32 = own.int().contiguous(), loc.int().contiguous()  # alive until the kernels ran
         N.check(N.lib.mobile_ep_dispatch(N.ptr(rows), N.ptr(ti), N.ptr(tk), T, k_max, 8, N.ptr(own32),
-                                         N.ptr(loc32), N.ptr(peers), G, 0, cap, 1, None, N.ptr(dest),
+                                         N.ptr(loc32), N.ptr(peers), G, 0, cap, 1, None, 0, N.ptr(dest),
                                          N.ptr(counts), N.ptr(flags), torch.cuda.current_stream().cuda_stream), "dispatch")
         torch.cuda.synchronize()
     finally:
