@@ -384,8 +384,8 @@ def resident_roofline(spec, dev, ctx, rank):
     reps = 20
     for kd in ("little", "big", "full"):
         k = eng.k[kd]
-        per_layer = (4 * d * d + (spec.num_experts + dw.n_gate_rows) * d) * eb + k * dw.expert_bytes \
-            + spec.n_shared * dw.shared_bytes + 2 * (ctx + 4) * d * 4
+        per_layer = (2 * d * d + 2 * d * spec.kv_dim + (spec.num_experts + dw.n_gate_rows) * d) * eb + k * dw.expert_bytes \
+            + spec.n_shared * dw.shared_bytes + 2 * (ctx + 4) * spec.kv_dim * 4
         tot = L * per_layer + spec.vocab_size * d * eb
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -552,8 +552,8 @@ def config_sweep(args, dev, P):
 
         def pass_bytes(k, B):
             experts = min(spec.num_experts, B * k) * dw.expert_bytes
-            per_layer = (4 * d * d + (spec.num_experts + dw.n_gate_rows) * d) * eb + experts \
-                + spec.n_shared * dw.shared_bytes + B * 2 * ctx * d * 4
+            per_layer = (2 * d * d + 2 * d * spec.kv_dim + (spec.num_experts + dw.n_gate_rows) * d) * eb + experts \
+                + spec.n_shared * dw.shared_bytes + B * 2 * ctx * spec.kv_dim * 4
             return L * per_layer + spec.vocab_size * d * eb
 
         def engine(B):

@@ -246,10 +246,13 @@ int mobile_attn_decode(const float* qkv, float* k_cache, float* v_cache, const i
  * returns the sizes (0 = no split for this shape); tickets must be zeroed once
  * and are left zero by every launch.  One workspace per concurrently running
  * caller (stream / captured graph).  Without a workspace (or too small) the
- * kernel runs unsplit.  mobile_attn_decode = mobile_attn_decode_ws without one. */
+ * kernel runs unsplit.  Grouped-query attention: Hkv key/value heads (H % Hkv
+ * == 0), qkv rows (B, d + 2 Hkv hd) = [q | k | v], caches (B, Hkv, max_len,
+ * hd); query head h reads key/value head h / (H / Hkv).  mobile_attn_decode
+ * = mobile_attn_decode_ws with Hkv = H and no workspace. */
 int mobile_attn_split_ws(int B, int d, int H, int max_len, int* ws_floats, int* n_tickets);
 int mobile_attn_decode_ws(const float* qkv, float* k_cache, float* v_cache, const int* pos, int B, int d,
-                          int H, int max_len, float* out, float* ws, unsigned* tickets, int ws_floats,
+                          int H, int Hkv, int max_len, float* out, float* ws, unsigned* tickets, int ws_floats,
                           int n_tickets, void* stream);
 int mobile_embed(const int* tok, const int* pos, const float* embed, const float* pe, int B, int d, float* x,
                  float* ln_out, void* stream);
@@ -408,9 +411,10 @@ long long* mobile_offload_zs_base(mobile_offload* o); /* progress value at the n
 typedef struct mobile_dp_model {
   int B, L, d, H, V, E, k, n_shared, n_gate, ffn, shared_ffn, activation, gate_norm, reuse_gates;
   int w_dtype, max_len, offload;
+  int Hkv;                    /* key/value heads (0 = H; fewer = grouped-query attention) */
   float logit_scale, gamma;
   /* weights (out-major, row-major rows) */
-  const void* qkv;            /* (L, 3d, d) */
+  const void* qkv;            /* (L, d + 2 Hkv hd, d) */
   const void* o;              /* (L, d, d) */
   const void* router;         /* (L, E + n_gate, d) */
   const void* shared;         /* (L, S, shared_stride bytes) packed [W13 | W2] */
@@ -424,7 +428,7 @@ typedef struct mobile_dp_model {
   /* state */
   const int* tok;             /* (B,) input token */
   const int* pos;             /* (B,) position */
-  float *kc, *vc;             /* (L, B, H, max_len, d/H) head-major */
+  float *kc, *vc;             /* (L, B, Hkv, max_len, d/H) head-major */
   float *x, *xa, *q, *att;    /* (B, d) */
   float *U, *Us, *Y, *Ys;     /* (B*k, ffn), (B*S, shared_ffn), (B*k, d), (B*S, d) */
   float* states;              /* (L, B, E) router logits of this pass */

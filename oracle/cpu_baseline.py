@@ -51,7 +51,8 @@ def aliased_weights(spec: R.OracleSpec, layer_pool=4, expert_pool=64, seed=0) ->
 
     lp = min(layer_pool, L)
     ep = min(expert_pool, L * E)
-    attn = [_ByLayer([U(d, d) for _ in range(lp)]) for _ in range(4)]
+    kvd = spec.kv_dim
+    attn = [_ByLayer([U(d, w) for _ in range(lp)]) for w in (d, kvd, kvd, d)]
     w_in = _ByExpert([U(d, I) for _ in range(ep)], E)
     w_up = _ByExpert([U(d, I) for _ in range(ep)], E) if spec.activation == "swiglu" else None
     w_out = _ByExpert([U(I, d, fan_in=I) for _ in range(ep)], E)
@@ -70,7 +71,8 @@ def oracle_spec_from(ms) -> R.OracleSpec:
                         hidden_dim=ms.hidden_dim, vocab_size=ms.vocab_size, eos_token=ms.eos_token, seed=ms.seed,
                         ffn_dim=ms.ffn, activation=ms.activation, n_shared=ms.n_shared,
                         shared_ffn_dim=ms.shared_ffn, shared_gate=ms.shared_gate, gate_norm=ms.gate_norm,
-                        n_heads=ms.n_heads, logit_scale=ms.logit_scale, embed_scale=ms.embed_scale,
+                        n_heads=ms.n_heads, n_kv_heads=ms.kv_heads, logit_scale=ms.logit_scale,
+                        embed_scale=ms.embed_scale,
                         pos_encoding=ms.pos_encoding)
 
 
@@ -92,7 +94,8 @@ C4_SPEC = R.OracleSpec(num_layers=27, num_experts=64, k_big=6, k_little=3, hidde
                        ffn_dim=1408, activation="swiglu", n_shared=2, shared_ffn_dim=1408, n_heads=16,
                        embed_scale=1.0, pos_encoding="none")
 C5_SPEC = R.OracleSpec(num_layers=32, num_experts=8, k_big=2, k_little=1, hidden_dim=4096, vocab_size=32000,
-                       ffn_dim=14336, activation="swiglu", n_heads=32, embed_scale=1.0, pos_encoding="none")
+                       ffn_dim=14336, activation="swiglu", n_heads=32, n_kv_heads=8, embed_scale=1.0,
+                       pos_encoding="none")
 SPECS = {"c2": C2_SPEC, "c3": C3_SPEC, "c4": C4_SPEC, "c5": C5_SPEC}
 
 
@@ -101,7 +104,7 @@ def c3_slots(cap_bytes: int, reserved_bytes: int, spec: R.OracleSpec = C3_SPEC) 
     (expert = 3 d I, dense/layer = qkv+o + router + shared + shared gate)."""
     d, per = spec.hidden_dim, 2
     expert = 3 * d * spec.ffn_dim * per
-    dense = 4 * d * d * per + d * spec.num_experts * per + spec.n_shared * 3 * d * spec.shared_ffn_dim * per \
+    dense = (2 * d * d + 2 * d * spec.kv_dim) * per + d * spec.num_experts * per + spec.n_shared * 3 * d * spec.shared_ffn_dim * per \
         + (spec.n_shared * d * per if spec.shared_gate == "sigmoid" else 0)
     return R.hbm_expert_slots(spec.num_layers, dense, cap_bytes, reserved_bytes, expert, spec.k_big)
 
@@ -111,7 +114,7 @@ def synthetic_context(dec: R.KVDecoder, n: int, seed: int = 3) -> None:
     prefilling an n-token prompt: decode cost depends on the cache length,
     not its contents)."""
     rng = np.random.default_rng(seed)
-    d = dec.W.spec.hidden_dim
+    d = dec.W.spec.kv_dim
     for l in range(dec.W.spec.num_layers):
         dec.k_cache[l] = rng.standard_normal((n, d), dtype=np.float32)
         dec.v_cache[l] = rng.standard_normal((n, d), dtype=np.float32)

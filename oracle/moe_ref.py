@@ -48,6 +48,7 @@ class OracleSpec:
     shared_gate: str = "none"  # "none" | "sigmoid" (Qwen-style)
     gate_norm: str = "selected_softmax"  # toymoe.py:201 | "softmax_all" (HF norm_topk_prob=False)
     n_heads: int = 1
+    n_kv_heads: int = 0  # 0 -> n_heads (extension: grouped-query attention)
     logit_scale: float = LOGIT_SCALE
     embed_scale: float = 0.0  # 0 -> 1/sqrt(d) as the toy (toymoe.py:109-112)
     pos_encoding: str = "sinusoidal"  # toymoe.py:135-140 | "none" (extension)
@@ -59,6 +60,12 @@ class OracleSpec:
             object.__setattr__(self, "ffn_dim", self.hidden_dim)
         if self.shared_ffn_dim == 0:
             object.__setattr__(self, "shared_ffn_dim", self.ffn_dim)
+        if self.n_kv_heads == 0:
+            object.__setattr__(self, "n_kv_heads", self.n_heads)
+
+    @property
+    def kv_dim(self) -> int:
+        return self.n_kv_heads * (self.hidden_dim // self.n_heads)
 
 
 # ---------------------------------------------------------------------------
@@ -158,7 +165,8 @@ def build_weights(spec: OracleSpec) -> OracleWeights:
         return rng.uniform(-1.0, 1.0, size=shape) * (1.0 / np.sqrt(fan_in))
 
     embed = mat(V, d, fan_in=1.0 / spec.embed_scale**2 if spec.embed_scale else d)
-    q, k, v, o = mat(L, d, d), mat(L, d, d), mat(L, d, d), mat(L, d, d)
+    kvd = spec.kv_dim  # = d unless grouped-query attention
+    q, k, v, o = mat(L, d, d), mat(L, d, kvd), mat(L, d, kvd), mat(L, d, d)
     router = mat(L, d, E)
     w_in = mat(L, E, d, I)
     w_out = mat(L, E, I, d, fan_in=I)
@@ -268,14 +276,16 @@ def attention(W: OracleWeights, layer: int, h: np.ndarray, k_cache=None, v_cache
         out = attn @ vv
     else:
         hd = d // H
+        grp = H // spec.n_kv_heads  # query heads per key/value head (1 = multi-head)
         out = np.empty_like(q)
         for hh in range(H):
             sl = slice(hh * hd, (hh + 1) * hd)
-            scores = q[:, sl] @ kk[:, sl].T / np.sqrt(hd) + mask
+            kv = slice((hh // grp) * hd, (hh // grp + 1) * hd)
+            scores = q[:, sl] @ kk[:, kv].T / np.sqrt(hd) + mask
             scores -= scores.max(axis=-1, keepdims=True)
             attn = np.exp(scores)
             attn /= attn.sum(axis=-1, keepdims=True)
-            out[:, sl] = attn @ vv[:, sl]
+            out[:, sl] = attn @ vv[:, kv]
     return out @ W.attn_o[layer], key, v
 
 
@@ -396,8 +406,8 @@ class KVDecoder:
         s = W.spec
         self.prefill_k = s.k_big if prefill_k is None else prefill_k
         dt = W.embed.dtype
-        self.k_cache = [np.zeros((0, s.hidden_dim), dtype=dt) for _ in range(s.num_layers)]
-        self.v_cache = [np.zeros((0, s.hidden_dim), dtype=dt) for _ in range(s.num_layers)]
+        self.k_cache = [np.zeros((0, s.kv_dim), dtype=dt) for _ in range(s.num_layers)]
+        self.v_cache = [np.zeros((0, s.kv_dim), dtype=dt) for _ in range(s.num_layers)]
 
     @property
     def length(self) -> int:

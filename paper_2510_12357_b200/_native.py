@@ -44,7 +44,8 @@ class mobile_channel(C.Structure):
 class mobile_dp_model(C.Structure):
     """include/mobile.h mobile_dp_model (persistent decode pass)."""
     _fields_ = [(n, C.c_int) for n in ("B", "L", "d", "H", "V", "E", "k", "n_shared", "n_gate", "ffn", "shared_ffn",
-                                       "activation", "gate_norm", "reuse_gates", "w_dtype", "max_len", "offload")] + [
+                                       "activation", "gate_norm", "reuse_gates", "w_dtype", "max_len", "offload",
+                                       "Hkv")] + [
         ("logit_scale", C.c_float), ("gamma", C.c_float),
         ("qkv", C.c_void_p), ("o", C.c_void_p), ("router", C.c_void_p), ("shared", C.c_void_p),
         ("shared_stride", C.c_longlong), ("shared_w2_offset", C.c_longlong), ("experts", C.c_void_p),
@@ -106,7 +107,7 @@ _SIGS = {
     "mobile_dense_gemv": ([P, I32, I32, I32, P, I32, I32, P, P, P], I32),
     "mobile_attn_decode": ([P, P, P, P, I32, I32, I32, I32, P, P], I32),
     "mobile_attn_split_ws": ([I32, I32, I32, I32, P, P], I32),
-    "mobile_attn_decode_ws": ([P, P, P, P, I32, I32, I32, I32, P, P, P, I32, I32, P], I32),
+    "mobile_attn_decode_ws": ([P, P, P, P, I32, I32, I32, I32, I32, P, P, P, I32, I32, P], I32),
     "mobile_embed": ([P, P, P, P, I32, I32, P, P, P], I32),
     "mobile_advance": ([P, I32, P, P, P], I32),
     "mobile_memcpy_async": ([P, P, SZ, P], I32),

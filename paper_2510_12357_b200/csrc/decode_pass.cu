@@ -91,6 +91,7 @@ struct Plan {
   int ppl, L, n_phases, bpl, upl, router_j;
   int B, d, H, E, k, S, n_gate, gate_norm, reuse_gates, max_len, V, nc_max, TT;
   int hd, npi;           // head dim; K/V positions per ring stage
+  int Hkv, grp;          // key/value heads; query heads per key/value head (grouped-query attention)
   int pf_window;         // L2 prefetch distance ahead of the ring, bytes per CTA (0 = off)
   float logit_scale, gamma;
   const int* tok;
@@ -822,7 +823,7 @@ __device__ void attn_unit(const Plan& P, int l, const Item& it, int nc, const ch
     if (lane == 0) mbar_arrive(&empty[st]);
   }
   if (it.c == nc - 1 && warp == 0) {  // the new position, written by this pass's qkv phase
-    const size_t row = (((size_t)l * B + it.b) * H + it.h) * P.max_len + spos[it.b];
+    const size_t row = (((size_t)l * B + it.b) * P.Hkv + it.h / P.grp) * P.max_len + spos[it.b];
     const float* kr = P.kc + row * hd;
     const float* vr = P.vc + row * hd;
     float kv[PER], vv[PER];
@@ -1128,7 +1129,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
             pu += G;
             if (a.np > 0) {
               const uint32_t bytes = (uint32_t)a.np * P.hd * 4u;
-              const size_t row = (((size_t)pl * P.B + a.b) * P.H + a.h) * P.max_len + a.p0;
+              const size_t row = (((size_t)pl * P.B + a.b) * P.Hkv + a.h / P.grp) * P.max_len + a.p0;
               if (lane == 0) { prefetch_l2(P.kc + row * P.hd, bytes); prefetch_l2(P.vc + row * P.hd, bytes); }
               pf_bytes += 2ull * bytes;
             }
@@ -1182,7 +1183,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
             if (iw >= (uint32_t)nst) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             meta[s].needx = 0;
             char* stg = smem + (size_t)s * stage_bytes;
-            const size_t row = (((size_t)wl * P.B + wit.b) * P.H + wit.h) * P.max_len + q0;
+            const size_t row = (((size_t)wl * P.B + wit.b) * P.Hkv + wit.h / P.grp) * P.max_len + q0;
             mbar_arrive_tx(&full[s], 2u * bytes);
             bulk_g2s(stg, P.kc + row * P.hd, bytes, &full[s]);
             bulk_g2s(stg + (size_t)P.npi * P.hd * 4, P.vc + row * P.hd, bytes, &full[s]);
@@ -1509,12 +1510,13 @@ __global__ void __launch_bounds__(kThreads, 1) decode_pass_kernel(const __grid_c
                 }
               } else if (Gr.epi == EP_QKV) {
                 const int d = P.d;
+                const int kvd = P.Hkv * P.hd;  // rows [q (d) | k (kvd) | v (kvd)]
                 if (r0 < d) P.q[(size_t)tb * d + r0] = v;
                 else {
-                  float* cache = r0 < 2 * d ? P.kc : P.vc;
-                  const int c = r0 < 2 * d ? r0 - d : r0 - 2 * d;
+                  float* cache = r0 < d + kvd ? P.kc : P.vc;
+                  const int c = r0 < d + kvd ? r0 - d : r0 - d - kvd;
                   const int hh = c / P.hd;
-                  cache[((((size_t)l * P.B + tb) * P.H + hh) * P.max_len + spos[tb]) * P.hd + (c - hh * P.hd)] = v;
+                  cache[((((size_t)l * P.B + tb) * P.Hkv + hh) * P.max_len + spos[tb]) * P.hd + (c - hh * P.hd)] = v;
                 }
               } else if (Gr.epi == EP_LOGITS) {
                 if (r0 < Gr.split) Gr.out[(size_t)tb * Gr.out_ld + r0] = v;
@@ -1694,6 +1696,8 @@ int mobile_dp_create(const mobile_dp_model* m, mobile_dp** out) {
     set_error("decode_pass: unsupported shape B=%d k=%d E=%d S=%d d=%d H=%d", B, k, E, S, d, m->H);
     return MOBILE_ERR_UNSUPPORTED;
   }
+  const int Hkv = m->Hkv > 0 ? m->Hkv : m->H;  // grouped-query attention: key/value heads
+  if (m->H % Hkv) { set_error("decode_pass: Hkv=%d must divide H=%d", Hkv, m->H); return MOBILE_ERR_INVALID; }
   auto* o = new mobile_dp();
   o->w_dtype = m->w_dtype;
   o->TT = B == 1 ? 1 : B == 2 ? 2 : 4;
@@ -1741,6 +1745,7 @@ int mobile_dp_create(const mobile_dp_model* m, mobile_dp** out) {
   P.reuse_gates = m->reuse_gates; P.max_len = m->max_len; P.L = L; P.V = m->V; P.nc_max = nc_max; P.TT = o->TT;
   P.logit_scale = m->logit_scale; P.gamma = m->gamma;
   P.hd = hd; P.npi = kWBytes / (2 * hd * 4);
+  P.Hkv = Hkv; P.grp = m->H / Hkv;
   // measured: an L2 prefetch cursor ahead of (or trailing) the ring slows the
   // pass (C3 little 2037 -> 1906 us without it); MOBILE_DP_PF_KB >= 0 enables it
   P.pf_window = -1;
@@ -1785,7 +1790,8 @@ int mobile_dp_create(const mobile_dp_model* m, mobile_dp** out) {
   {  // qkv
     Tmpl t{};
     t.type = PT_GEMV; t.n_groups = 1; t.end_bar = 1;
-    t.g[0] = dense_group(m->qkv, 3 * Wsz, d, 3 * d, EP_QKV);
+    const int qkv_rows = d + 2 * (d / m->H) * Hkv;  // [q | k | v], k / v narrower under GQA
+    t.g[0] = dense_group(m->qkv, (long long)qkv_rows * d * eb, d, qkv_rows, EP_QKV);
     t.xkind0 = XK_EMBED_LN; t.xkind = XK_COMBINE_LN; t.xsrc = m->xa; t.xdst = m->x;
     ts.push_back(t);
   }

@@ -122,9 +122,9 @@ __global__ void __launch_bounds__(kGemvThreads) dense_gemv_kernel(const float* _
 // each, at pos[b]).  qkv (B, 3d) = [q | k | v]; the new k/v rows are written to
 // the cache first.  One CTA per (sequence, head), head_dim <= 256.
 __global__ void attn_decode_kernel(const float* __restrict__ qkv, float* __restrict__ kc,
-                                   float* __restrict__ vc, const int* __restrict__ pos, int d, int H,
+                                   float* __restrict__ vc, const int* __restrict__ pos, int d, int H, int Hkv,
                                    int max_len, float* __restrict__ out) {
-  extern __shared__ __align__(16) float sc[];  // max_len scores + hd q
+  extern __shared__ __align__(16) float sc[];  // max_len scores + hd q + hd new k + hd new v
   __shared__ float red[32];
   pdl_trigger();
   pdl_wait();
@@ -137,23 +137,32 @@ __global__ void attn_decode_kernel(const float* __restrict__ qkv, float* __restr
     return;
   }
   float* q = sc + max_len;
-  const float* src = qkv + (size_t)b * 3 * d;
-  // head-major cache (B, H, max_len, hd)
-  const size_t head0 = ((size_t)b * H + hh) * max_len;
+  float* knew = q + hd;
+  float* vnew = knew + hd;
+  // grouped-query attention: query head hh reads key/value head g; the new
+  // position's K/V come from this step's qkv row (other query heads of the
+  // group run in other CTAs), the group's first head writes them to the cache
+  const int grp = H / Hkv, g = hh / grp, kvd = Hkv * hd;
+  const float* src = qkv + (size_t)b * (d + 2 * kvd);
+  // head-major cache (B, Hkv, max_len, hd)
+  const size_t head0 = ((size_t)b * Hkv + g) * max_len;
   float* kr = kc + (head0 + p) * hd;
   float* vr = vc + (head0 + p) * hd;
   for (int e = threadIdx.x; e < hd; e += blockDim.x) {
     q[e] = src[hh * hd + e];
-    kr[e] = src[d + hh * hd + e];
-    vr[e] = src[2 * d + hh * hd + e];
+    knew[e] = src[d + g * hd + e];
+    vnew[e] = src[d + kvd + g * hd + e];
+    if (hh % grp == 0) {
+      kr[e] = knew[e];
+      vr[e] = vnew[e];
+    }
   }
-  __threadfence_block();
   __syncthreads();
   const float scale = 1.0f / sqrtf((float)hd);
   // scores: one warp per position
   float mx = -INFINITY;
   for (int j = warp; j <= p; j += nw) {
-    const float* kj = kc + (head0 + j) * hd;
+    const float* kj = j == p ? knew : kc + (head0 + j) * hd;
     float s = 0.f;
     for (int e = lane; e < hd; e += 32) s = fmaf(q[e], kj[e], s);
     s = warp_sum(s) * scale;
@@ -179,7 +188,8 @@ __global__ void attn_decode_kernel(const float* __restrict__ qkv, float* __restr
   const float inv = 1.0f / sum;
   for (int e = threadIdx.x; e < hd; e += blockDim.x) {
     float acc = 0.f;
-    for (int j = 0; j <= p; ++j) acc = fmaf(sc[j], vc[(head0 + j) * hd + e], acc);
+    for (int j = 0; j < p; ++j) acc = fmaf(sc[j], vc[(head0 + j) * hd + e], acc);
+    acc = fmaf(sc[p], vnew[e], acc);
     out[(size_t)b * d + hh * hd + e] = acc * inv;
   }
 }
@@ -198,13 +208,14 @@ template <int HD>
 __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const float* __restrict__ qkv,
                                                                        float* __restrict__ kc, float* __restrict__ vc,
                                                                        const int* __restrict__ pos, int d, int H,
-                                                                       int max_len, float* __restrict__ out, int nsplit,
+                                                                       int Hkv, int max_len, float* __restrict__ out,
+                                                                       int nsplit,
                                                                        float* __restrict__ ws, unsigned* __restrict__ tk) {
   constexpr int NW = kAttnThreads / 32;
   constexpr int LS = HD / 16, PS = 32 / LS;  // score lanes per position, positions per warp step
   constexpr int LV = HD / 4, PV = 32 / LV;   // P.V lanes per position, positions per warp step
   extern __shared__ __align__(16) float sc[];  // this split's scores
-  __shared__ __align__(16) float qs[HD];
+  __shared__ __align__(16) float qs[HD], knew[HD], vnew[HD];
   __shared__ __align__(16) float part[NW * PV][HD];
   __shared__ float red[NW];
   __shared__ int last_s;
@@ -222,13 +233,19 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
   // split sp owns positions [j0, j1) of [0, p]; the split holding p writes the new row
   const int n = p + 1;
   const int j0 = (int)((long long)n * sp / nsplit), j1 = (int)((long long)n * (sp + 1) / nsplit);
-  const float* src = qkv + (size_t)b * 3 * d;
-  const size_t head0 = ((size_t)b * H + hh) * max_len;  // head-major cache (B, H, max_len, HD)
+  // grouped-query attention: query head hh reads key/value head g; position
+  // p's K/V come from this step's qkv row (query heads of the group run in
+  // other CTAs); the group's first head (its split holding p) writes them
+  const int grp = H / Hkv, g = hh / grp, kvd = Hkv * HD;
+  const float* src = qkv + (size_t)b * (d + 2 * kvd);
+  const size_t head0 = ((size_t)b * Hkv + g) * max_len;  // head-major cache (B, Hkv, max_len, HD)
   for (int e = threadIdx.x; e < HD; e += blockDim.x) {
     qs[e] = src[hh * HD + e];
-    if (j1 == n) {
-      kc[(head0 + p) * HD + e] = src[d + hh * HD + e];
-      vc[(head0 + p) * HD + e] = src[2 * d + hh * HD + e];
+    knew[e] = src[d + g * HD + e];
+    vnew[e] = src[d + kvd + g * HD + e];
+    if (j1 == n && hh % grp == 0) {
+      kc[(head0 + p) * HD + e] = knew[e];
+      vc[(head0 + p) * HD + e] = vnew[e];
     }
   }
   __syncthreads();
@@ -246,10 +263,15 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
     const int j = jj + sg;
     float s = 0.f;
     if (j < j1) {
-      const float4* kr = reinterpret_cast<const float4*>(kc + (head0 + j) * HD + sl * 16);
       float4 k4[4];
+      if (j == p) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) k4[i] = __ldcs(kr + i);
+        for (int i = 0; i < 4; ++i) k4[i] = reinterpret_cast<const float4*>(knew + sl * 16)[i];
+      } else {
+        const float4* kr = reinterpret_cast<const float4*>(kc + (head0 + j) * HD + sl * 16);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) k4[i] = __ldcs(kr + i);
+      }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
         s += qv[4 * i] * k4[i].x + qv[4 * i + 1] * k4[i].y + qv[4 * i + 2] * k4[i].z + qv[4 * i + 3] * k4[i].w;
@@ -286,7 +308,8 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int j = j0 + warp * PV + vg; j < j1; j += NW * PV) {
     const float w = sc[j - j0];
-    const float4 v4 = __ldcs(reinterpret_cast<const float4*>(vc + (head0 + j) * HD) + vl);
+    const float4 v4 = j == p ? reinterpret_cast<const float4*>(vnew)[vl]
+                             : __ldcs(reinterpret_cast<const float4*>(vc + (head0 + j) * HD) + vl);
     acc.x = fmaf(w, v4.x, acc.x); acc.y = fmaf(w, v4.y, acc.y);
     acc.z = fmaf(w, v4.z, acc.z); acc.w = fmaf(w, v4.w, acc.w);
   }
@@ -457,9 +480,12 @@ extern "C" int mobile_attn_split_ws(int B, int d, int H, int max_len, int* ws_fl
 // tickets zeroed once, every launch leaves them zero).  One workspace per
 // concurrently running caller (stream / graph): two launches sharing one race.
 extern "C" int mobile_attn_decode_ws(const float* qkv, float* k_cache, float* v_cache, const int* pos, int B, int d,
-                                     int H, int max_len, float* out, float* ws, unsigned* tickets, int ws_floats,
-                                     int n_tickets, void* stream) {
-  if (B <= 0 || d <= 0 || H <= 0 || d % H || max_len <= 0) { set_error("attn_decode: bad shape"); return MOBILE_ERR_INVALID; }
+                                     int H, int Hkv, int max_len, float* out, float* ws, unsigned* tickets,
+                                     int ws_floats, int n_tickets, void* stream) {
+  if (B <= 0 || d <= 0 || H <= 0 || d % H || max_len <= 0 || Hkv <= 0 || H % Hkv) {
+    set_error("attn_decode: bad shape");
+    return MOBILE_ERR_INVALID;
+  }
   const int hd = d / H;
   if ((hd == 64 || hd == 128) && (d & 3) == 0) {
     const size_t vsmem = sizeof(float) * (size_t)max_len;
@@ -470,19 +496,19 @@ extern "C" int mobile_attn_decode_ws(const float* qkv, float* k_cache, float* v_
     const int bhn = B * H;
     if (nsplit > 1 && (!ws || !tickets || ws_floats < bhn * nsplit * (hd + 2) || n_tickets < bhn)) nsplit = 1;
     return launch_pdl(kern, dim3(bhn * nsplit), dim3(kAttnThreads), vsmem, (cudaStream_t)stream, 1, "attn_decode", qkv,
-                      k_cache, v_cache, pos, d, H, max_len, out, nsplit, nsplit > 1 ? ws : nullptr,
+                      k_cache, v_cache, pos, d, H, Hkv, max_len, out, nsplit, nsplit > 1 ? ws : nullptr,
                       nsplit > 1 ? tickets : nullptr);
   }
-  const size_t smem = sizeof(float) * ((size_t)max_len + d / H);
+  const size_t smem = sizeof(float) * ((size_t)max_len + 3 * (d / H));
   if (smem > 200 * 1024) { set_error("attn_decode: max_len=%d too long", max_len); return MOBILE_ERR_UNSUPPORTED; }
   set_smem_once((const void*)attn_decode_kernel, smem);
   return launch_pdl(attn_decode_kernel, dim3(B * H), dim3(128), smem, (cudaStream_t)stream, 1, "attn_decode", qkv,
-                    k_cache, v_cache, pos, d, H, max_len, out);
+                    k_cache, v_cache, pos, d, H, Hkv, max_len, out);
 }
 
 extern "C" int mobile_attn_decode(const float* qkv, float* k_cache, float* v_cache, const int* pos, int B, int d,
                                   int H, int max_len, float* out, void* stream) {
-  return mobile_attn_decode_ws(qkv, k_cache, v_cache, pos, B, d, H, max_len, out, nullptr, nullptr, 0, 0, stream);
+  return mobile_attn_decode_ws(qkv, k_cache, v_cache, pos, B, d, H, H, max_len, out, nullptr, nullptr, 0, 0, stream);
 }
 
 extern "C" int mobile_embed(const int* tok, const int* pos, const float* embed, const float* pe, int B, int d,

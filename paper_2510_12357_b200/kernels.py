@@ -201,15 +201,16 @@ def attn_split_workspace(B, d, n_heads, max_len, device):
 
 
 def attn_decode(qkv, k_cache, v_cache, pos, n_heads, out=None, stream=None, ws=None):
-    B, d3 = qkv.shape
-    d = d3 // 3
-    max_len = k_cache.shape[2]  # head-major (B, H, max_len, head_dim)
+    """qkv (B, d + 2 Hkv hd); caches head-major (B, Hkv, max_len, hd); Hkv < n_heads = GQA."""
+    B = qkv.shape[0]
+    Hkv, max_len, hd = k_cache.shape[1], k_cache.shape[2], k_cache.shape[3]
+    d = n_heads * hd
     if out is None:
         out = torch.empty(B, d, device=qkv.device, dtype=torch.float32)
     _count()
     wp, tp, nf, nt = (N.ptr(ws[0]), N.ptr(ws[1]), ws[0].numel(), ws[1].numel()) if ws is not None else (None, None, 0, 0)
     N.check(N.lib.mobile_attn_decode_ws(N.ptr(qkv), N.ptr(k_cache), N.ptr(v_cache), N.ptr(pos), B, d, n_heads,
-                                        max_len, N.ptr(out), wp, tp, nf, nt, _s(stream)), "attn_decode")
+                                        Hkv, max_len, N.ptr(out), wp, tp, nf, nt, _s(stream)), "attn_decode")
     return out
 
 

@@ -341,10 +341,13 @@ class DeviceModel:
         dw, s = self.dw, self.spec
         n, d = x.shape
         h = Fn.layer_norm(x, (d,), eps=1e-5)
-        q, k, v = self._lin(h, dw.qkv[layer]).split(d, dim=-1)
-        H = s.n_heads
+        kvd = s.kv_dim
+        q, k, v = self._lin(h, dw.qkv[layer]).split([d, kvd, kvd], dim=-1)
+        H, Hk = s.n_heads, s.kv_heads
         hd = d // H
-        qh, kh, vh = (t.reshape(n, H, hd).transpose(0, 1) for t in (q, k, v))
+        qh = q.reshape(n, H, hd).transpose(0, 1)
+        # grouped-query attention: query head h reads key/value head h // (H / Hk)
+        kh, vh = (t.reshape(n, Hk, hd).transpose(0, 1).repeat_interleave(H // Hk, dim=0) for t in (k, v))
         scores = (qh @ kh.transpose(1, 2)) / math.sqrt(hd)
         mask = torch.ones(n, n, dtype=torch.bool, device=x.device).triu(1)
         scores = scores.masked_fill(mask, float("-inf"))
@@ -406,10 +409,11 @@ class DecodeSession:
         s = model.spec
         self.m, self.B, self.max_len = model, batch, max_len
         dev = model.device
-        # head-major KV cache (L, B, H, max_len, head_dim): one head's positions
-        # are contiguous, so a (head, position-chunk) block is one bulk copy
-        H = s.n_heads
-        self.kc = torch.zeros(s.num_layers, batch, H, max_len, s.hidden_dim // H, device=dev, dtype=torch.float32)
+        # head-major KV cache (L, B, Hkv, max_len, head_dim): one key/value
+        # head's positions are contiguous, so a (head, position-chunk) block is
+        # one bulk copy (Hkv = kv_heads: fewer than the query heads under GQA)
+        self.kc = torch.zeros(s.num_layers, batch, s.kv_heads, max_len, s.hidden_dim // s.n_heads, device=dev,
+                              dtype=torch.float32)
         self.vc = torch.zeros_like(self.kc)
         self.pos = 0
 
@@ -420,13 +424,13 @@ class DecodeSession:
         dw = m.dw
         Bn = x.shape[0] // n
         d = s.hidden_dim
-        H = s.n_heads
+        H, Hk, kvd = s.n_heads, s.kv_heads, s.kv_dim
         hd = d // H
         h = Fn.layer_norm(x, (d,), eps=1e-5)
-        q, k, v = m._lin(h, dw.qkv[layer]).split(d, dim=-1)
-        q, k, v = (t.reshape(Bn, n, d) for t in (q, k, v))
-        kn = k.view(Bn, n, H, hd).transpose(1, 2)
-        vn = v.view(Bn, n, H, hd).transpose(1, 2)
+        q, k, v = m._lin(h, dw.qkv[layer]).split([d, kvd, kvd], dim=-1)
+        q = q.reshape(Bn, n, d)
+        kn = k.reshape(Bn, n, Hk, hd).transpose(1, 2)
+        vn = v.reshape(Bn, n, Hk, hd).transpose(1, 2)
         if rows is None:
             self.kc[layer, :, :, pos:pos + n] = kn
             self.vc[layer, :, :, pos:pos + n] = vn
@@ -445,9 +449,11 @@ class DecodeSession:
             mask = None if pos == 0 else \
                 torch.ones(n, pos + n, dtype=torch.bool, device=x.device).tril(pos)
             out = Fn.scaled_dot_product_attention(qh.to(dt), kh.to(dt), vh.to(dt), attn_mask=mask,
-                                                  is_causal=pos == 0)
+                                                  is_causal=pos == 0, enable_gqa=Hk != H)
             out = out.float().transpose(1, 2).reshape(Bn * n, d)
             return m._lin(out, dw.o[layer], resid=x)
+        if Hk != H:
+            kh, vh = kh.repeat_interleave(H // Hk, dim=1), vh.repeat_interleave(H // Hk, dim=1)
         scores = (qh @ kh.transpose(-1, -2)) / math.sqrt(hd)
         attn = torch.softmax(scores, dim=-1)
         out = (attn @ vh).transpose(1, 2).reshape(Bn * n, d)

@@ -3,8 +3,8 @@
 Real shapes come from the public model configs; the reference
 itself only builds the toy C1.  Deviations from the original models, kept so
 the MoBiLE layer semantics stay the reference's: LayerNorm without affine,
-sinusoidal positions, full multi-head attention (Mixtral's GQA K/V heads are
-modelled as full heads), selected-softmax gating (toymoe.py:201; the HF models
+no rotary positions, grouped-query attention where the model has it (Mixtral:
+8 key/value heads for 32 query heads), selected-softmax gating (toymoe.py:201; the HF models
 use softmax-over-all, available as gate_norm="softmax_all"), DeepSeek's one
 dense first layer omitted (27 MoE layers).
 
@@ -38,7 +38,8 @@ DEEPSEEK_MOE_16B = ModelSpec(num_layers=27, num_experts=64, k_big=6, k_little=3,
                              dtype="bfloat16", seed=0, embed_scale=1.0, pos_encoding="none")
 
 MIXTRAL_8X7B = ModelSpec(num_layers=32, num_experts=8, k_big=2, k_little=1, hidden_dim=4096, vocab_size=32000,
-                         ffn_dim=14336, activation="swiglu", n_heads=32, dtype="bfloat16", seed=0, embed_scale=1.0, pos_encoding="none")
+                         ffn_dim=14336, activation="swiglu", n_heads=32, n_kv_heads=8, dtype="bfloat16", seed=0,
+                         embed_scale=1.0, pos_encoding="none")
 
 PRESETS = {"c1": C1_TINY, "c2": OLMOE, "c3": QWEN15_MOE, "c4": DEEPSEEK_MOE_16B, "c5": MIXTRAL_8X7B}
 NAMES = {"c1": "tiny (SPEC.md)", "c2": "OLMoE-1B-7B", "c3": "Qwen1.5-MoE-A2.7B", "c4": "DeepSeek-MoE-16B",

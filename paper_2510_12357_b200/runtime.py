@@ -79,7 +79,8 @@ class StepEngine:
         self.tok_host = torch.zeros(B, dtype=i32, pin_memory=True)
         self.x = torch.empty(B, d, dtype=f32, device=dev)
         self.ln = torch.empty(B, d, dtype=f32, device=dev)  # LN of the layer input (from embed / combine)
-        self.qkv = torch.empty(B, 3 * d, dtype=f32, device=dev)
+        self.qkv_rows = d + 2 * s.kv_dim  # [q | k | v] (k, v narrower under grouped-query attention)
+        self.qkv = torch.empty(B, self.qkv_rows, dtype=f32, device=dev)
         self.att = torch.empty(B, d, dtype=f32, device=dev)
         self.xa = torch.empty(B, d, dtype=f32, device=dev)
         # this engine's own split-KV workspace (its stream and graphs only)
@@ -123,7 +124,7 @@ class StepEngine:
         if self.gemm_path:
             return self._attn_gemm(l, x_in)
         wc = self.dm.moe.wcode
-        K.stream_gemv([K.sg_group(w_base=dw.qkv[l].data_ptr(), K=d, rows=3 * d, x=self.ln, dense_T=B,
+        K.stream_gemv([K.sg_group(w_base=dw.qkv[l].data_ptr(), K=d, rows=self.qkv_rows, x=self.ln, dense_T=B,
                                   out=self.qkv)], wc, B)
         K.attn_decode(self.qkv, self.sess.kc[l], self.sess.vc[l], self.pos, s.n_heads, out=self.att, ws=self.attn_ws)
         K.stream_gemv([K.sg_group(w_base=dw.o[l].data_ptr(), K=d, rows=d, x=self.att, dense_T=B, out=self.xa,
@@ -142,7 +143,7 @@ class StepEngine:
         f32 accumulate), the O projection accumulated onto the residual."""
         dw, d, B = self.dm.dw, self.spec.hidden_dim, self.B
         K.gather_bf16(self.ln, None, 1, B, self.xb)
-        self._dense_gemm(dw.qkv[l], 3 * d, self.qkv, K.GG_STORE_F32)
+        self._dense_gemm(dw.qkv[l], self.qkv_rows, self.qkv, K.GG_STORE_F32)
         K.attn_decode(self.qkv, self.sess.kc[l], self.sess.vc[l], self.pos, self.spec.n_heads, out=self.att,
                       ws=self.attn_ws)
         K.gather_bf16(self.att, None, 1, B, self.xb)
@@ -226,6 +227,7 @@ class StepEngine:
         for kd in KINDS:
             m = N.mobile_dp_model()
             m.B, m.L, m.d, m.H, m.V, m.E, m.k = B, L, d, s.n_heads, s.vocab_size, E, self.k[kd]
+            m.Hkv = s.kv_heads
             m.n_shared, m.n_gate, m.ffn, m.shared_ffn = S, ng, s.ffn, s.shared_ffn if S else 0
             m.activation = self.dm.moe.act
             m.gate_norm = self.dm.moe.gate_norm

@@ -18,7 +18,8 @@ same rows).
            W13 = (2I, d) SwiGLU gate/up rows interleaved in groups of 8+8
                  (or (I, d) = W_in^T for ReLU), W2 = (d, I) = W_out^T
   shared   (L, S, Ps)           same packing with the shared ffn dim
-  qkv      (L, 3d, d)           [Wq^T; Wk^T; Wv^T] (one GEMV per layer)
+  qkv      (L, d + 2 kvd, d)    [Wq^T; Wk^T; Wv^T] (one GEMV per layer; kvd = kv_heads x head_dim,
+                                = d without grouped-query attention)
   o        (L, d, d)            Wo^T
   head     (V, d)               = head^T
   embed    (V, d) f32
@@ -202,7 +203,7 @@ class DeviceWeights:
             return t.to(dtype)
 
         dw.embed = U(V, d, fan_in=1.0 / spec.embed_scale**2 if spec.embed_scale else d, dtype=torch.float32)
-        dw.qkv = U(L, 3 * d, d)
+        dw.qkv = U(L, d + 2 * spec.kv_dim, d)
         dw.o = U(L, d, d)
         dw.router = U(L, E + dw.n_gate_rows, d)
         dw.head = U(V, d)

@@ -31,8 +31,8 @@ for name in sys.argv[1:] or ["c3", "c2"]:
             eng.step(False, next_token=i + 5)
         for kd in ("little", "big", "full"):
             k = eng.k[kd]
-            per_layer = (4 * d * d + (spec.num_experts + dw.n_gate_rows) * d) * eb + k * dw.expert_bytes \
-                + spec.n_shared * dw.shared_bytes + 2 * ctx * d * 4
+            per_layer = (2 * d * d + 2 * d * spec.kv_dim + (spec.num_experts + dw.n_gate_rows) * d) * eb + k * dw.expert_bytes \
+                + spec.n_shared * dw.shared_bytes + 2 * ctx * spec.kv_dim * 4
             tot = L * per_layer + spec.vocab_size * d * eb
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

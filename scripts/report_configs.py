@@ -34,8 +34,8 @@ BATCHES = {"c4": (1, 2, 4, 8, 64, 256)}
 def pass_bytes(spec, dw, kind_k, ctx, B):
     eb, d, L = dw.elem_bytes, spec.hidden_dim, spec.num_layers
     experts = min(spec.num_experts, B * kind_k) * dw.expert_bytes
-    per_layer = (4 * d * d + (spec.num_experts + dw.n_gate_rows) * d) * eb + experts + spec.n_shared * dw.shared_bytes \
-        + B * 2 * ctx * d * 4
+    per_layer = (2 * d * d + 2 * d * spec.kv_dim + (spec.num_experts + dw.n_gate_rows) * d) * eb + experts + spec.n_shared * dw.shared_bytes \
+        + B * 2 * ctx * spec.kv_dim * 4
     return L * per_layer + spec.vocab_size * d * eb
 
 

@@ -100,8 +100,9 @@ def device_oracle(dw) -> R.OracleWeights:
     W.spec = oracle_spec_from(spec)
     W.embed = _Embed(dw.embed)
     W.attn_q = _PerLayer(lambda l: np.ascontiguousarray(_np(dw.qkv[l, :d]).T))
-    W.attn_k = _PerLayer(lambda l: np.ascontiguousarray(_np(dw.qkv[l, d:2 * d]).T))
-    W.attn_v = _PerLayer(lambda l: np.ascontiguousarray(_np(dw.qkv[l, 2 * d:]).T))
+    kvd = dw.spec.kv_dim
+    W.attn_k = _PerLayer(lambda l: np.ascontiguousarray(_np(dw.qkv[l, d:d + kvd]).T))
+    W.attn_v = _PerLayer(lambda l: np.ascontiguousarray(_np(dw.qkv[l, d + kvd:]).T))
     W.attn_o = _PerLayer(lambda l: np.ascontiguousarray(_np(dw.o[l]).T))
     W.router = _PerLayer(lambda l: np.ascontiguousarray(_np(dw.router[l, :E]).T))
     store = dw.experts if dw.experts is not None else dw.host_experts

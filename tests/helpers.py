@@ -89,3 +89,6 @@ def _agree(got, want, logits, tol):
     return True, near
 
 QWEN_MINI_NOPE = dict(QWEN_MINI, embed_scale=1.0, pos_encoding="none", seed=9)
+# grouped-query attention (Mixtral-style: 2 key/value heads for 4 query heads), head_dim 32
+GQA_MINI = dict(num_layers=2, num_experts=8, k_big=2, k_little=1, hidden_dim=128, vocab_size=320, seed=11, ffn_dim=128,
+                activation="swiglu", n_heads=4, n_kv_heads=2, embed_scale=1.0, pos_encoding="none")

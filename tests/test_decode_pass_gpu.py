@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 import torch
 
-from tests.helpers import OLMOE_MINI, QWEN_MINI, matched, selections_agree
+from tests.helpers import GQA_MINI, OLMOE_MINI, QWEN_MINI, matched, selections_agree
 from tests.test_runtime_gpu import _oracle
 
 pytestmark = pytest.mark.gpu
@@ -14,7 +14,8 @@ pytestmark = pytest.mark.gpu
 TOY = dict(num_layers=2, num_experts=16, k_big=4, k_little=2, hidden_dim=256, vocab_size=256, seed=0)
 
 
-@pytest.mark.parametrize("spec_kw,dtype", [(TOY, "float32"), (OLMOE_MINI, "bfloat16"), (QWEN_MINI, "float32")])
+@pytest.mark.parametrize("spec_kw,dtype", [(TOY, "float32"), (OLMOE_MINI, "bfloat16"), (QWEN_MINI, "float32"),
+                                           (GQA_MINI, "bfloat16")])
 @pytest.mark.parametrize("full", [False, True])
 def test_persistent_matches_oracle(cuda_ok, spec_kw, dtype, full):
     from paper_2510_12357_b200.runtime import StepEngine

@@ -330,20 +330,24 @@ def test_logits_confidence_vs_torch(cuda_ok, T, V):
     assert (out["fallback"].cpu().bool() == (out["conf"].cpu() <= gamma)).all()
 
 
-@pytest.mark.parametrize("B,H,hd,max_len,pos", [(1, 16, 128, 1024, [700]), (2, 4, 64, 512, [5, 400]),
-                                                (1, 32, 128, 2100, [2047]), (3, 2, 128, 256, [0, 1, 255]),
-                                                (8, 16, 128, 64, [10, 20, 30, 40, 50, 60, 63, 0])])
-def test_attn_decode_vs_torch(cuda_ok, B, H, hd, max_len, pos):
+@pytest.mark.parametrize("B,H,Hkv,hd,max_len,pos", [(1, 16, 16, 128, 1024, [700]), (2, 4, 4, 64, 512, [5, 400]),
+                                                    (1, 32, 32, 128, 2100, [2047]), (3, 2, 2, 128, 256, [0, 1, 255]),
+                                                    (8, 16, 16, 128, 64, [10, 20, 30, 40, 50, 60, 63, 0]),
+                                                    (1, 32, 8, 128, 2100, [2047]), (2, 8, 2, 64, 300, [0, 299]),
+                                                    (2, 4, 1, 96, 40, [7, 39])])
+def test_attn_decode_vs_torch(cuda_ok, B, H, Hkv, hd, max_len, pos):
     """KV-cache attention at one new position per sequence (head-major cache):
     the new K/V rows land in the cache, output = softmax(q K^T / sqrt(hd)) V
     over positions 0..pos -- with and without the split-KV path (few
-    (sequence, head) pairs on a long cache), empty splits included."""
+    (sequence, head) pairs on a long cache), empty splits included; grouped-
+    query attention (Hkv < H: query head h reads key/value head h / (H/Hkv);
+    hd = 96 runs the general kernel)."""
     from paper_2510_12357_b200 import kernels as K
-    d = H * hd
+    d, kvd = H * hd, Hkv * hd
     g = torch.Generator(device="cuda").manual_seed(B * 100 + H)
-    kc = torch.randn(B, H, max_len, hd, device="cuda", generator=g)
-    vc = torch.randn(B, H, max_len, hd, device="cuda", generator=g)
-    qkv = torch.randn(B, 3 * d, device="cuda", generator=g)
+    kc = torch.randn(B, Hkv, max_len, hd, device="cuda", generator=g)
+    vc = torch.randn(B, Hkv, max_len, hd, device="cuda", generator=g)
+    qkv = torch.randn(B, d + 2 * kvd, device="cuda", generator=g)
     p = torch.tensor(pos, dtype=torch.int32, device="cuda")
     kc0, vc0 = kc.clone(), vc.clone()
     out = torch.empty(B, d, device="cuda")
@@ -357,11 +361,14 @@ def test_attn_decode_vs_torch(cuda_ok, B, H, hd, max_len, pos):
         if w is not None:
             assert int(w[1].abs().sum()) == 0
         for b in range(B):
-            q, k, v = qkv[b, :d].view(H, hd), qkv[b, d:2 * d].view(H, hd), qkv[b, 2 * d:].view(H, hd)
+            q = qkv[b, :d].view(H, hd)
+            k, v = qkv[b, d:d + kvd].view(Hkv, hd), qkv[b, d + kvd:].view(Hkv, hd)
             kk, vv = kc0[b].clone(), vc0[b].clone()
             kk[:, pos[b]] = k
             vv[:, pos[b]] = v
             assert torch.equal(kc[b, :, pos[b]], k) and torch.equal(vc[b, :, pos[b]], v)
-            sc = torch.einsum("hd,hpd->hp", q.double(), kk[:, :pos[b] + 1].double()) / hd ** 0.5
-            want = torch.einsum("hp,hpd->hd", torch.softmax(sc, dim=-1), vv[:, :pos[b] + 1].double()).reshape(d)
+            kq = kk.repeat_interleave(H // Hkv, dim=0)[:, :pos[b] + 1].double()
+            vq = vv.repeat_interleave(H // Hkv, dim=0)[:, :pos[b] + 1].double()
+            sc = torch.einsum("hd,hpd->hp", q.double(), kq) / hd ** 0.5
+            want = torch.einsum("hp,hpd->hd", torch.softmax(sc, dim=-1), vq).reshape(d)
             assert torch.allclose(out[b].double(), want, rtol=1e-4, atol=1e-5), (b, (out[b].double() - want).abs().max())

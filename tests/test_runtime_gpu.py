@@ -4,7 +4,7 @@ import pytest
 import torch
 
 from oracle import moe_ref as R
-from tests.helpers import DSEEK_MINI, QWEN_MINI, QWEN_MINI_NOPE, matched, selections_agree
+from tests.helpers import DSEEK_MINI, GQA_MINI, QWEN_MINI, QWEN_MINI_NOPE, matched, selections_agree
 
 pytestmark = pytest.mark.gpu
 
@@ -45,7 +45,7 @@ def _offload_dm(dm, ms):
 
 @pytest.mark.parametrize("persistent", [False, True])
 @pytest.mark.parametrize("mode", ["resident", "offload"])
-@pytest.mark.parametrize("spec_kw", [QWEN_MINI, DSEEK_MINI, QWEN_MINI_NOPE])
+@pytest.mark.parametrize("spec_kw", [QWEN_MINI, DSEEK_MINI, QWEN_MINI_NOPE, GQA_MINI])
 @pytest.mark.parametrize("full", [False, True])
 def test_step_engine_matches_oracle(cuda_ok, mode, spec_kw, full, persistent):
     from paper_2510_12357_b200.offload import OffloadRuntime
