@@ -498,7 +498,21 @@ def ep_block(args, ws, rank, dev, P):
     p_any = 1.0 - (1.0 - r) ** B
     t_mob = ms["little"] + p_any * ms["big"]  # conservative: the big pass over the whole batch
     eng.close()
-    del eng, local, dm, dw
+    del eng
+    # expert-parallel prefill: a 512-token prompt per rank through the session
+    # path with every MoE layer's experts exchanged (wall clock, max over ranks)
+    pe = EPStepEngine(dm, local, 1, ctx + 8, group=group, graphs=False)
+    prompt = torch.randint(1, spec.vocab_size, (ctx + 1,), generator=torch.Generator().manual_seed(5 + rank)).tolist()
+    pe.prefill(prompt)  # warm-up (TMA descriptors, the prompt-sized exchange)
+    barrier(ws)
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    pe.prefill(prompt)
+    torch.cuda.synchronize()
+    t_pf = max_over_ranks(ws, time.perf_counter() - w0, dev)
+    pe.close()
+    del pe
+    del local, dm, dw
     torch.cuda.empty_cache()
     return {"workload": f"C4 DeepSeek-MoE-16B shape, batched decode, {B} sequences per rank, context {ctx}, "
                         f"expert-parallel over {ws} rank(s) (experts {lo}-{hi - 1} on rank {rank})",
@@ -508,6 +522,9 @@ def ep_block(args, ws, rank, dev, P):
             "full_topk_tokens_s": round(ws * B / ms["full"] * 1e3, 1),
             "speedup_vs_full_topk": round(ms["full"] / t_mob, 4), "r": r, "p_any_fallback": round(p_any, 4),
             "exchange_ms_per_little_pass": legs,
+            "prefill": {"tokens_per_rank": ctx, "ms": round(t_pf * 1e3, 2), "tokens_s": round(ws * ctx / t_pf, 1),
+                        "note": "EPStepEngine.prefill: the prompt through the session path, every MoE layer's "
+                                "experts exchanged; wall clock max over ranks"},
             "note": "pass times max over ranks; MoBiLE = little + P(any row falls back) x big (whole-batch replay); "
                     "exchange legs from an eager pass (CUDA events on the engine stream)"}
 

@@ -334,6 +334,12 @@ class P2PExpertParallelMoE(ExpertParallelMoE):
         self.x = P2PExchange(E, d, cap, group, bf16_rows=local_moe.tc_ok)
 
     def forward(self, x, layer, k_tok, k_max, replay=None, replay_mask=None, reuse_gates=False, ln_out=None):
+        return self.forward_sc(x, layer, k_tok, k_max, replay=replay, replay_mask=replay_mask,
+                               reuse_gates=reuse_gates, ln_out=ln_out)[0]
+
+    def forward_sc(self, x, layer, k_tok, k_max, replay=None, replay_mask=None, reuse_gates=False, ln_out=None):
+        """forward() plus the router scratch (logits, selections): the
+        DecodeSession layer interface (MoBiLEMoE.forward)."""
         from . import kernels as K
         rm = self.router_moe
         sc = rm.route(x, layer, k_tok, k_max, replay=replay, replay_mask=replay_mask, reuse_gates=reuse_gates)
@@ -345,7 +351,7 @@ class P2PExpertParallelMoE(ExpertParallelMoE):
         Y = self.x.exchange(r["h2"], r["idx"], k_tok, experts)
         Ys = rm.shared_rows(layer, r["h2"], sc) if rm.S else None
         shared_logits = r["extra"] if rm.dw.n_gate_rows else None
-        return K.combine(x, Y, r["gates"], k_tok, Ys, rm.S, shared_logits, ln_out=ln_out)
+        return K.combine(x, Y, r["gates"], k_tok, Ys, rm.S, shared_logits, ln_out=ln_out), sc
 
 
 
@@ -373,6 +379,8 @@ class EPStepEngine(StepEngine):
         super().__init__(dm, batch, max_len, graphs=graphs, persistent=False, gemm=gemm)
         s = dm.spec
         self.ep_local = local
+        self.ep_group = group
+        self._pf = None  # prompt-sized exchange (prefill), created on first use
         self.xch = P2PExchange(s.num_experts, s.hidden_dim, batch * s.k_big, group, dm.device, bf16_rows=local.tc_ok)
         self.ex_timer: ExchangeTimer | None = None  # eager mode: CUDA events around the exchange legs
 
@@ -390,5 +398,27 @@ class EPStepEngine(StepEngine):
         shared_logits = r["extra"] if rm.dw.n_gate_rows else None
         return K.combine(self.xa, Y, r["gates"], k_tok, Ys, rm.S, shared_logits, x_out=sc["x_out"], ln_out=self.ln)
 
+    def prefill(self, prompt: list[int], prefill_k: int | None = None):
+        """The prompt through the session path with the MoE layers expert-
+        parallel (collective: every rank prefills, in lockstep); the exchange
+        for prompt-sized batches is created on first use (capacity = the
+        prompt's pairs)."""
+        s = self.spec
+        n = max(len(prompt) - 1, 1)
+        kpf = s.k_big if prefill_k is None else prefill_k
+        if self._pf is None or self._pf.x.cap < n * kpf:
+            if self._pf is not None:
+                self._pf.x.close()
+            self._pf = P2PExpertParallelMoE(self.dm.moe, self.ep_local, s.num_experts, s.hidden_dim, cap=n * kpf,
+                                            group=self.ep_group)
+        self.sess.moe_forward = self._pf.forward_sc
+        try:
+            super().prefill(prompt, prefill_k)
+        finally:
+            self.sess.moe_forward = None
+
     def close(self):
         self.xch.close()
+        if self._pf is not None:
+            self._pf.x.close()
+            self._pf = None

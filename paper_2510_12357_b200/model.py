@@ -416,6 +416,7 @@ class DecodeSession:
                               dtype=torch.float32)
         self.vc = torch.zeros_like(self.kc)
         self.pos = 0
+        self.moe_forward = None  # optional MoE layer override (expert parallelism: ep.EPStepEngine.prefill)
 
     def _attn_step(self, x: torch.Tensor, layer: int, rows: torch.Tensor | None, pos: int, n: int):
         """Attention for n new positions [pos, pos+n) of the sequences `rows`
@@ -484,8 +485,12 @@ class DecodeSession:
             x = self._attn_step(x, layer, rows, pos, n)
             if replay is not None:
                 rep_full[last] = replay[layer]
-            x_new, sc = m.moe.forward(x, layer, k_tok, k_max, replay=rep_full, replay_mask=rep_mask_full,
-                                      reuse_gates=reuse_gates, hook=expert_hook, timer=timer)
+            if self.moe_forward is not None:  # expert-parallel layer (ep.py): (x_new, scratch)
+                x_new, sc = self.moe_forward(x, layer, k_tok, k_max, replay=rep_full, replay_mask=rep_mask_full,
+                                             reuse_gates=reuse_gates)
+            else:
+                x_new, sc = m.moe.forward(x, layer, k_tok, k_max, replay=rep_full, replay_mask=rep_mask_full,
+                                          reuse_gates=reuse_gates, hook=expert_hook, timer=timer)
             lg = sc["router"]["logits"].view(Bn, n, s.num_experts)
             states[layer] = lg[:, -1]
             idx[layer] = sc["router"]["idx"].view(Bn, n, k_max)[:, -1]

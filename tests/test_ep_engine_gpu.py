@@ -106,6 +106,33 @@ def _engine_case(rank, world, groups, B, steps=4):
     return bad
 
 
+def _prefill_case(rank, world, groups, n):
+    """EP prefill (the session path with the layers' experts exchanged) of an
+    n-token prompt: every layer's K/V cache rows identical for world 1 / 2."""
+    from paper_2510_12357_b200.ep import EPStepEngine, partition
+    from paper_2510_12357_b200.model import MoBiLEMoE
+    _, ms, dm = matched(QWEN_MINI, "bfloat16")
+    lo, hi = partition(ms.num_experts, world)[rank]
+    e2 = EPStepEngine(dm, MoBiLEMoE(dm.dw.shard_experts(lo, hi)), 1, 64, group=groups["world"], graphs=False)
+    e1 = EPStepEngine(dm, MoBiLEMoE(dm.dw.shard_experts(0, ms.num_experts)), 1, 64, group=groups["self"],
+                      graphs=False)
+    prompt = np.random.default_rng(5 + rank).integers(1, ms.vocab_size, size=n).tolist()
+    bad = []
+    try:
+        e2.prefill(prompt)
+        e1.prefill(prompt)
+        torch.cuda.synchronize()
+        for name in ("kc", "vc"):
+            a, b = getattr(e2.sess, name), getattr(e1.sess, name)
+            if not torch.equal(a, b):
+                bad.append((name, (a - b).abs().max().item()))
+        assert int(e2._pf.x.flags.item()) == 0
+    finally:
+        e2.close()
+        e1.close()
+    return bad
+
+
 def _worker(rank, world, port, case, arg, q):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -114,7 +141,7 @@ def _worker(rank, world, port, case, arg, q):
     try:
         selfs = [dist.new_group([r]) for r in range(world)]  # collective: every rank creates every group
         groups = {"world": dist.group.WORLD, "self": selfs[rank]}
-        fn = _layer_case if case == "layer" else _engine_case
+        fn = {"layer": _layer_case, "engine": _engine_case, "prefill": _prefill_case}[case]
         q.put((rank, fn(rank, world, groups, arg), None))
     except Exception as exc:  # noqa: BLE001
         import traceback
@@ -147,6 +174,13 @@ def test_ep_layer_bit_identical_world1_vs_world2(cuda_ok, T):
 @pytest.mark.parametrize("B", [1, 8])
 def test_ep_engine_bit_identical_world1_vs_world2(cuda_ok, B):
     for rank, bad, exc in _spawn("engine", B):
+        assert exc is None, (rank, exc)
+        assert bad == [], (rank, bad)
+
+
+@pytest.mark.parametrize("n", [2, 17])
+def test_ep_prefill_bit_identical_world1_vs_world2(cuda_ok, n):
+    for rank, bad, exc in _spawn("prefill", n):
         assert exc is None, (rank, exc)
         assert bad == [], (rank, bad)
 
