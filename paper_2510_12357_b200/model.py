@@ -45,7 +45,7 @@ def positional(n: int, d: int, start: int, device) -> torch.Tensor:
     """Sinusoidal encoding, toymoe.py:135-140 (computed in fp64, stored f32)."""
     pos = torch.arange(start, start + n, device=device, dtype=torch.float64)[:, None]
     dim = torch.arange(d, device=device, dtype=torch.float64)[None, :]
-    angle = pos / torch.pow(torch.tensor(10000.0, dtype=torch.float64, device=device), (2 * (dim // 2)) / d)
+    angle = pos / torch.pow(10000.0, (2 * (dim // 2)) / d)  # scalar base: no host copy (graph-capturable)
     return torch.where(dim.long() % 2 == 0, torch.sin(angle), torch.cos(angle)).to(torch.float32)
 
 

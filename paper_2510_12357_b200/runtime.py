@@ -104,6 +104,8 @@ class StepEngine:
         if runtime is not None:
             self.active_host = torch.zeros(L, E + 1, dtype=i32, pin_memory=True)
         self.reuse_gates = False
+        self.prefill_graphs = True  # capture one prefill graph per prompt length (resident experts)
+        self._pf_graphs: dict = {}
         self.timer = None  # kernel timer (eager mode only: events are not graph nodes here)
         # persistent decode-pass kernel (decode_pass.cu): one launch per pass /
         # offload segment.  None = use it whenever the shape is supported.
@@ -492,14 +494,38 @@ class StepEngine:
         ctx = list(prompt[:-1])
         self.sess.pos = 0
         if ctx:
-            t = torch.tensor([ctx], dtype=torch.long, device=self.dm.device)
-            k = torch.full((len(ctx),), kpf, dtype=torch.int32, device=self.dm.device)
-            hook = self.rt.demand_hook("prefill") if self.rt else None
-            with torch.cuda.stream(self.stream):
-                self.sess.run(t, k, kpf, expert_hook=hook)
-            if self.rt:
-                self.stream.synchronize()
-                self.rt.token_end()
+            n = len(ctx)
+            # resident experts: the prompt's kernels are one CUDA graph per
+            # prompt length (captured after the first eager prefill of that
+            # length; the prompt ids are read from a static device buffer)
+            key = (n, kpf)
+            capturable = (self.use_graphs and self.rt is None and self.sess.moe_forward is None
+                          and self.prefill_graphs)
+            if capturable and key in self._pf_graphs:
+                g, tbuf = self._pf_graphs[key]
+                tbuf.copy_(torch.tensor([ctx], dtype=torch.long), non_blocking=False)
+                self.stream.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(self.stream):
+                    g.replay()
+                self.sess.pos = n
+            else:
+                t = torch.tensor([ctx], dtype=torch.long, device=self.dm.device)
+                k = torch.full((n,), kpf, dtype=torch.int32, device=self.dm.device)
+                hook = self.rt.demand_hook("prefill") if self.rt else None
+                with torch.cuda.stream(self.stream):
+                    self.sess.run(t, k, kpf, expert_hook=hook)
+                if self.rt:
+                    self.stream.synchronize()
+                    self.rt.token_end()
+                if capturable:  # capture this length for the next prefills (the eager run warmed it up)
+                    self.stream.synchronize()
+                    tbuf = t.clone()
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=self.stream):
+                        self.sess.pos = 0
+                        self.sess.run(tbuf, k, kpf)
+                    self._pf_graphs[key] = (g, tbuf)
+                    self.sess.pos = n
         self.pos.fill_(len(ctx))
         self.tok.fill_(prompt[-1])
         torch.cuda.synchronize()

@@ -1,4 +1,6 @@
-"""One prefill (per-op engine) for an ncu launch list.  python scripts/prof_prefill.py c5 2048"""
+"""One prefill (per-op engine) for an ncu launch list (the second prefill,
+between cudaProfilerStart/Stop):
+    ncu --profile-from-start off --metrics gpu__time_duration.sum ... python scripts/prof_prefill.py c5 2048"""
 import sys
 from pathlib import Path
 
@@ -16,6 +18,10 @@ spec = PRESETS[name]
 dm = DeviceModel(DeviceWeights.random(spec, torch.device("cuda"), seed=0))
 eng = StepEngine(dm, 1, n + 8, persistent=False)
 prompt = np.random.default_rng(0).integers(1, spec.vocab_size, size=n + 1).tolist()
+eng.prefill(prompt)  # warm-up
+torch.cuda.synchronize()
+torch.cuda.profiler.start()  # ncu --profile-from-start off: only the second prefill
 eng.prefill(prompt)
 torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("ok")

@@ -89,3 +89,25 @@ def test_step_engine_confidence_rule(cuda_ok):
             tok, fb = eng.step()
             conf = eng.head["little"]["conf"].item()
             assert fb == (conf <= gamma)
+
+
+def test_graph_prefill_equals_eager(cuda_ok):
+    """A prompt length seen before replays its captured prefill graph (prompt
+    ids from a static buffer): KV caches and the following step identical to
+    an eager prefill of the same prompt."""
+    from paper_2510_12357_b200.runtime import StepEngine
+    _, ms, dm = matched(QWEN_MINI, "bfloat16")
+    a = StepEngine(dm, 1, 64, persistent=False).build()
+    b = StepEngine(dm, 1, 64, persistent=False).build()
+    b.prefill_graphs = False
+    a.prefill([5, 9, 13, 2, 7, 1])       # eager + capture (length 5)
+    a.prefill([3, 17, 42, 8, 11, 4])     # graph replay, other ids
+    assert (5, ms.k_big) in a._pf_graphs
+    b.prefill([3, 17, 42, 8, 11, 4])     # eager
+    torch.cuda.synchronize()
+    assert a.sess.pos == b.sess.pos == 5
+    assert torch.equal(a.sess.kc[:, :, :, :5], b.sess.kc[:, :, :, :5])
+    assert torch.equal(a.sess.vc[:, :, :, :5], b.sess.vc[:, :, :, :5])
+    ta, _ = a.step(False, next_token=6)
+    tb, _ = b.step(False, next_token=6)
+    assert ta == tb and torch.equal(a.states["little"], b.states["little"])
