@@ -671,12 +671,12 @@ def c1_line(n_tokens=24):
     kw = dict(num_layers=2, num_experts=16, k_big=4, k_little=2, hidden_dim=256, vocab_size=256, seed=0)
     prompt = [3, 17, 42, 5]
     rm = RT.build_model(RC.ModelSpec(**kw))
-    RT.generate(rm, prompt, RC.PolicySpec(), 2)  # warm-up
+    RT.generate(rm, prompt, RC.PolicySpec(), n_tokens)  # warm-up: the same lengths as the timed run
     w0 = time.perf_counter()
     rt, rd = RT.generate(rm, prompt, RC.PolicySpec(), n_tokens)
     t_ref = time.perf_counter() - w0
     om = M.build_model(M.ModelSpec(**kw))
-    M.generate(om, prompt, M.PolicySpec(), 2)  # warm-up
+    M.generate(om, prompt, M.PolicySpec(), n_tokens)  # warm-up: every prefix length once (first-shape costs)
     torch.cuda.synchronize()
     w0 = time.perf_counter()
     ot, od = M.generate(om, prompt, M.PolicySpec(), n_tokens)
