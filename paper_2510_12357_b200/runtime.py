@@ -38,6 +38,7 @@ KINDS = ("little", "big", "full")
 GEMV_MAX_BATCH = 4  # largest batch on the GEMV decode path (stream GEMV / persistent pass tile)
 GEMM_MIN_BATCH = 3  # resident bf16 decode switches to the GEMM path from here (profiles/r1_configs.json)
 MAX_BATCH = 1024
+PREFILL_GRAPHS_MAX = 4  # captured prefill graphs kept per engine (one per prompt length, oldest dropped)
 
 
 class StepEngine:
@@ -525,6 +526,8 @@ class StepEngine:
                         self.sess.pos = 0
                         self.sess.run(tbuf, k, kpf)
                     self._pf_graphs[key] = (g, tbuf)
+                    while len(self._pf_graphs) > PREFILL_GRAPHS_MAX:  # bounded: drop the oldest length
+                        self._pf_graphs.pop(next(iter(self._pf_graphs)))
                     self.sess.pos = n
         self.pos.fill_(len(ctx))
         self.tok.fill_(prompt[-1])
