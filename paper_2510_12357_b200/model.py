@@ -136,7 +136,7 @@ class MoBiLEMoE:
         return dict(sc, router=r)
 
     def experts(self, x: torch.Tensor, layer: int, sc: dict, k_tok: torch.Tensor, k_max: int,
-                loc: ExpertLocation | None = None, timer=None, ln_out=None) -> torch.Tensor:
+                loc: ExpertLocation | None = None, timer=None, ln_out=None, x_out=None) -> torch.Tensor:
         """Grouped expert FFN + shared experts + combine/residual (toymoe.py:202-207).
 
         Decode (T < TC_MIN_TOKENS): bulk-copy streaming GEMV launches (gate-up
@@ -153,8 +153,9 @@ class MoBiLEMoE:
             self._stream_ffn(r["h2"], sc["perm"], layer, T, k_max, loc, sc, timer)
             Ys = sc["Ys"] if self.S else None
         shared_logits = r["extra"] if self.dw.n_gate_rows else None
-        K.combine(x, sc["Y"], r["gates"], k_tok, Ys, self.S, shared_logits, x_out=sc["x_out"], ln_out=ln_out)
-        return sc["x_out"]
+        out = sc["x_out"] if x_out is None else x_out
+        K.combine(x, sc["Y"], r["gates"], k_tok, Ys, self.S, shared_logits, x_out=out, ln_out=ln_out)
+        return out
 
     def _stream_ffn(self, h2, p, layer, T, k_max, loc, sc, timer=None, shared=True):
         """Decode FFN on the bulk-copy engine: writes sc["Y"] (and sc["Ys"])."""
@@ -281,7 +282,7 @@ class MoBiLEMoE:
 
     def forward(self, x: torch.Tensor, layer: int, k_tok: torch.Tensor, k_max: int, *, replay=None,
                 replay_mask=None, reuse_gates=False, experts: ExpertLocation | None = None,
-                hook=None, timer=None):
+                hook=None, timer=None, x_out=None):
         """x (T, d) f32 residual -> (x_out, scratch): route, then experts.
 
         `hook` (optional) has `pre(layer, router_out, perm) -> ExpertLocation`,
@@ -293,7 +294,7 @@ class MoBiLEMoE:
         sc = self.route(x, layer, k_tok, k_max, replay=replay, replay_mask=replay_mask, reuse_gates=reuse_gates)
         if hook is not None:
             experts = hook.pre(layer, sc["router"], sc["perm"])
-        x_out = self.experts(x, layer, sc, k_tok, k_max, experts, timer)
+        x_out = self.experts(x, layer, sc, k_tok, k_max, experts, timer, x_out=x_out)
         if hook is not None:
             hook.post(layer)
         return x_out, sc
@@ -310,7 +311,8 @@ class DeviceModel:
         self.head_ws: dict = {}
 
     # ------------------------------------------------------------- pieces
-    def _lin(self, h: torch.Tensor, w: torch.Tensor, resid: torch.Tensor | None = None) -> torch.Tensor:
+    def _lin(self, h: torch.Tensor, w: torch.Tensor, resid: torch.Tensor | None = None,
+             resid_inplace: bool = False) -> torch.Tensor:
         """(resid +) h @ w.T for an out-major weight (N, d), on libmobile kernels:
         up to 8 rows the bulk-copy GEMV (f32 activations); more rows of a bf16
         model the tcgen05 grouped GEMM in dense mode (bf16 operands, f32
@@ -325,8 +327,8 @@ class DeviceModel:
         if w.dtype == torch.bfloat16 and d % 128 == 0 and n_out % 128 == 0:
             xb = torch.empty(n, d, dtype=torch.bfloat16, device=h.device)
             K.gather_bf16(h.contiguous(), None, 1, n, xb)
-            if resid is not None:
-                out, epi = resid.clone(), K.GG_ACCUM_F32
+            if resid is not None:  # accumulated in the GEMM epilogue (in place when the caller allows)
+                out, epi = (resid if resid_inplace else resid.clone()), K.GG_ACCUM_F32
             else:
                 out, epi = torch.empty(n, n_out, dtype=torch.float32, device=h.device), K.GG_STORE_F32
             K.grouped_gemm(xb, d, w.data_ptr(), w.numel() * w.element_size(), 1, n_out,
@@ -428,7 +430,8 @@ class DecodeSession:
         H, Hk, kvd = s.n_heads, s.kv_heads, s.kv_dim
         hd = d // H
         h = Fn.layer_norm(x, (d,), eps=1e-5)
-        q, k, v = m._lin(h, dw.qkv[layer]).split([d, kvd, kvd], dim=-1)
+        qkv = m._lin(h, dw.qkv[layer])
+        q, k, v = qkv.split([d, kvd, kvd], dim=-1)
         q = q.reshape(Bn, n, d)
         kn = k.reshape(Bn, n, Hk, hd).transpose(1, 2)
         vn = v.reshape(Bn, n, Hk, hd).transpose(1, 2)
@@ -447,12 +450,18 @@ class DecodeSession:
             # bounds the error -- memory-efficient f32 otherwise), causal with
             # the chunk's offset into the cache
             dt = torch.bfloat16 if dw.wdtype == torch.bfloat16 else torch.float32
-            mask = None if pos == 0 else \
-                torch.ones(n, pos + n, dtype=torch.bool, device=x.device).tril(pos)
-            out = Fn.scaled_dot_product_attention(qh.to(dt), kh.to(dt), vh.to(dt), attn_mask=mask,
-                                                  is_causal=pos == 0, enable_gqa=Hk != H)
+            if pos == 0 and rows is None:  # the whole context is this chunk: one conversion of the qkv rows
+                qkv_t = qkv.to(dt).view(Bn, n, d + 2 * kvd)
+                qs = qkv_t[..., :d].view(Bn, n, H, hd).transpose(1, 2)
+                ks = qkv_t[..., d:d + kvd].view(Bn, n, Hk, hd).transpose(1, 2)
+                vs = qkv_t[..., d + kvd:].view(Bn, n, Hk, hd).transpose(1, 2)
+                out = Fn.scaled_dot_product_attention(qs, ks, vs, is_causal=True, enable_gqa=Hk != H)
+            else:
+                mask = torch.ones(n, pos + n, dtype=torch.bool, device=x.device).tril(pos)
+                out = Fn.scaled_dot_product_attention(qh.to(dt), kh.to(dt), vh.to(dt), attn_mask=mask,
+                                                      enable_gqa=Hk != H)
             out = out.float().transpose(1, 2).reshape(Bn * n, d)
-            return m._lin(out, dw.o[layer], resid=x)
+            return m._lin(out, dw.o[layer], resid=x, resid_inplace=True)
         if Hk != H:
             kh, vh = kh.repeat_interleave(H // Hk, dim=1), vh.repeat_interleave(H // Hk, dim=1)
         scores = (qh @ kh.transpose(-1, -2)) / math.sqrt(hd)
@@ -479,6 +488,7 @@ class DecodeSession:
             rep_mask_full = torch.zeros(T, device=dev, dtype=torch.uint8)
             last = torch.arange(Bn, device=dev) * n + (n - 1)
             rep_mask_full[last] = replay_mask if replay_mask is not None else 1
+        spare = None  # the residual buffer the next combine writes
         for layer in range(s.num_layers):
             if layer_hook is not None:
                 layer_hook(layer)
@@ -488,13 +498,17 @@ class DecodeSession:
             if self.moe_forward is not None:  # expert-parallel layer (ep.py): (x_new, scratch)
                 x_new, sc = self.moe_forward(x, layer, k_tok, k_max, replay=rep_full, replay_mask=rep_mask_full,
                                              reuse_gates=reuse_gates)
-            else:
+                x_new = x_new.clone()
+            else:  # the combine writes the other of two residual buffers (no copy per layer)
+                if spare is None:
+                    spare = torch.empty_like(x)
                 x_new, sc = m.moe.forward(x, layer, k_tok, k_max, replay=rep_full, replay_mask=rep_mask_full,
-                                          reuse_gates=reuse_gates, hook=expert_hook, timer=timer)
+                                          reuse_gates=reuse_gates, hook=expert_hook, timer=timer, x_out=spare)
+                spare = x
             lg = sc["router"]["logits"].view(Bn, n, s.num_experts)
             states[layer] = lg[:, -1]
             idx[layer] = sc["router"]["idx"].view(Bn, n, k_max)[:, -1]
-            x = x_new.clone()
+            x = x_new
         if advance:
             self.pos += n
         x_last = x.view(Bn, n, s.hidden_dim)[:, -1].contiguous()
