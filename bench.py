@@ -532,7 +532,7 @@ def ep_block(args, ws, rank, dev, P):
 # ----------------------------------------------------------------------------- other configs
 R_PAPER = {"c2": 0.21, "c3": 0.11, "c4": 0.11, "c5": 0.11}  # PAPER.md: OLMoE 0.21, Qwen 0.11
 CTX = {"c2": 512, "c3": 512, "c4": 512, "c5": 2048}
-BATCHES = {"c2": (1,), "c4": (1, 64), "c5": (1,)}
+BATCHES = {"c2": (1,), "c4": (1, 8, 64, 256), "c5": (1,)}
 
 
 def config_sweep(args, dev, P):
