@@ -36,7 +36,7 @@ from .policy import plan_from_targets
 
 KINDS = ("little", "big", "full")
 GEMV_MAX_BATCH = 4  # largest batch on the GEMV decode path (stream GEMV / persistent pass tile)
-GEMM_MIN_BATCH = 3  # resident bf16 decode switches to the GEMM path from here (profiles/r1_configs.json)
+GEMM_MIN_BATCH = 5  # resident bf16 decode switches to the GEMM path from here (scripts/batch_paths.py, round 2)
 MAX_BATCH = 1024
 PREFILL_GRAPHS_MAX = 4  # captured prefill graphs kept per engine (one per prompt length, oldest dropped)
 
@@ -52,12 +52,14 @@ class StepEngine:
             gemm = batch > GEMV_MAX_BATCH or (batch >= GEMM_MIN_BATCH and runtime is None and dm.moe.tc_ok
                                               and persistent is not True)
         self.gemm_path = bool(gemm)
-        # resident batch 1: the per-op engine (graph-replayed, PDL-chained
-        # kernels; split-KV attention) beats the persistent pass on every
-        # config (scripts/batch_paths.py: C2 1.07 vs 1.29 ms, C3 1.94 vs 2.13,
-        # C4 1.92 vs 2.31, C5 4.61 vs 5.76 ms little pass); the persistent pass
-        # stays the default for B = 2 and for offloaded experts (zero-sync)
-        if persistent is None and runtime is None and batch == 1 and not self.gemm_path:
+        # resident batches 1, 3 and 4: the per-op engine (graph-replayed,
+        # PDL-chained kernels; split-KV attention) beats the persistent pass
+        # (scripts/batch_paths.py, round 2, little pass: C2 1.04 vs 1.18 ms,
+        # C3 1.89 vs 2.07, C4 1.89 vs 2.07 at B = 1; C4 4.58 vs 5.67 / 4.71 GEMM
+        # at B = 3, 5.83 vs 6.16 / 5.91 at B = 4); the persistent pass stays the
+        # default for B = 2 (C4 2.55 vs 2.92 ms) and for offloaded experts
+        # (zero-sync)
+        if persistent is None and runtime is None and batch != 2 and not self.gemm_path:
             persistent = False
         if self.gemm_path:
             if not dm.moe.tc_ok:
