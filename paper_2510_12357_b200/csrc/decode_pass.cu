@@ -79,7 +79,7 @@ struct Group {
   int K, rows, kind, epi, n_exp, xstage, units, out_ld, split;
 };
 
-struct Tmpl {
+struct alignas(16) Tmpl {  // 16-byte multiple: copied to shared memory as int4s
   int type, n_groups, xkind, xkind0, keep_x, end_bar, units, has_routed;
   const float* xsrc;    // XK_LN / XK_PLAIN source; XK_COMBINE_LN residual (xa)
   float* xdst;          // XK_COMBINE_LN / XK_EMBED_LN: where CTA 0 writes the new residual
@@ -138,6 +138,8 @@ struct Plan {
   int* diag;                  // optional mapped host int[16]: watchdog diagnostics (survive the trap)
   unsigned long long* evt;    // optional event log: per CTA and role (0 producer, 1 consumers) kEvt x {time, code}
 };
+
+static_assert(sizeof(Tmpl) % 16 == 0, "templates are copied as int4s (a 3-group template's tail was dropped)");
 
 struct Route {          // one layer's selection + permute, in shared memory (E <= 256)
   int n_active;
