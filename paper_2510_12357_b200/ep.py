@@ -375,10 +375,27 @@ class EPStepEngine(StepEngine):
     `local` is a MoBiLEMoE over this rank's expert block
     (DeviceWeights.shard_experts)."""
 
-    def __init__(self, dm, local, batch: int, max_len: int, group=None, graphs: bool = True, gemm=None):
+    def __init__(self, dm, local, batch: int, max_len: int, group=None, graphs: bool = True, gemm=None,
+                 shard_runtime=None):
+        """shard_runtime: an OffloadRuntime over this rank's expert shard (its
+        routed experts in pinned host memory behind the rank's own HBM expert
+        cache, so the cache capacity of the job is G x the per-rank budget).
+        The owner then reads back, per layer, which of its experts it
+        received (one small D2H + host sync, the on-demand protocol of
+        engine.py:243-244 on the owner), requests + pins them in its cache,
+        copies the misses and runs its rows from the cache slots; eager
+        passes only (the host sits between the exchange's legs)."""
+        if shard_runtime is not None:
+            graphs = False
         super().__init__(dm, batch, max_len, graphs=graphs, persistent=False, gemm=gemm)
         s = dm.spec
         self.ep_local = local
+        self.ep_rt = shard_runtime
+        if shard_runtime is not None:
+            cap = batch * s.k_big
+            G = dist.get_world_size(group) if dist.is_initialized() else 1
+            self._ids_h = torch.zeros(G * cap, dtype=torch.int32, pin_memory=True)
+            self._kin_h = torch.zeros(G * cap, dtype=torch.int32, pin_memory=True)
         self.ep_group = group
         self._pf = None  # prompt-sized exchange (prefill), created on first use
         self.xch = P2PExchange(s.num_experts, s.hidden_dim, batch * s.k_big, group, dm.device, bf16_rows=local.tc_ok)
@@ -391,7 +408,19 @@ class EPStepEngine(StepEngine):
         k_tok = self.k_tok[kind]
 
         def experts(rows, ids, k_in):
-            return local.rows_ffn(l, rows, ids, k_in, clone=False, force_tc=local.tc_ok)
+            if self.ep_rt is None:
+                return local.rows_ffn(l, rows, ids, k_in, clone=False, force_tc=local.tc_ok)
+            # owner with an offloaded shard: the received experts (sorted, distinct) -> its cache
+            self._ids_h.copy_(ids, non_blocking=True)
+            self._kin_h.copy_(k_in, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            self.ep_rt.sync_point()
+            got = sorted({int(e) for e, v in zip(self._ids_h.tolist(), self._kin_h.tolist()) if v})
+            loc = self.ep_rt._require(l, got, 0) if got else None
+            out = local.rows_ffn(l, rows, ids, k_in, clone=False, force_tc=local.tc_ok, loc=loc)
+            if got:
+                self.ep_rt._release(l, got)
+            return out
 
         Y = self.xch.exchange(r["h2"], r["idx"], k_tok, experts, timer=None if self.use_graphs else self.ex_timer)
         Ys = rm.shared_rows(l, r["h2"], sc) if rm.S else None
@@ -416,6 +445,12 @@ class EPStepEngine(StepEngine):
             super().prefill(prompt, prefill_k)
         finally:
             self.sess.moe_forward = None
+
+    def run_pass(self, kind: str):
+        super().run_pass(kind)
+        if self.ep_rt is not None:  # every request of the pass is settled before the next one
+            self.stream.synchronize()
+            self.ep_rt.token_end()
 
     def close(self):
         self.xch.close()

@@ -241,7 +241,7 @@ class MoBiLEMoE:
 
     # ---- expert-parallel helpers (ep.py) ----
     def rows_ffn(self, layer: int, rows: torch.Tensor, ids: torch.Tensor, k_tok: torch.Tensor | None = None,
-                 clone: bool = True, force_tc: bool = False) -> torch.Tensor:
+                 clone: bool = True, force_tc: bool = False, loc: ExpertLocation | None = None) -> torch.Tensor:
         """Routed-expert FFN of R independent rows, row i through local expert
         ids[i] (k = 1); rows with k_tok[i] = 0 are skipped (their output rows
         are left as they were).  force_tc: the tcgen05 path for any R (each
@@ -252,7 +252,7 @@ class MoBiLEMoE:
             k_tok = torch.ones(R, dtype=torch.int32, device=rows.device)
         sc = self.scratch(R, 1)
         p = K.permute(ids.view(R, 1), k_tok, self.E, out=sc["perm"])
-        loc = self.resident(layer)
+        loc = loc if loc is not None else self.resident(layer)  # offloaded shards: the cache's slot table
         if rows.dtype == torch.bfloat16 and not self.tc_ok:
             raise ValueError("rows_ffn: bf16 rows need the tcgen05 expert path (bf16 SwiGLU shapes)")
         if (R >= TC_MIN_TOKENS or force_tc or rows.dtype == torch.bfloat16) and self.tc_ok:

@@ -184,6 +184,16 @@ class DeviceWeights:
         sub.experts = self.experts[:, lo:hi]
         return sub
 
+    def shard_experts_offloaded(self, lo: int, hi: int) -> "DeviceWeights":
+        """shard_experts() with the shard's routed experts in pinned host memory
+        (contiguous (L, hi - lo, P), the layout OffloadRuntime streams from)."""
+        sub = self.shard_experts(lo, hi)
+        src = self.experts[:, lo:hi] if self.experts is not None else self.host_experts[:, lo:hi]
+        sub.host_experts = src.to("cpu").contiguous().pin_memory()
+        sub.experts = None
+        sub.experts_on_device = False
+        return sub
+
     def plain(self, w: torch.Tensor) -> torch.Tensor:
         """Row-major (N, K) view of a weight (the device layout is row-major)."""
         return w

@@ -133,6 +133,55 @@ def _prefill_case(rank, world, groups, n):
     return bad
 
 
+def _offload_case(rank, world, groups, B, steps=3):
+    """EP decode with each rank's expert shard OFFLOADED (pinned host memory
+    behind the rank's own HBM expert cache, smaller than the shard) against
+    the resident EP engine: identical logits, selections and confidences;
+    the caches issue transfers and hit on repeats."""
+    from paper_2510_12357_b200.ep import EPStepEngine, partition
+    from paper_2510_12357_b200.model import MoBiLEMoE
+    from paper_2510_12357_b200.offload import OffloadRuntime
+    _, ms, dm = matched(QWEN_MINI, "bfloat16")
+    lo, hi = partition(ms.num_experts, world)[rank]
+    res = EPStepEngine(dm, MoBiLEMoE(dm.dw.shard_experts(lo, hi)), B, 32, group=groups["world"]).build()
+    shard = dm.dw.shard_experts_offloaded(lo, hi)
+    rt = OffloadRuntime(shard, slots=max(ms.k_big, (hi - lo) // 2 + 1), lookahead=1)
+    off = EPStepEngine(dm, MoBiLEMoE(shard), B, 32, group=groups["world"], shard_runtime=rt).build()
+    g = torch.Generator(device="cuda").manual_seed(9 + rank)
+    kc = torch.randn(res.sess.kc.shape, device="cuda", generator=g)
+    vc = torch.randn(res.sess.vc.shape, device="cuda", generator=g)
+    rng = np.random.default_rng(9 + rank)
+    bad = []
+    try:
+        for e in (res, off):
+            e.sess.kc.copy_(kc)
+            e.sess.vc.copy_(vc)
+            e.pos.fill_(5)
+        for i in range(steps):
+            tok = torch.tensor(rng.integers(1, ms.vocab_size, size=B), dtype=torch.int32, device="cuda")
+            outs = []
+            for e in (res, off):
+                e.tok.copy_(tok)
+                for kd in ("little", "big", "full"):
+                    e.run_pass(kd)
+                e.stream.synchronize()
+                outs.append({kd: (e.states[kd].clone(), e.idx[kd].clone(), e.head[kd]["conf"].clone())
+                             for kd in ("little", "big", "full")})
+                e.pos.add_(1)
+            torch.cuda.synchronize()
+            for kd in outs[0]:
+                for a, b, name in zip(outs[0][kd], outs[1][kd], ("states", "idx", "conf")):
+                    if not torch.equal(a, b):
+                        bad.append((i, kd, name))
+        st = rt.cache.stats
+        nbytes, transfers = rt.counters()
+        assert transfers > 0 and st.hits > 0 and transfers == st.issued, (transfers, st)
+    finally:
+        res.close()
+        off.close()
+    return bad
+
+
 def _worker(rank, world, port, case, arg, q):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -141,7 +190,7 @@ def _worker(rank, world, port, case, arg, q):
     try:
         selfs = [dist.new_group([r]) for r in range(world)]  # collective: every rank creates every group
         groups = {"world": dist.group.WORLD, "self": selfs[rank]}
-        fn = {"layer": _layer_case, "engine": _engine_case, "prefill": _prefill_case}[case]
+        fn = {"layer": _layer_case, "engine": _engine_case, "prefill": _prefill_case, "offload": _offload_case}[case]
         q.put((rank, fn(rank, world, groups, arg), None))
     except Exception as exc:  # noqa: BLE001
         import traceback
@@ -183,6 +232,17 @@ def test_ep_prefill_bit_identical_world1_vs_world2(cuda_ok, n):
     for rank, bad, exc in _spawn("prefill", n):
         assert exc is None, (rank, exc)
         assert bad == [], (rank, bad)
+
+
+@pytest.mark.parametrize("B", [1, 4])
+def test_ep_offloaded_shards_match_resident(cuda_ok, B):
+    """World 1 in-process: the owner-side cache protocol (host read-back of
+    the received experts between the exchange legs).  The two-process variant
+    on the box's single GPU fails with a launch failure (not diagnosed; the
+    owner's host sync between two time-sliced contexts' spin-waiting exchange
+    kernels is the suspect) -- the resident EP engine passes it; multi-GPU
+    validation of the offloaded shards waits for a multi-GPU box."""
+    assert _offload_case(0, 1, {"world": None, "self": None}, B) == []
 
 
 def test_ep_engine_world1_matches_single_gpu_engine(cuda_ok):
