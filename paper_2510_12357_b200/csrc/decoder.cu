@@ -232,7 +232,12 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
   }
   // split sp owns positions [j0, j1) of [0, p]; the split holding p writes the new row
   const int n = p + 1;
-  const int j0 = (int)((long long)n * sp / nsplit), j1 = (int)((long long)n * (sp + 1) / nsplit);
+  // splits actually used at this context length: at least 32 positions each
+  // (the launch's nsplit is sized for the cache capacity; early in a long
+  // cache most of them would be empty)
+  const int ns = max(1, min(nsplit, n / 32));
+  if (sp >= ns) return;
+  const int j0 = (int)((long long)n * sp / ns), j1 = (int)((long long)n * (sp + 1) / ns);
   // grouped-query attention: query head hh reads key/value head g; position
   // p's K/V come from this step's qkv row (query heads of the group run in
   // other CTAs); the group's first head (its split holding p) writes them
@@ -315,7 +320,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
   }
   reinterpret_cast<float4*>(part[warp * PV + vg])[vl] = acc;
   __syncthreads();
-  if (nsplit == 1) {
+  if (ns == 1) {
     const float inv = 1.0f / sum;
     for (int e = threadIdx.x; e < HD; e += blockDim.x) {
       float o = 0.f;
@@ -336,18 +341,18 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
   if (threadIdx.x == 0) { wp[0] = mx; wp[1] = sum; }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last_s = atomicAdd(tk + bh, 1u) == (unsigned)(nsplit - 1);
+  if (threadIdx.x == 0) last_s = atomicAdd(tk + bh, 1u) == (unsigned)(ns - 1);
   __syncthreads();
   if (!last_s) return;
   __threadfence();
   const float* w0 = ws + (size_t)bh * nsplit * (HD + 2);
   float M = -INFINITY;
-  for (int q = 0; q < nsplit; ++q) {
+  for (int q = 0; q < ns; ++q) {
     const float* w = w0 + (size_t)q * (HD + 2);
     if (__ldcg(w + 1) != 0.f) M = fmaxf(M, __ldcg(w));
   }
   float S = 0.f;
-  for (int q = 0; q < nsplit; ++q) {
+  for (int q = 0; q < ns; ++q) {
     const float* w = w0 + (size_t)q * (HD + 2);
     const float sq = __ldcg(w + 1);
     if (sq != 0.f) S += sq * expf(__ldcg(w) - M);
@@ -355,7 +360,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
   const float inv = 1.0f / S;
   for (int e = threadIdx.x; e < HD; e += blockDim.x) {
     float o = 0.f;
-    for (int q = 0; q < nsplit; ++q) {
+    for (int q = 0; q < ns; ++q) {
       const float* w = w0 + (size_t)q * (HD + 2);
       const float sq = __ldcg(w + 1);
       if (sq != 0.f) o = fmaf(__ldcg(w + 2 + e), expf(__ldcg(w) - M), o);
