@@ -173,16 +173,6 @@ int mobile_stream_gemv(const mobile_sg_group* groups, int n_groups, int w_dtype,
  * layer-normalised), conf[t] = max softmax, first argmax, fallback =
  * conf <= gamma.  T <= 4.  workspace >= mobile_stream_head_ws_bytes(), zeroed
  * once (the kernel leaves it zeroed). */
-/* Down projection fused with the combine (mobile_combine semantics, run by
- * the last CTA to finish): groups as mobile_stream_gemv (they write Y /
- * Y_shared), then x_out = x + sum_j gates*Y (selection order) + shared, and
- * ln_out = LN(x_out) if non-NULL.  workspace >= mobile_down_combine_ws_bytes(),
- * zeroed once (left zeroed). */
-size_t mobile_down_combine_ws_bytes(void);
-int mobile_down_combine(const mobile_sg_group* groups, int n_groups, int w_dtype, int max_tokens,
-                        const float* x, const float* Y, const float* gates, const int* k_tok, int T, int k_max,
-                        int d, const float* Y_shared, int n_shared, const float* shared_logits, float* x_out,
-                        float* ln_out, void* workspace, void* stream);
 size_t mobile_stream_head_ws_bytes(void);
 int mobile_stream_head(const float* x_ln, int T, int d, const void* w_head, int w_dtype, int V,
                        float logit_scale, float gamma, float* logits_out, float* conf_out, int* argmax_out,

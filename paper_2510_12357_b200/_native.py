@@ -101,8 +101,6 @@ _SIGS = {
     "mobile_ep_collect": ([P, P, I32, I32, I32, I32, P, P], I32),
     "mobile_stream_gemv": ([P, I32, I32, I32, P], I32),
     "mobile_stream_head_ws_bytes": ([], SZ),
-    "mobile_down_combine_ws_bytes": ([], SZ),
-    "mobile_down_combine": ([P, I32, I32, I32, P, P, P, P, I32, I32, I32, P, I32, P, P, P, P, P], I32),
     "mobile_stream_head": ([P, I32, I32, P, I32, I32, F, F, P, P, P, P, P, P], I32),
     "mobile_dense_gemv": ([P, I32, I32, I32, P, I32, I32, P, P, P], I32),
     "mobile_attn_decode": ([P, P, P, P, I32, I32, I32, I32, P, P], I32),

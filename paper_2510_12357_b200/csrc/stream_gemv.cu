@@ -69,23 +69,9 @@ struct SgHead {             // HEAD epilogue state (one dense group)
   unsigned* ticket;         // left at 0
 };
 
-struct SgCombine {          // fused combine epilogue (last CTA), toymoe.py:204, 207
-  const float* x;           // (T, d) residual in
-  const float* Y;           // (T*k_max, d) routed expert outputs (pair order)
-  const float* gates;       // (T, k_max)
-  const int* k_tok;         // (T,) or NULL
-  const float* Ys;          // (T, S, d) shared outputs or NULL
-  const float* shared_logits;  // (T, S) sigmoid gates or NULL
-  float* x_out;             // (T, d)
-  float* ln_out;            // (T, d) LN(x_out) or NULL
-  unsigned* ticket;         // left at 0
-  int T, d, k_max, n_shared;
-};
-
 struct SgArgs {
   SgGroup g[kSgMaxGroups];
   SgHead head;
-  SgCombine comb;
   int n_groups;
   int total_units;
 };
@@ -464,61 +450,6 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
     cons.next(A, KC);
   }
 
-  if (A.comb.x_out != nullptr) {
-    // ---------------- fused combine: the last CTA to finish mixes the expert
-    // outputs in selection order, adds the shared experts and the residual,
-    // and writes LN(x_out) for the next layer (one launch less per layer)
-    __threadfence();
-    asm volatile("bar.sync 1, %0;" ::"n"(kSgConsumerWarps * 32));
-    if (tid == 0) is_last = atomicAdd(A.comb.ticket, 1u) == gridDim.x - 1;
-    asm volatile("bar.sync 1, %0;" ::"n"(kSgConsumerWarps * 32));
-    if (!is_last) return;
-    __threadfence();
-    const SgCombine& Cb = A.comb;
-    float* red = &hred[0][0][0];  // 8 warps x 2 floats of scratch
-    for (int t = 0; t < Cb.T; ++t) {
-      const int kt = Cb.k_tok ? Cb.k_tok[t] : Cb.k_max;
-      float sum = 0.f;
-      for (int i = tid; i < Cb.d; i += kSgConsumerWarps * 32) {
-        float m = 0.f;
-        for (int j = 0; j < kt; ++j)
-          m = fmaf(Cb.gates[(size_t)t * Cb.k_max + j], __ldcg(Cb.Y + ((size_t)t * Cb.k_max + j) * Cb.d + i), m);
-        for (int sh = 0; sh < Cb.n_shared; ++sh) {
-          float ys = __ldcg(Cb.Ys + ((size_t)t * Cb.n_shared + sh) * Cb.d + i);
-          if (Cb.shared_logits) ys = sigmoid_f(Cb.shared_logits[(size_t)t * Cb.n_shared + sh]) * ys;
-          m += ys;
-        }
-        const float v = Cb.x[(size_t)t * Cb.d + i] + m;
-        Cb.x_out[(size_t)t * Cb.d + i] = v;
-        sum += v;
-      }
-      if (Cb.ln_out) {
-        sum = warp_sum(sum);
-        if (lane == 0) red[warp] = sum;
-        asm volatile("bar.sync 1, %0;" ::"n"(kSgConsumerWarps * 32));
-        float mean = 0.f;
-        for (int w = 0; w < kSgConsumerWarps; ++w) mean += red[w];
-        mean /= (float)Cb.d;
-        float q = 0.f;
-        for (int i = tid; i < Cb.d; i += kSgConsumerWarps * 32) {
-          const float c = Cb.x_out[(size_t)t * Cb.d + i] - mean;
-          q += c * c;
-        }
-        q = warp_sum(q);
-        asm volatile("bar.sync 1, %0;" ::"n"(kSgConsumerWarps * 32));
-        if (lane == 0) red[warp] = q;
-        asm volatile("bar.sync 1, %0;" ::"n"(kSgConsumerWarps * 32));
-        float var = 0.f;
-        for (int w = 0; w < kSgConsumerWarps; ++w) var += red[w];
-        const float inv = 1.0f / sqrtf(var / (float)Cb.d + 1e-5f);
-        for (int i = tid; i < Cb.d; i += kSgConsumerWarps * 32)
-          Cb.ln_out[(size_t)t * Cb.d + i] = (Cb.x_out[(size_t)t * Cb.d + i] - mean) * inv;
-        asm volatile("bar.sync 1, %0;" ::"n"(kSgConsumerWarps * 32));
-      }
-    }
-    if (tid == 0) *Cb.ticket = 0u;
-    return;
-  }
   if (A.head.conf == nullptr) return;
   // ---------------- HEAD: merge warps (warp order), then CTAs (CTA order)
   const int T = A.g[0].dense_T;
@@ -566,7 +497,7 @@ static int sg_launch(const SgArgs& A, cudaStream_t s) {
   const size_t smem = (size_t)SgCfg<TT>::kStages * SgCfg<TT>::kStageBytes;
   if (int st = set_smem_once((const void*)k, smem)) return st;
   int grid = sm_count();
-  if (A.head.conf == nullptr && A.comb.x_out == nullptr && A.total_units < grid) grid = A.total_units;
+  if (A.head.conf == nullptr && A.total_units < grid) grid = A.total_units;
   if (grid <= 0) return MOBILE_OK;
   return launch_pdl(k, dim3(grid), dim3(kSgThreads), smem, s, 1, "stream_gemv", A);
 }
@@ -574,7 +505,7 @@ static int sg_launch(const SgArgs& A, cudaStream_t s) {
 static int sg_dispatch(SgArgs& A, int w_dtype, int max_tok, cudaStream_t s) {
   A.total_units = 0;
   for (int i = 0; i < A.n_groups; ++i) A.total_units += A.g[i].units;
-  if (A.total_units == 0 && A.head.conf == nullptr && A.comb.x_out == nullptr) return MOBILE_OK;
+  if (A.total_units == 0 && A.head.conf == nullptr) return MOBILE_OK;
   const int TT = max_tok <= 1 ? 1 : max_tok <= 2 ? 2 : 4;
   if (w_dtype == MOBILE_BF16) {
     if (TT == 1) return sg_launch<__nv_bfloat16, 1>(A, s);
@@ -672,22 +603,3 @@ extern "C" int mobile_stream_head(const float* x_ln, int T, int d, const void* w
   return sg_dispatch(A, w_dtype, T, (cudaStream_t)stream);
 }
 
-extern "C" size_t mobile_down_combine_ws_bytes(void) { return 256; }
-
-extern "C" int mobile_down_combine(const mobile_sg_group* groups, int n_groups, int w_dtype, int max_tokens,
-                                   const float* x, const float* Y, const float* gates, const int* k_tok, int T,
-                                   int k_max, int d, const float* Y_shared, int n_shared,
-                                   const float* shared_logits, float* x_out, float* ln_out, void* workspace,
-                                   void* stream) {
-  if (n_groups < 1 || n_groups > kSgMaxGroups || T < 1 || d <= 0 || n_shared < 0 || !x_out) {
-    set_error("down_combine: bad arguments");
-    return MOBILE_ERR_INVALID;
-  }
-  SgArgs A{};
-  A.n_groups = n_groups;
-  for (int i = 0; i < n_groups; ++i)
-    if (int st = fill_group(A.g[i], &groups[i], w_dtype)) return st;
-  A.comb = SgCombine{x, Y, gates, k_tok, Y_shared, shared_logits, x_out, ln_out,
-                     reinterpret_cast<unsigned*>(workspace), T, d, k_max, Y_shared ? n_shared : 0};
-  return sg_dispatch(A, w_dtype, max_tokens, (cudaStream_t)stream);
-}

@@ -260,19 +260,6 @@ def stream_head(x_ln, w_head, gamma, logit_scale, *, ws: StreamHeadWorkspace, lo
     return out
 
 
-def down_combine(groups, w_dtype, max_tokens, x, Y, gates, k_tok, Y_shared, n_shared, shared_logits, x_out,
-                 ln_out, ws, stream=None):
-    """Down-projection launch whose last CTA also runs the combine (+LN)."""
-    arr = (N.mobile_sg_group * len(groups))(*groups)
-    T, d = x.shape
-    _count()
-    N.check(N.lib.mobile_down_combine(arr, len(groups), w_dtype, int(max_tokens), N.ptr(x), N.ptr(Y), N.ptr(gates),
-                                      N.ptr(k_tok), T, gates.shape[1], d, N.ptr(Y_shared), int(n_shared),
-                                      N.ptr(shared_logits), N.ptr(x_out), N.ptr(ln_out), N.ptr(ws), _s(stream)),
-            "down_combine")
-    return x_out
-
-
 GG_STORE_F32, GG_SWIGLU_BF16, GG_STORE_BF16, GG_ACCUM_F32 = 0, 1, 2, 3
 
 

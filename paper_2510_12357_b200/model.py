@@ -78,8 +78,6 @@ class MoBiLEMoE:
         self.act = _ACT[s.activation]
         self.gate_norm = _GATE[s.gate_norm]
         self._scratch: dict = {}
-        # ticket word of the fused down+combine launch (zeroed once, left zeroed)
-        self.comb_ws = torch.zeros(int(N.lib.mobile_down_combine_ws_bytes()), dtype=torch.uint8, device=dw.device)
 
     def resident(self, layer: int) -> ExpertLocation:
         dw = self.dw
