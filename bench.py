@@ -567,11 +567,15 @@ def config_sweep(args, dev, P):
         res = {"model": NAMES[name], "context": ctx, "r": r, "decode": {}}
         eb, d, L = dw.elem_bytes, spec.hidden_dim, spec.num_layers
 
-        def pass_bytes(k, B):
-            experts = min(spec.num_experts, B * k) * dw.expert_bytes
-            per_layer = (2 * d * d + 2 * d * spec.kv_dim + (spec.num_experts + dw.n_gate_rows) * d) * eb + experts \
+        def pass_bytes(e, kd, B):
+            """Algorithmic bytes of one pass: every weight the pass needs once,
+            routed experts counted as the DISTINCT experts each layer selected
+            in this pass (several tokens on one expert read it once)."""
+            idx = e.idx[kd][:, :B, :e.k[kd]].reshape(L, -1)
+            distinct = int(sum(torch.unique(idx[l]).numel() for l in range(L)))
+            per_layer = (2 * d * d + 2 * d * spec.kv_dim + (spec.num_experts + dw.n_gate_rows) * d) * eb \
                 + spec.n_shared * dw.shared_bytes + B * 2 * ctx * spec.kv_dim * 4
-            return L * per_layer + spec.vocab_size * d * eb
+            return L * per_layer + distinct * dw.expert_bytes + spec.vocab_size * d * eb, distinct
 
         def engine(B):
             e = StepEngine(dm, B, ctx + 48).build()
@@ -600,9 +604,9 @@ def config_sweep(args, dev, P):
             row = {"engine": "gemm" if eng.gemm_path else ("persistent" if eng.dp else "per-op")}
             for kd in ("little", "big", "full"):
                 t = time_pass(eng, kd)
-                nb = pass_bytes(eng.k[kd], B)
-                row[kd] = {"ms": round(t * 1e3, 3), "bytes": nb, "gbs": round(nb / t / 1e9, 1),
-                           "hbm_frac": round(nb / t / 1e9 / hbm, 4)}
+                nb, distinct = pass_bytes(eng, kd, B)
+                row[kd] = {"ms": round(t * 1e3, 3), "bytes": nb, "distinct_experts": distinct,
+                           "gbs": round(nb / t / 1e9, 1), "hbm_frac": round(nb / t / 1e9 / hbm, 4)}
             del eng
             torch.cuda.empty_cache()
             # batched MoBiLE: the big pass replays only the rows that fell back
