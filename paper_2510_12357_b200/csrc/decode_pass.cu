@@ -243,7 +243,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, %0;" ::"n"(kCW * 32) : "memory"); }
 
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+#if MOBILE_DP_ARRIVE_RELAXED  // timing experiment only: no release ordering
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#else
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#endif
 }
 
 // Sum of 16 per-lane row partials over the 32 lanes of a warp: recursive

@@ -201,10 +201,9 @@ class MoBiLEMoE:
             bf = torch.bfloat16
             tc = dict(X=torch.empty(P, d, device=dev, dtype=bf), U=torch.empty(P, self.I, device=dev, dtype=bf))
             if self.S:
-                tc["Xs"] = torch.empty(T, d, device=dev, dtype=bf)
-                tc["Us"] = torch.empty(T, self.Is, device=dev, dtype=bf)
-                tc["s_rows"] = [(torch.arange(T, device=dev, dtype=torch.int32) * self.S + s).contiguous()
-                                for s in range(self.S)]
+                # expert-major rows s*T + t of every shared expert (one grouped launch for all S)
+                tc["Xs"] = torch.empty(self.S * T, d, device=dev, dtype=bf)
+                tc["Us"] = torch.empty(self.S * T, self.Is, device=dev, dtype=bf)
             self._scratch[key]["tc"] = tc
         return tc
 
@@ -223,18 +222,20 @@ class MoBiLEMoE:
                        row_to_pair=p["sorted_pairs"])
 
     def _shared_tc(self, h2, layer, T, sc):
-        """Shared experts on tcgen05 (dense groups) into sc["Ys"] (T, S, d)."""
-        dw, d, Is = self.dw, self.d, self.Is
+        """Shared experts on tcgen05 into sc["Ys"] (T, S, d): ONE grouped
+        gate-up and ONE down launch for all S shared experts (expert s owns
+        the rows s*T .. s*T+T-1 of a gathered copy of h2), so the S weight
+        streams share the SMs instead of running S small launches in turn."""
+        dw, d, Is, S = self.dw, self.d, self.Is, self.S
         tc = self._tc_scratch(sc, T, sc["perm"]["sorted_pairs"].numel() // max(T, 1))
-        K.gather_bf16(h2, None, 1, T, tc["Xs"])
-        mt = (T + 127) // 128
-        for s_ in range(self.S):
-            base = dw.shared[layer, s_].data_ptr()
-            K.grouped_gemm(tc["Xs"], d, base, dw.shared_bytes, 1, 2 * Is, max_tiles=mt * (2 * Is // 128),
-                           dense_rows=T, dense_experts=1, epi=K.GG_SWIGLU_BF16, out_bf16=tc["Us"], ldo=Is)
-            K.grouped_gemm(tc["Us"], Is, base + dw.s_w13_elems * dw.elem_bytes, dw.shared_bytes, 1, d,
-                           max_tiles=mt * (d // 128), dense_rows=T, dense_experts=1, epi=K.GG_STORE_F32,
-                           out_f32=sc["Ys"], ldo=d, row_to_pair=tc["s_rows"][s_])
+        K.gather_bf16(h2, sc["s_pairs"], S, S * T, tc["Xs"])
+        base = dw.shared[layer].data_ptr()
+        bound = S * ((T + 127) // 128)
+        K.grouped_gemm(tc["Xs"], d, base, dw.shared_bytes, S, 2 * Is, offsets=sc["s_offsets"], active=sc["s_active"],
+                       max_tiles=bound * (2 * Is // 128), epi=K.GG_SWIGLU_BF16, out_bf16=tc["Us"], ldo=Is)
+        K.grouped_gemm(tc["Us"], Is, base + dw.s_w13_elems * dw.elem_bytes, dw.shared_bytes, S, d,
+                       offsets=sc["s_offsets"], active=sc["s_active"], max_tiles=bound * (d // 128),
+                       epi=K.GG_STORE_F32, out_f32=sc["Ys"], ldo=d, row_to_pair=sc["s_pairs"])
         return sc["Ys"]
 
     # ---- expert-parallel helpers (ep.py) ----
