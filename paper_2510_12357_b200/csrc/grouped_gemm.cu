@@ -311,23 +311,29 @@ __global__ void __launch_bounds__(kGgThreads, 1) grouped_gemm_kernel(const __gri
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (red_last) {
           __threadfence();
-          const float* w0 = a.ws + (size_t)tile * ks * kGgBM * BN + (size_t)r * BN;
-#pragma unroll 1
-          for (int c = 0; c < BN / 16 && live; ++c) {
+          // the 128 epilogue threads split the live (row, 16-column chunk)
+          // pairs, so every partial load of the reduction is in flight at once
+          // (one L2 round trip instead of one per chunk); each output element
+          // still sums its ks partials in split order (deterministic)
+          const float* w0 = a.ws + (size_t)tile * ks * kGgBM * BN;
+          const int nch = min(BN, a.N - T.n0) / 16;
+          for (int u = (warp - 2) * 32 + lane; u < T.nrows * nch; u += 128) {
+            const int rr = u / nch, c = u - rr * nch;
             const int n = T.n0 + c * 16;
-            if (n >= a.N) break;
+            const int row2 = T.row0 + rr;
+            const int orow2 = a.epi == kGgStoreF32Scatter && a.row_to_pair ? a.row_to_pair[row2] : row2;
             float v[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] = 0.f;
             for (int sp = 0; sp < ks; ++sp) {
-              const float4* src = reinterpret_cast<const float4*>(w0 + (size_t)sp * kGgBM * BN + c * 16);
+              const float4* src = reinterpret_cast<const float4*>(w0 + (size_t)sp * kGgBM * BN + (size_t)rr * BN + c * 16);
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
                 const float4 f = __ldcg(src + j);
                 v[4 * j] += f.x; v[4 * j + 1] += f.y; v[4 * j + 2] += f.z; v[4 * j + 3] += f.w;
               }
             }
-            gg_store(a, T, row, orow, n, v);
+            gg_store(a, T, row2, orow2, n, v);
           }
           if (warp == 2 && lane == 0) a.tickets[tile] = 0u;  // reusable by the next launch
         }
