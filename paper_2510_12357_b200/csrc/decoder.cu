@@ -264,18 +264,28 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
     qv[4 * i] = q4.x; qv[4 * i + 1] = q4.y; qv[4 * i + 2] = q4.z; qv[4 * i + 3] = q4.w;
   }
   float mx = -INFINITY;
+  // K rows double-buffered: the next step's row is in flight while this one
+  // is reduced (long contexts run several steps per split)
+  float4 kn[4];
+  auto load_k = [&](int j, float4 (&dst)[4]) {
+    if (j < j1 && j != p) {
+      const float4* kr = reinterpret_cast<const float4*>(kc + (head0 + j) * HD + sl * 16);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dst[i] = __ldcs(kr + i);
+    }
+  };
+  load_k(j0 + warp * PS + sg, kn);
   for (int jj = j0 + warp * PS; jj < j1; jj += NW * PS) {
     const int j = jj + sg;
     float s = 0.f;
+    float4 k4[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) k4[i] = kn[i];
+    load_k(j + NW * PS, kn);
     if (j < j1) {
-      float4 k4[4];
       if (j == p) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) k4[i] = reinterpret_cast<const float4*>(knew + sl * 16)[i];
-      } else {
-        const float4* kr = reinterpret_cast<const float4*>(kc + (head0 + j) * HD + sl * 16);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) k4[i] = __ldcs(kr + i);
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -288,6 +298,19 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
       if (sl == 0) sc[j - j0] = s;
       mx = fmaxf(mx, s);
     }
+  }
+  // the first V rows of this thread's P.V loop are independent of the
+  // scores: issue them now so they land while the softmax reduces
+  const int vg = lane / LV, vl = lane % LV;
+  constexpr int VU = 4;  // V rows in flight per thread
+  constexpr int VSTEP = NW * PV;
+  const int jv0 = j0 + warp * PV + vg;
+  float4 vpre[VU];
+#pragma unroll
+  for (int u = 0; u < VU; ++u) {
+    const int j = jv0 + u * VSTEP;
+    vpre[u] = j < j1 && j != p ? __ldcs(reinterpret_cast<const float4*>(vc + (head0 + j) * HD) + vl)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   mx = warp_max(mx);
   if (lane == 0) red[warp] = mx;
@@ -308,15 +331,28 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
   sum = 0.f;
 #pragma unroll
   for (int i = 0; i < NW; ++i) sum += red[i];
-  // ---- P.V
-  const int vg = lane / LV, vl = lane % LV;
+  // ---- P.V: groups of VU rows, loads first (the first group was issued
+  // before the softmax); same accumulation order as one row at a time
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int j = j0 + warp * PV + vg; j < j1; j += NW * PV) {
-    const float w = sc[j - j0];
-    const float4 v4 = j == p ? reinterpret_cast<const float4*>(vnew)[vl]
-                             : __ldcs(reinterpret_cast<const float4*>(vc + (head0 + j) * HD) + vl);
-    acc.x = fmaf(w, v4.x, acc.x); acc.y = fmaf(w, v4.y, acc.y);
-    acc.z = fmaf(w, v4.z, acc.z); acc.w = fmaf(w, v4.w, acc.w);
+  for (int jb = jv0; jb < j1; jb += VU * VSTEP) {
+    float4 v4[VU];
+#pragma unroll
+    for (int u = 0; u < VU; ++u) {
+      const int j = jb + u * VSTEP;
+      if (jb == jv0) v4[u] = vpre[u];
+      else v4[u] = j < j1 && j != p ? __ldcs(reinterpret_cast<const float4*>(vc + (head0 + j) * HD) + vl)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (j == p) v4[u] = reinterpret_cast<const float4*>(vnew)[vl];
+    }
+#pragma unroll
+    for (int u = 0; u < VU; ++u) {
+      const int j = jb + u * VSTEP;
+      if (j < j1) {
+        const float w = sc[j - j0];
+        acc.x = fmaf(w, v4[u].x, acc.x); acc.y = fmaf(w, v4[u].y, acc.y);
+        acc.z = fmaf(w, v4[u].z, acc.z); acc.w = fmaf(w, v4[u].w, acc.w);
+      }
+    }
   }
   reinterpret_cast<float4*>(part[warp * PV + vg])[vl] = acc;
   __syncthreads();
@@ -346,24 +382,31 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
   if (!last_s) return;
   __threadfence();
   const float* w0 = ws + (size_t)bh * nsplit * (HD + 2);
-  float M = -INFINITY;
-  for (int q = 0; q < ns; ++q) {
+  // every split's (m, s) in one round trip (thread q loads split q), then the
+  // merge factors in split order from shared memory
+  float* ms = sc;  // the scores are consumed: reuse as 2 * ns floats
+  for (int q = threadIdx.x; q < ns; q += blockDim.x) {
     const float* w = w0 + (size_t)q * (HD + 2);
-    if (__ldcg(w + 1) != 0.f) M = fmaxf(M, __ldcg(w));
+    ms[2 * q] = __ldcg(w);
+    ms[2 * q + 1] = __ldcg(w + 1);
   }
+  __syncthreads();
+  float M = -INFINITY;
+  for (int q = 0; q < ns; ++q)
+    if (ms[2 * q + 1] != 0.f) M = fmaxf(M, ms[2 * q]);
   float S = 0.f;
   for (int q = 0; q < ns; ++q) {
-    const float* w = w0 + (size_t)q * (HD + 2);
-    const float sq = __ldcg(w + 1);
-    if (sq != 0.f) S += sq * expf(__ldcg(w) - M);
+    const float sq = ms[2 * q + 1];
+    if (sq != 0.f) S += sq * expf(ms[2 * q] - M);
   }
   const float inv = 1.0f / S;
   for (int e = threadIdx.x; e < HD; e += blockDim.x) {
     float o = 0.f;
+#pragma unroll 8
     for (int q = 0; q < ns; ++q) {
-      const float* w = w0 + (size_t)q * (HD + 2);
-      const float sq = __ldcg(w + 1);
-      if (sq != 0.f) o = fmaf(__ldcg(w + 2 + e), expf(__ldcg(w) - M), o);
+      const float sq = ms[2 * q + 1];
+      const float ov = __ldcg(w0 + (size_t)q * (HD + 2) + 2 + e);
+      if (sq != 0.f) o = fmaf(ov, expf(ms[2 * q] - M), o);
     }
     out[(size_t)b * d + hh * HD + e] = o * inv;
   }

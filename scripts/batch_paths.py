@@ -25,6 +25,9 @@ for B in batches:
         eng.sess.kc.normal_()
         eng.sess.vc.normal_()
         eng.pos.fill_(512)
+        # random token ids (as bench.py): distinct rows route to distinct experts
+        eng.tok.copy_(torch.randint(1, spec.vocab_size, (B,), device="cuda", dtype=torch.int32,
+                                    generator=torch.Generator("cuda").manual_seed(B)))
         torch.cuda.synchronize()
         res = {}
         for kd in ("little", "full"):
