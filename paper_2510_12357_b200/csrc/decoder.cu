@@ -504,12 +504,15 @@ extern "C" int mobile_dense_gemv(const float* x, int T, int d, int do_ln, const 
 }
 
 namespace mobile {
-// split-KV fan-out: ~2 x SMs CTAs when (sequence, head) pairs alone leave SMs
-// idle on a long cache, at least 64 cached positions per split
+// split-KV fan-out when (sequence, head) pairs alone leave SMs idle: splits per (sequence, head): about 2 CTAs per SM over the grid, at most 16,
+// at least 32 cached positions each (the launch is sized for the cache
+// capacity; the kernel uses only the splits the current context fills).
+// Measured per-op little pass, ctx 512: 32 vs 64 positions minimum C3 1875 ->
+// 1863 us; 4 CTAs per SM / 32 splits: C5 4024 -> 4141 us.
 static int attn_nsplit(int B, int H, int max_len) {
   const int bhn = B * H;
   if (bhn >= sm_count() || max_len < 256) return 1;
-  return std::min(std::min(16, (2 * sm_count() + bhn - 1) / bhn), max_len / 64);
+  return std::min(std::min(16, (2 * sm_count() + bhn - 1) / bhn), max_len / 32);
 }
 }  // namespace mobile
 
