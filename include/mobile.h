@@ -203,6 +203,11 @@ int mobile_grouped_gemm(const void* A, int rows_a, int K, const void* B_base, lo
 int mobile_gather_bf16(const float* src, const int* pairs, int div, int P, int d, void* X, void* stream);
 /* the same gather from bf16 source rows (expert-parallel mailbox rows) */
 int mobile_gather_rows_bf16(const void* src, const int* pairs, int div, int P, int d, void* X, void* stream);
+/* X[r] = bf16(LN(src[pairs[r] / div])) (pairs NULL: row r): the pre-MoE
+ * LayerNorm (toymoe.py:129-132, 188) with the router kernel's reduction
+ * order, so X equals bf16 of the router's h2 rows bit for bit (the shared
+ * experts of a batch start from the residual, concurrently with routing). */
+int mobile_gather_ln_bf16(const float* src, const int* pairs, int div, int P, int d, void* X, void* stream);
 
 /* ---- combine -------------------------------------------------------------
  * toymoe.py:192, 204, 207:  moe = sum_j gates[t,j] * Y[t*k_max + j] (selection

@@ -88,6 +88,7 @@ _SIGS = {
     "mobile_grouped_gemm": ([P, I32, I32, P, I64, I32, I32, P, P, P, I32, I32, I32, I32, P, P, I32, I32, P, P], I32),
     "mobile_gather_rows_bf16": ([P, P, I32, I32, I32, P, P], I32),
     "mobile_gather_bf16": ([P, P, I32, I32, I32, P, P], I32),
+    "mobile_gather_ln_bf16": ([P, P, I32, I32, I32, P, P], I32),
     "mobile_ep_mailbox_bytes": ([I32, I32, I32], SZ),
     "mobile_ep_mailbox_create": ([I32, I32, I32, P], I32),
     "mobile_ep_mailbox_destroy": ([P], I32),

@@ -204,7 +204,11 @@ __global__ void attn_decode_kernel(const float* __restrict__ qkv, float* __restr
 //          warps in a fixed order
 constexpr int kAttnThreads = 256;
 
-template <int HD>
+// PF (split launches, few (sequence, head) pairs): V rows issued before the
+// softmax and in groups of 4, K rows double-buffered -- fewer dependent HBM
+// round trips per CTA.  Without PF (B*H >= SMs: many CTAs per SM hide the
+// latency) the kernel keeps its registers low for occupancy.
+template <int HD, bool PF>
 __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const float* __restrict__ qkv,
                                                                        float* __restrict__ kc, float* __restrict__ vc,
                                                                        const int* __restrict__ pos, int d, int H,
@@ -268,20 +272,24 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
   // is reduced (long contexts run several steps per split)
   float4 kn[4];
   auto load_k = [&](int j, float4 (&dst)[4]) {
-    if (j < j1 && j != p) {
+    if (j < j1 && j >= j0 && j != p) {
       const float4* kr = reinterpret_cast<const float4*>(kc + (head0 + j) * HD + sl * 16);
 #pragma unroll
       for (int i = 0; i < 4; ++i) dst[i] = __ldcs(kr + i);
     }
   };
-  load_k(j0 + warp * PS + sg, kn);
+  if (PF) load_k(j0 + warp * PS + sg, kn);
   for (int jj = j0 + warp * PS; jj < j1; jj += NW * PS) {
     const int j = jj + sg;
     float s = 0.f;
     float4 k4[4];
+    if (PF) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) k4[i] = kn[i];
-    load_k(j + NW * PS, kn);
+      for (int i = 0; i < 4; ++i) k4[i] = kn[i];
+      load_k(j + NW * PS, kn);
+    } else {
+      load_k(j, k4);
+    }
     if (j < j1) {
       if (j == p) {
 #pragma unroll
@@ -302,15 +310,17 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
   // the first V rows of this thread's P.V loop are independent of the
   // scores: issue them now so they land while the softmax reduces
   const int vg = lane / LV, vl = lane % LV;
-  constexpr int VU = 4;  // V rows in flight per thread
+  constexpr int VU = PF ? 4 : 1;  // V rows in flight per thread
   constexpr int VSTEP = NW * PV;
   const int jv0 = j0 + warp * PV + vg;
   float4 vpre[VU];
+  if constexpr (PF) {
 #pragma unroll
-  for (int u = 0; u < VU; ++u) {
-    const int j = jv0 + u * VSTEP;
-    vpre[u] = j < j1 && j != p ? __ldcs(reinterpret_cast<const float4*>(vc + (head0 + j) * HD) + vl)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int u = 0; u < VU; ++u) {
+      const int j = jv0 + u * VSTEP;
+      vpre[u] = j < j1 && j != p ? __ldcs(reinterpret_cast<const float4*>(vc + (head0 + j) * HD) + vl)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   }
   mx = warp_max(mx);
   if (lane == 0) red[warp] = mx;
@@ -339,7 +349,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
 #pragma unroll
     for (int u = 0; u < VU; ++u) {
       const int j = jb + u * VSTEP;
-      if (jb == jv0) v4[u] = vpre[u];
+      if (PF && jb == jv0) v4[u] = vpre[u];
       else v4[u] = j < j1 && j != p ? __ldcs(reinterpret_cast<const float4*>(vc + (head0 + j) * HD) + vl)
                                     : make_float4(0.f, 0.f, 0.f, 0.f);
       if (j == p) v4[u] = reinterpret_cast<const float4*>(vnew)[vl];
@@ -541,11 +551,12 @@ extern "C" int mobile_attn_decode_ws(const float* qkv, float* k_cache, float* v_
   if ((hd == 64 || hd == 128) && (d & 3) == 0) {
     const size_t vsmem = sizeof(float) * (size_t)max_len;
     if (vsmem > 160 * 1024) { set_error("attn_decode: max_len=%d too long", max_len); return MOBILE_ERR_UNSUPPORTED; }
-    auto kern = hd == 64 ? attn_decode_vec_kernel<64> : attn_decode_vec_kernel<128>;
-    if (int st = set_smem_once((const void*)kern, vsmem)) return st;
     int nsplit = attn_nsplit(B, H, max_len);
     const int bhn = B * H;
     if (nsplit > 1 && (!ws || !tickets || ws_floats < bhn * nsplit * (hd + 2) || n_tickets < bhn)) nsplit = 1;
+    auto kern = nsplit > 1 ? (hd == 64 ? attn_decode_vec_kernel<64, true> : attn_decode_vec_kernel<128, true>)
+                           : (hd == 64 ? attn_decode_vec_kernel<64, false> : attn_decode_vec_kernel<128, false>);
+    if (int st = set_smem_once((const void*)kern, vsmem)) return st;
     return launch_pdl(kern, dim3(bhn * nsplit), dim3(kAttnThreads), vsmem, (cudaStream_t)stream, 1, "attn_decode", qkv,
                       k_cache, v_cache, pos, d, H, Hkv, max_len, out, nsplit, nsplit > 1 ? ws : nullptr,
                       nsplit > 1 ? tickets : nullptr);

@@ -362,6 +362,56 @@ __global__ void gather_bf16_kernel(const float* __restrict__ src, const int* __r
     *reinterpret_cast<__nv_bfloat162*>(o + i) = __floats2bfloat162_rn(s[i], s[i + 1]);
 }
 
+// X[r, :] = bf16(LN(src[row_to_src(r), :])): the pre-MoE LayerNorm
+// (toymoe.py:129-132, 188) with the router kernel's exact reduction (256
+// threads, strided per-thread sums, warp butterflies, warp 0 over the warp
+// partials: router.cu tile_layer_norm), so the rows equal bf16(h2) of the
+// router launch bit for bit.  Lets the shared experts start from the
+// residual before the router has run.
+constexpr int kGatherLnThreads = 256;
+__global__ void __launch_bounds__(kGatherLnThreads) gather_ln_bf16_kernel(const float* __restrict__ src,
+                                                                          const int* __restrict__ pairs, int div,
+                                                                          int P, int d, __nv_bfloat16* __restrict__ X) {
+  __shared__ float red[kGatherLnThreads / 32 + 2];
+  constexpr int NW = kGatherLnThreads / 32;
+  pdl_trigger();
+  pdl_wait();
+  const int r = blockIdx.x;
+  if (r >= P) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float* row = src + (size_t)(pairs ? pairs[r] / div : r) * d;
+  float s = 0.f;
+  for (int i = tid; i < d; i += kGatherLnThreads) s += row[i];
+  s = warp_sum(s);
+  if (lane == 0) red[warp] = s;
+  __syncthreads();
+  if (warp == 0) {
+    float v = lane < NW ? red[lane] : 0.f;
+    v = warp_sum(v);
+    if (lane == 0) red[NW] = v / (float)d;
+  }
+  __syncthreads();
+  const float mean = red[NW];
+  float q = 0.f;
+  for (int i = tid; i < d; i += kGatherLnThreads) {
+    const float c = row[i] - mean;
+    q += c * c;
+  }
+  q = warp_sum(q);
+  __syncthreads();
+  if (lane == 0) red[warp] = q;
+  __syncthreads();
+  if (warp == 0) {
+    float v = lane < NW ? red[lane] : 0.f;
+    v = warp_sum(v);
+    if (lane == 0) red[NW + 1] = v / (float)d;
+  }
+  __syncthreads();
+  const float inv = 1.0f / sqrtf(red[NW + 1] + 1e-5f);
+  __nv_bfloat16* o = X + (size_t)r * d;
+  for (int i = tid; i < d; i += kGatherLnThreads) o[i] = __float2bfloat16_rn((row[i] - mean) * inv);
+}
+
 // the same gather from bf16 rows (expert-parallel mailboxes hold bf16 rows)
 __global__ void gather_rows_bf16_kernel(const __nv_bfloat16* __restrict__ src, const int* __restrict__ pairs, int div,
                                         int P, int d, __nv_bfloat16* __restrict__ X) {
@@ -548,6 +598,14 @@ extern "C" int mobile_gather_rows_bf16(const void* src, const int* pairs, int di
   return launch_pdl(gather_rows_bf16_kernel, dim3(P), dim3(256), 0, (cudaStream_t)stream, 1, "gather_rows_bf16",
                     reinterpret_cast<const __nv_bfloat16*>(src), pairs, div > 0 ? div : 1, P, d,
                     reinterpret_cast<__nv_bfloat16*>(X));
+}
+
+extern "C" int mobile_gather_ln_bf16(const float* src, const int* pairs, int div, int P, int d, void* X,
+                                     void* stream) {
+  if (P <= 0) return MOBILE_OK;
+  if (d <= 0) { set_error("gather_ln: bad d"); return MOBILE_ERR_INVALID; }
+  return launch_pdl(gather_ln_bf16_kernel, dim3(P), dim3(kGatherLnThreads), 0, (cudaStream_t)stream, 1,
+                    "gather_ln_bf16", src, pairs, div > 0 ? div : 1, P, d, reinterpret_cast<__nv_bfloat16*>(X));
 }
 
 extern "C" int mobile_gather_bf16(const float* src, const int* pairs, int div, int P, int d, void* X, void* stream) {

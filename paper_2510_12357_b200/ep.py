@@ -388,6 +388,7 @@ class EPStepEngine(StepEngine):
         if shard_runtime is not None:
             graphs = False
         super().__init__(dm, batch, max_len, graphs=graphs, persistent=False, gemm=gemm)
+        self.fork_shared = False  # _experts below runs the shared experts itself
         s = dm.spec
         self.ep_local = local
         self.ep_rt = shard_runtime
@@ -401,7 +402,7 @@ class EPStepEngine(StepEngine):
         self.xch = P2PExchange(s.num_experts, s.hidden_dim, batch * s.k_big, group, dm.device, bf16_rows=local.tc_ok)
         self.ex_timer: ExchangeTimer | None = None  # eager mode: CUDA events around the exchange legs
 
-    def _experts(self, l: int, kind: str, sc: dict, loc) -> torch.Tensor:
+    def _experts(self, l: int, kind: str, sc: dict, loc, shared_join=None) -> torch.Tensor:
         from . import kernels as K
         rm, local = self.dm.moe, self.ep_local
         r = sc["router"]

@@ -291,6 +291,14 @@ def logits_confidence(logits, logit_scale, gamma, out, stream=None):
     return out
 
 
+def gather_ln_bf16(src, pairs, div, P, X, stream=None):
+    """X[r] = bf16(LN(src[pairs[r] / div])) (src f32): the router's h2 rows in bf16."""
+    _count()
+    N.check(N.lib.mobile_gather_ln_bf16(N.ptr(src), N.ptr(pairs), int(div), int(P), src.shape[1], N.ptr(X),
+                                        _s(stream)), "gather_ln_bf16")
+    return X
+
+
 def gather_bf16(src, pairs, div, P, X, stream=None):
     """X[r] = bf16(src[pairs[r] / div]) (src f32, or bf16 rows: a plain copy)."""
     _count()

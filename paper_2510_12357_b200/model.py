@@ -134,19 +134,27 @@ class MoBiLEMoE:
         return dict(sc, router=r)
 
     def experts(self, x: torch.Tensor, layer: int, sc: dict, k_tok: torch.Tensor, k_max: int,
-                loc: ExpertLocation | None = None, timer=None, ln_out=None, x_out=None) -> torch.Tensor:
+                loc: ExpertLocation | None = None, timer=None, ln_out=None, x_out=None,
+                shared_join=None) -> torch.Tensor:
         """Grouped expert FFN + shared experts + combine/residual (toymoe.py:202-207).
 
         Decode (T < TC_MIN_TOKENS): bulk-copy streaming GEMV launches (gate-up
         of routed + shared experts in one launch, then down of both) and the
-        combine.  Prefill / batched: the tcgen05 grouped GEMM.
+        combine.  Prefill / batched: the tcgen05 grouped GEMM.  `shared_join`
+        (batched engine): the shared experts were launched from the residual
+        by shared_from_residual on a side stream; called before the combine
+        (it makes the current stream wait for them).
         FFN_IMPL="stream_only" keeps the streaming path for any T (tests)."""
         T = x.shape[0]
         loc = loc if loc is not None else self.resident(layer)
         r = sc["router"]
         if T >= TC_MIN_TOKENS and self.tc_ok and FFN_IMPL != "stream_only":
             self._routed_tc(r["h2"], sc["perm"], T, k_max, loc, sc)
-            Ys = self._shared_tc(r["h2"], layer, T, sc) if self.S else None
+            if shared_join is not None:  # shared experts already running on a side stream
+                shared_join()
+                Ys = sc["Ys"]
+            else:
+                Ys = self._shared_tc(r["h2"], layer, T, sc) if self.S else None
         else:
             self._stream_ffn(r["h2"], sc["perm"], layer, T, k_max, loc, sc, timer)
             Ys = sc["Ys"] if self.S else None
@@ -221,6 +229,17 @@ class MoBiLEMoE:
                        slot=loc.slot, max_tiles=bound * (d // 128), epi=K.GG_STORE_F32, out_f32=sc["Y"], ldo=d,
                        row_to_pair=p["sorted_pairs"])
 
+    def shared_from_residual(self, x: torch.Tensor, layer: int, T: int, k_max: int) -> None:
+        """Shared experts of a batch straight from the post-attention residual
+        x: LN + bf16 gather (bit-identical to bf16 of the router's h2) and the
+        two grouped launches into the (T, k_max) scratch's Ys.  They do not
+        depend on the routing, so the batched engine runs them on a side
+        stream concurrently with the router / permute / routed experts."""
+        sc = self.scratch(T, k_max)
+        tc = self._tc_scratch(sc, T, k_max)
+        K.gather_ln_bf16(x, sc["s_pairs"], self.S, self.S * T, tc["Xs"])
+        self._shared_gemms(layer, T, sc, tc)
+
     def _shared_tc(self, h2, layer, T, sc):
         """Shared experts on tcgen05 into sc["Ys"] (T, S, d): ONE grouped
         gate-up and ONE down launch for all S shared experts (expert s owns
@@ -229,6 +248,11 @@ class MoBiLEMoE:
         dw, d, Is, S = self.dw, self.d, self.Is, self.S
         tc = self._tc_scratch(sc, T, sc["perm"]["sorted_pairs"].numel() // max(T, 1))
         K.gather_bf16(h2, sc["s_pairs"], S, S * T, tc["Xs"])
+        self._shared_gemms(layer, T, sc, tc)
+        return sc["Ys"]
+
+    def _shared_gemms(self, layer, T, sc, tc):
+        dw, d, Is, S = self.dw, self.d, self.Is, self.S
         base = dw.shared[layer].data_ptr()
         bound = S * ((T + 127) // 128)
         K.grouped_gemm(tc["Xs"], d, base, dw.shared_bytes, S, 2 * Is, offsets=sc["s_offsets"], active=sc["s_active"],
@@ -236,7 +260,6 @@ class MoBiLEMoE:
         K.grouped_gemm(tc["Us"], Is, base + dw.s_w13_elems * dw.elem_bytes, dw.shared_bytes, S, d,
                        offsets=sc["s_offsets"], active=sc["s_active"], max_tiles=bound * (d // 128),
                        epi=K.GG_STORE_F32, out_f32=sc["Ys"], ldo=d, row_to_pair=sc["s_pairs"])
-        return sc["Ys"]
 
     # ---- expert-parallel helpers (ep.py) ----
     def rows_ffn(self, layer: int, rows: torch.Tensor, ids: torch.Tensor, k_tok: torch.Tensor | None = None,

@@ -52,6 +52,11 @@ class StepEngine:
             gemm = batch > GEMV_MAX_BATCH or (batch >= GEMM_MIN_BATCH and runtime is None and dm.moe.tc_ok
                                               and persistent is not True)
         self.gemm_path = bool(gemm)
+        # batched GEMM path: each layer's shared experts run on a side stream
+        # concurrently with routing and the routed experts (C4 B = 8 / 64 / 256)
+        self.fork_shared = (self.gemm_path and dm.moe.S > 0 and dm.moe.tc_ok
+                            and os.environ.get("MOBILE_SHARED_FORK", "1") != "0")
+        self.side = torch.cuda.Stream(device=dm.device) if self.fork_shared else None
         # resident batches 1, 3 and 4: the per-op engine (graph-replayed,
         # PDL-chained kernels; split-KV attention) beats the persistent pass
         # (scripts/batch_paths.py, round 2, little pass: C2 1.04 vs 1.18 ms,
@@ -164,9 +169,10 @@ class StepEngine:
                          reuse_gates=self.reuse_gates and kind == "big",
                          logits_out=self.states[kind][l], idx_out=self.idx[kind][l])
 
-    def _experts(self, l: int, kind: str, sc: dict, loc) -> torch.Tensor:
+    def _experts(self, l: int, kind: str, sc: dict, loc, shared_join=None) -> torch.Tensor:
         return self.dm.moe.experts(self.xa, l, sc, self.k_tok[kind], self.k[kind], loc,
-                                   timer=None if self.use_graphs else self.timer, ln_out=self.ln)
+                                   timer=None if self.use_graphs else self.timer, ln_out=self.ln,
+                                   shared_join=shared_join)
 
     def _head(self, x_last: torch.Tensor, kind: str):
         """LN(x) is already in self.ln (written by the last layer's combine)."""
@@ -307,9 +313,21 @@ class StepEngine:
         x_in = self.x
         for l in range(self.spec.num_layers):
             self._attn(l, x_in)
+            join = self._shared_fork(l, kind) if self.fork_shared else None
             sc = self._route(l, kind)
-            x_in = self._experts(l, kind, sc, None)
+            x_in = self._experts(l, kind, sc, None, shared_join=join)
         self._head(x_in, kind)
+
+    def _shared_fork(self, l: int, kind: str):
+        """Batched (GEMM-path) pass: the layer's shared experts start from the
+        post-attention residual on a side stream while the main stream routes
+        and runs the routed experts; the returned join makes the main stream
+        wait for them before the combine (captured as fork / join edges)."""
+        main = torch.cuda.current_stream()
+        self.side.wait_stream(main)
+        with torch.cuda.stream(self.side):
+            self.dm.moe.shared_from_residual(self.xa, l, self.B, self.k[kind])
+        return lambda: main.wait_stream(self.side)
 
     def _capture(self, key, fn):
         if not self.use_graphs:

@@ -202,3 +202,37 @@ def test_large_batch_gemm_path_equals_batch1(cuda_ok, preset, B):
             assert float(ref.max() - ref[am]) <= 1e-5 * float(ref.abs().max()), (kd, s_)
             assert bool(big.head[kd]["fallback"][s_]) == (ca <= 0.7)
             assert torch.allclose(big.sess.kc[:, s_, :, ctx], one.sess.kc[:, 0, :, ctx], rtol=2e-2, atol=2e-2)
+
+
+@pytest.mark.parametrize("B", [8, 64])
+def test_shared_fork_bit_identical(cuda_ok, monkeypatch, B):
+    """Batched GEMM path: the shared experts forked onto a side stream (from
+    the residual, LN in the gather) give the same pass, bit for bit, as the
+    serial order (shared experts after routing, from the router's h2) -- in
+    graph replay, for little and full passes."""
+    from paper_2510_12357_b200.model import DeviceModel
+    from paper_2510_12357_b200.presets import PRESETS
+    from paper_2510_12357_b200.runtime import StepEngine
+    from paper_2510_12357_b200.weights import DeviceWeights
+    spec = replace(PRESETS["c4"], num_layers=3)
+    dm = DeviceModel(DeviceWeights.random(spec, torch.device("cuda"), seed=9))
+    engines = []
+    for fork in ("1", "0"):
+        monkeypatch.setenv("MOBILE_SHARED_FORK", fork)
+        e = StepEngine(dm, B, 40).build()
+        assert e.gemm_path and e.fork_shared == (fork == "1")
+        g = torch.Generator(device="cuda").manual_seed(3)
+        e.sess.kc.copy_(torch.randn(e.sess.kc.shape, device="cuda", generator=g))
+        e.sess.vc.copy_(torch.randn(e.sess.vc.shape, device="cuda", generator=g))
+        e.tok.copy_(torch.randint(1, spec.vocab_size, (B,), device="cuda", dtype=torch.int32, generator=g))
+        e.pos.fill_(21)
+        engines.append(e)
+    for kd in ("little", "full"):
+        outs = []
+        for e in engines:
+            torch.cuda.synchronize()
+            e.graphs[kd].replay()
+            torch.cuda.synchronize()
+            outs.append((e.states[kd].clone(), e.idx[kd].clone(), e.ln.clone(), e.head[kd]["conf"].clone()))
+        for a, b in zip(*outs):
+            assert torch.equal(a, b), kd

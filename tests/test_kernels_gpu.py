@@ -276,6 +276,27 @@ def test_router_fused_permute(dev, T, k):
 
 
 
+@pytest.mark.parametrize("T,S,d", [(1, 1, 256), (8, 2, 2048), (64, 2, 2048), (300, 1, 4096), (5, 3, 1000)])
+def test_gather_ln_equals_router_h2(dev, T, S, d):
+    """gather_ln_bf16(x) (the batched engine's shared-expert input, computed
+    from the residual before routing) == bf16 of the router kernel's h2, bit
+    for bit, in the expert-major row order of the shared-expert launch."""
+    from paper_2510_12357_b200 import kernels as K
+    rng = np.random.default_rng(T + 7 * S + d)
+    E = 16
+    x = torch.tensor(rng.normal(size=(T, d)) * 3 + 0.5, dtype=torch.float32, device=dev)
+    w = torch.tensor(rng.uniform(-1, 1, size=(E, d)) / 16, dtype=torch.bfloat16, device=dev)
+    r = K.router_topk(x, w, E, 2, torch.full((T,), 2, dtype=torch.int32, device=dev))
+    pairs = (torch.arange(T, device=dev, dtype=torch.int32)[None, :] * S +
+             torch.arange(S, device=dev, dtype=torch.int32)[:, None]).reshape(-1).contiguous()
+    got = torch.empty(S * T, d, dtype=torch.bfloat16, device=dev)
+    ref = torch.empty(S * T, d, dtype=torch.bfloat16, device=dev)
+    K.gather_ln_bf16(x, pairs, S, S * T, got)
+    K.gather_bf16(r["h2"], pairs, S, S * T, ref)
+    torch.cuda.synchronize()
+    assert torch.equal(got.view(torch.int16), ref.view(torch.int16))
+
+
 @pytest.mark.parametrize("wdt", ["float32", "bfloat16"])
 @pytest.mark.parametrize("T", [1, 2, 4])
 @pytest.mark.parametrize("d,V", [(256, 5003), (2048, 50304), (128, 17)])
