@@ -88,6 +88,18 @@ int mobile_router_topk(const float* x, float* h2_out, const void* w_router, int 
                        int gate_norm, float* logits_out, float* extra_out, int* idx_out,
                        float* gates_out, int* flags, int* perm_offsets, int* perm_pairs,
                        int* perm_active, void* stream);
+/* The same, and once the selection is known the launch also moves each
+ * selected expert's first pf_bytes (at pf_base + e * pf_stride, resident
+ * expert pool) toward L2 (cp.async.bulk.prefetch.L2: no result changes; the
+ * routed gate-up launch that follows finds its first tiles in L2).
+ * pf_base NULL = mobile_router_topk. */
+int mobile_router_topk_pf(const float* x, float* h2_out, const void* w_router, int w_dtype,
+                          int T, int d, int E, int n_extra, int k_max, const int* k_tok,
+                          const float* replay, const uint8_t* replay_mask, int reuse_gates,
+                          int gate_norm, float* logits_out, float* extra_out, int* idx_out,
+                          float* gates_out, int* flags, int* perm_offsets, int* perm_pairs,
+                          int* perm_active, const void* pf_base, long long pf_stride, long long pf_bytes,
+                          void* stream);
 
 /* Row-wise top-k (toymoe.py:80-88) over R rows of E logits (f32 or f64):
  * used by top_k(), build_mobile_plan (policy.py:98-103) and

@@ -77,6 +77,8 @@ _SIGS = {
     "mobile_num_sms": ([], I32),
     "mobile_router_topk": ([P, P, P, I32, I32, I32, I32, I32, I32, P, P, P, I32, I32, P, P, P, P, P, P, P, P, P],
                            I32),
+    "mobile_router_topk_pf": ([P, P, P, I32, I32, I32, I32, I32, I32, P, P, P, I32, I32, P, P, P, P, P, P, P, P,
+                               P, I64, I64, P], I32),
     "mobile_topk_rows": ([P, I32, I32, I32, I32, P, P, P], I32),
     "mobile_head_ws_bytes": ([I32, I32], SZ),
     "mobile_head_confidence": ([P, P, I32, I32, I32, I32, F, F, P, P, P, P, P, P], I32),

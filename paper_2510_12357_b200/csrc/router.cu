@@ -39,6 +39,11 @@ struct RouterArgs {
   int* perm_offsets;   // fused permute (single token tile, T*k_max <= 32), else NULL
   int* perm_pairs;
   int* perm_active;
+  // optional: L2 prefetch of each selected expert's first pf_bytes at
+  // pf_base + e * pf_stride, issued as soon as the selection is known (the
+  // routed gate-up launch that follows finds its first tiles in L2)
+  const char* pf_base;
+  long long pf_stride, pf_bytes;
 };
 
 // Deterministic stable permute of <= 32 (token, slot) pairs by one warp
@@ -337,6 +342,21 @@ __global__ void __launch_bounds__(kRouterThreads) router_kernel(RouterArgs a) {
     __syncthreads();
     if (warp == 0) warp_permute(a);
   }
+  if (a.pf_base) {  // 5. the selected experts' weights toward L2 (HBM is idle during routing)
+    __syncthreads();
+    constexpr long long kChunk = 64 * 1024;
+    for (int q = warp; q < rows * a.k_max; q += kRouterWarps) {
+      const int t = q / a.k_max, j = q - t * a.k_max;
+      const int kt = a.k_tok ? a.k_tok[t0 + t] : a.k_max;
+      if (j >= kt) continue;
+      const int e = a.idx_out[(size_t)(t0 + t) * a.k_max + j];
+      const char* src = a.pf_base + (long long)e * a.pf_stride;
+      for (long long off = (long long)lane * kChunk; off < a.pf_bytes; off += 32 * kChunk) {
+        const unsigned n = (unsigned)min(kChunk, a.pf_bytes - off);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + off), "r"(n) : "memory");
+      }
+    }
+  }
 }
 
 constexpr int kRouterClusterMaxT = 256;  // measured: clusters win up to batch 256, lose at 512-token prefill
@@ -423,6 +443,18 @@ extern "C" int mobile_router_topk(const float* x, float* h2_out, const void* w_r
                                   int gate_norm, float* logits_out, float* extra_out, int* idx_out,
                                   float* gates_out, int* flags, int* perm_offsets, int* perm_pairs,
                                   int* perm_active, void* stream) {
+  return mobile_router_topk_pf(x, h2_out, w_router, w_dtype, T, d, E, n_extra, k_max, k_tok, replay, replay_mask,
+                               reuse_gates, gate_norm, logits_out, extra_out, idx_out, gates_out, flags,
+                               perm_offsets, perm_pairs, perm_active, nullptr, 0, 0, stream);
+}
+
+extern "C" int mobile_router_topk_pf(const float* x, float* h2_out, const void* w_router, int w_dtype,
+                                     int T, int d, int E, int n_extra, int k_max, const int* k_tok,
+                                     const float* replay, const uint8_t* replay_mask, int reuse_gates,
+                                     int gate_norm, float* logits_out, float* extra_out, int* idx_out,
+                                     float* gates_out, int* flags, int* perm_offsets, int* perm_pairs,
+                                     int* perm_active, const void* pf_base, long long pf_stride,
+                                     long long pf_bytes, void* stream) {
   if (T < 0 || d <= 0 || E <= 0 || k_max <= 0) { set_error("router: bad shape T=%d d=%d E=%d k=%d", T, d, E, k_max); return MOBILE_ERR_INVALID; }
   if (E > kMaxE) { set_error("router: E=%d exceeds kernel limit %d", E, kMaxE); return MOBILE_ERR_UNSUPPORTED; }
   if (n_extra < 0 || n_extra > kMaxExtra) { set_error("router: n_extra=%d unsupported", n_extra); return MOBILE_ERR_UNSUPPORTED; }
@@ -436,7 +468,10 @@ extern "C" int mobile_router_topk(const float* x, float* h2_out, const void* w_r
   const bool fuse = perm_offsets && perm_pairs && perm_active && T <= TT && T * k_max <= 32;
   RouterArgs a{x, h2_out, w_router, T, d, E, n_extra, k_max, k_tok, replay, replay_mask, reuse_gates,
                gate_norm, logits_out, extra_out, idx_out, gates_out, flags,
-               fuse ? perm_offsets : nullptr, fuse ? perm_pairs : nullptr, fuse ? perm_active : nullptr};
+               fuse ? perm_offsets : nullptr, fuse ? perm_pairs : nullptr, fuse ? perm_active : nullptr,
+               (pf_bytes >= 16 && (pf_stride & 15) == 0 && (reinterpret_cast<uintptr_t>(pf_base) & 15) == 0)
+                   ? reinterpret_cast<const char*>(pf_base) : nullptr,
+               pf_stride, pf_bytes & ~15LL};
   cudaStream_t s = (cudaStream_t)stream;
   int st;
   if (w_dtype == MOBILE_BF16) st = launch_router_tt<__nv_bfloat16>(a, TT, s);

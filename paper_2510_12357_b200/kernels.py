@@ -39,9 +39,12 @@ def _dev(*ts):
 
 
 def router_topk(x, w_router, E, k_max, k_tok, *, n_extra=0, replay=None, replay_mask=None,
-                reuse_gates=False, gate_norm=N.GATE_SELECTED_SOFTMAX, out=None, perm=None, stream=None):
+                reuse_gates=False, gate_norm=N.GATE_SELECTED_SOFTMAX, out=None, perm=None, stream=None,
+                prefetch=None):
     """Fused LN + router GEMV + top-k + replay + gates (toymoe.py:188-201).
-    With `perm` (dict offsets/sorted_pairs/active) the permute is fused too."""
+    With `perm` (dict offsets/sorted_pairs/active) the permute is fused too.
+    `prefetch` = (base, stride, bytes): the selected experts' first bytes go
+    toward L2 once the selection is known (no result changes)."""
     _dev(x, w_router, k_tok, replay, replay_mask)
     T, d = x.shape
     dev = x.device
@@ -54,13 +57,14 @@ def router_topk(x, w_router, E, k_max, k_tok, *, n_extra=0, replay=None, replay_
             gates=torch.empty(T, k_max, device=dev, dtype=torch.float32),
             flags=torch.zeros(1, device=dev, dtype=torch.int32),
         )
-    st = N.lib.mobile_router_topk(
+    pf_base, pf_stride, pf_bytes = prefetch if prefetch is not None else (None, 0, 0)
+    st = N.lib.mobile_router_topk_pf(
         N.ptr(x), N.ptr(out["h2"]), N.ptr(w_router), dtype_code(w_router), T, d, E, n_extra, k_max,
         N.ptr(k_tok), N.ptr(replay), N.ptr(replay_mask), int(bool(reuse_gates)), gate_norm,
         N.ptr(out["logits"]), N.ptr(out["extra"]) if n_extra else None, N.ptr(out["idx"]),
         N.ptr(out["gates"]), N.ptr(out["flags"]),
         N.ptr(perm["offsets"]) if perm else None, N.ptr(perm["sorted_pairs"]) if perm else None,
-        N.ptr(perm["active"]) if perm else None, _s(stream))
+        N.ptr(perm["active"]) if perm else None, pf_base, int(pf_stride), int(pf_bytes), _s(stream))
     _count()
     N.check(st, "router_topk")
     return out

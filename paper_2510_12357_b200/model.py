@@ -116,9 +116,12 @@ class MoBiLEMoE:
         return sc
 
     def route(self, x: torch.Tensor, layer: int, k_tok: torch.Tensor, k_max: int, *, replay=None,
-              replay_mask=None, reuse_gates=False, logits_out=None, idx_out=None) -> dict:
+              replay_mask=None, reuse_gates=False, logits_out=None, idx_out=None,
+              prefetch_experts: bool = False) -> dict:
         """Router + permute (toymoe.py:188-201): returns the scratch dict with
-        `router` (h2, logits, idx, gates, ...) and `perm` (offsets, pairs, active)."""
+        `router` (h2, logits, idx, gates, ...) and `perm` (offsets, pairs, active).
+        prefetch_experts (resident experts, decode): the router launch moves
+        the selected experts' gate-up weights toward L2 once it knows them."""
         T = x.shape[0]
         sc = self.scratch(T, k_max)
         rout = sc["router"]
@@ -128,9 +131,13 @@ class MoBiLEMoE:
                 rout["logits"] = logits_out
             if idx_out is not None:
                 rout["idx"] = idx_out
+        pf = None
+        if prefetch_experts:
+            loc = self.resident(layer)
+            pf = (loc.w13_base, loc.stride, self.dw.w13_elems * self.dw.elem_bytes)
         r = K.router_topk(x, self.dw.router[layer], self.E, k_max, k_tok, n_extra=self.dw.n_gate_rows,
                           replay=replay, replay_mask=replay_mask, reuse_gates=reuse_gates,
-                          gate_norm=self.gate_norm, out=rout, perm=sc["perm"])
+                          gate_norm=self.gate_norm, out=rout, perm=sc["perm"], prefetch=pf)
         return dict(sc, router=r)
 
     def experts(self, x: torch.Tensor, layer: int, sc: dict, k_tok: torch.Tensor, k_max: int,

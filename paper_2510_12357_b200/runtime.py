@@ -57,6 +57,10 @@ class StepEngine:
         self.fork_shared = (self.gemm_path and dm.moe.S > 0 and dm.moe.tc_ok
                             and os.environ.get("MOBILE_SHARED_FORK", "1") != "0")
         self.side = torch.cuda.Stream(device=dm.device) if self.fork_shared else None
+        # GEMV decode with resident experts: the router launch starts the
+        # selected experts' gate-up weights toward L2 (HBM idles while routing)
+        self.router_prefetch = (runtime is None and not self.gemm_path
+                                and os.environ.get("MOBILE_ROUTER_PF", "1") != "0")
         # resident batches 1, 3 and 4: the per-op engine (graph-replayed,
         # PDL-chained kernels; split-KV attention) beats the persistent pass
         # (scripts/batch_paths.py, round 2, little pass: C2 1.04 vs 1.18 ms,
@@ -167,7 +171,8 @@ class StepEngine:
         mask = self.ones if kind == "big" else None
         return moe.route(self.xa, l, self.k_tok[kind], self.k[kind], replay=replay, replay_mask=mask,
                          reuse_gates=self.reuse_gates and kind == "big",
-                         logits_out=self.states[kind][l], idx_out=self.idx[kind][l])
+                         logits_out=self.states[kind][l], idx_out=self.idx[kind][l],
+                         prefetch_experts=self.router_prefetch)
 
     def _experts(self, l: int, kind: str, sc: dict, loc, shared_join=None) -> torch.Tensor:
         return self.dm.moe.experts(self.xa, l, sc, self.k_tok[kind], self.k[kind], loc,
