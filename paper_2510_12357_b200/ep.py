@@ -417,7 +417,10 @@ class EPStepEngine(StepEngine):
             torch.cuda.current_stream().synchronize()
             self.ep_rt.sync_point()
             got = sorted({int(e) for e, v in zip(self._ids_h.tolist(), self._kin_h.tolist()) if v})
-            loc = self.ep_rt._require(l, got, 0) if got else None
+            # a rank that received no rows this layer still needs the cache's
+            # slot table (no expert is active, nothing is read through it);
+            # the resident location does not exist for an offloaded shard
+            loc = self.ep_rt._require(l, got, 0) if got else self.ep_rt._location(l, 0)
             out = local.rows_ffn(l, rows, ids, k_in, clone=False, force_tc=local.tc_ok, loc=loc)
             if got:
                 self.ep_rt._release(l, got)
