@@ -57,10 +57,13 @@ class StepEngine:
         self.fork_shared = (self.gemm_path and dm.moe.S > 0 and dm.moe.tc_ok
                             and os.environ.get("MOBILE_SHARED_FORK", "1") != "0")
         self.side = torch.cuda.Stream(device=dm.device) if self.fork_shared else None
-        # GEMV decode with resident experts: the router launch starts the
-        # selected experts' gate-up weights toward L2 (HBM idles while routing)
+        # opt-in (MOBILE_ROUTER_PF=1): the router launch starts the selected
+        # experts' whole gate-up weights toward L2.  Measured 2-8x SLOWER
+        # (per-op little pass C2 1.02 -> 3.14 ms, C3 1.86 -> 4.08, C5 4.02 ->
+        # 33.96; profiles/r2_ab_routerpf.txt): the prefetch doubles the
+        # experts' HBM traffic and thrashes L2 for experts larger than it
         self.router_prefetch = (runtime is None and not self.gemm_path
-                                and os.environ.get("MOBILE_ROUTER_PF", "1") != "0")
+                                and os.environ.get("MOBILE_ROUTER_PF", "0") == "1")
         # resident batches 1, 3 and 4: the per-op engine (graph-replayed,
         # PDL-chained kernels; split-KV attention) beats the persistent pass
         # (scripts/batch_paths.py, round 2, little pass: C2 1.04 vs 1.18 ms,

@@ -145,7 +145,9 @@ def _offload_case(rank, world, groups, B, steps=3):
     lo, hi = partition(ms.num_experts, world)[rank]
     res = EPStepEngine(dm, MoBiLEMoE(dm.dw.shard_experts(lo, hi)), B, 32, group=groups["world"]).build()
     shard = dm.dw.shard_experts_offloaded(lo, hi)
-    rt = OffloadRuntime(shard, slots=max(ms.k_big, (hi - lo) // 2 + 1), lookahead=1)
+    # the cache holds at least one layer's working set (up to B * k_big distinct
+    # experts of the shard; fewer slots is the reference's CapacityDeadlock)
+    rt = OffloadRuntime(shard, slots=max(min(hi - lo, B * ms.k_big), (hi - lo) // 2 + 1), lookahead=1)
     off = EPStepEngine(dm, MoBiLEMoE(shard), B, 32, group=groups["world"], shard_runtime=rt).build()
     g = torch.Generator(device="cuda").manual_seed(9 + rank)
     kc = torch.randn(res.sess.kc.shape, device="cuda", generator=g)
