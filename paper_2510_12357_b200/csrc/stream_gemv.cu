@@ -31,9 +31,18 @@ namespace mobile {
 
 constexpr int kSgConsumerWarps = 8;
 constexpr int kSgThreads = (kSgConsumerWarps + 1) * 32;  // + 1 producer warp
-constexpr int kSgWBytes = 64 * 1024;   // weight tile region of a stage
+#ifndef MOBILE_SG_ROW_BYTES
+#define MOBILE_SG_ROW_BYTES 4096  // K chunk per tile row (bytes of weight)
+#endif
+#ifndef MOBILE_SG_ILP
+#define MOBILE_SG_ILP 0           // consumer inner loop: short product chains (see the consumer loop)
+#endif
+#ifndef MOBILE_SG_STAGES1
+#define MOBILE_SG_STAGES1 3       // ring depth at batch 1
+#endif
 constexpr int kSgTileRows = 16;
-constexpr int kSgTileRowBytes = 4096;  // K chunk per tile row
+constexpr int kSgTileRowBytes = MOBILE_SG_ROW_BYTES;
+constexpr int kSgWBytes = kSgTileRows * kSgTileRowBytes;  // weight tile region of a stage
 constexpr int kSgMaxGroups = 4;
 constexpr int kSgMaxTok = 4;
 
@@ -112,8 +121,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 template <int TT>
 struct SgCfg {
-  static constexpr int kStages = TT == 1 ? 3 : 2;
-  static constexpr int kXBytes = TT * 8192;  // TT activation slices of <= 4 KB-of-K (f32: 2048 floats max)
+  static constexpr int kStages = TT == 1 ? MOBILE_SG_STAGES1 : 2;
+  // TT f32 activation slices of one K chunk (bf16 weights: 2 x the row bytes)
+  static constexpr int kXBytes = TT * 2 * kSgTileRowBytes;
   static constexpr int kStageBytes = kSgWBytes + kXBytes;
 };
 
@@ -388,6 +398,34 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
         for (int t = 0; t < TT; ++t) {
           if (t < nt) {
             const float4* xp = reinterpret_cast<const float4*>(xs + (size_t)t * kn + vi * V);
+#if MOBILE_SG_ILP
+            // short independent chains per 4-element group, summed pairwise, one
+            // add into the running sum: the running-sum chain is one FADD per
+            // vector instead of V dependent FFMAs (the consumers are latency-
+            // bound at 2 warps per SMSP; fixed order, deterministic)
+            float p0[V / 4], p1[V / 4];
+#pragma unroll
+            for (int q = 0; q < V / 4; ++q) {
+              const float4 xq = xp[q];
+              p0[q] = f0[4 * q] * xq.x;
+              p0[q] = fmaf(f0[4 * q + 1], xq.y, p0[q]);
+              p0[q] = fmaf(f0[4 * q + 2], xq.z, p0[q]);
+              p0[q] = fmaf(f0[4 * q + 3], xq.w, p0[q]);
+              if (has1) {
+                p1[q] = f1[4 * q] * xq.x;
+                p1[q] = fmaf(f1[4 * q + 1], xq.y, p1[q]);
+                p1[q] = fmaf(f1[4 * q + 2], xq.z, p1[q]);
+                p1[q] = fmaf(f1[4 * q + 3], xq.w, p1[q]);
+              }
+            }
+#pragma unroll
+            for (int q = 1; q < V / 4; ++q) {
+              p0[0] += p0[q];
+              if (has1) p1[0] += p1[q];
+            }
+            acc[0][t] += p0[0];
+            if (has1) acc[1][t] += p1[0];
+#else
 #pragma unroll
             for (int q = 0; q < V / 4; ++q) {
               const float4 xq = xp[q];
@@ -402,6 +440,7 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
                 acc[1][t] = fmaf(f1[4 * q + 3], xq.w, acc[1][t]);
               }
             }
+#endif
           }
         }
       }
