@@ -12,9 +12,14 @@
 // (2048 bf16 / 1024 f32): when a whole row fits the chunk the tile is one
 // contiguous bulk copy of up to 64 KB, otherwise 16 row copies.
 //
-// Warp 8 is the producer (one lane issues copies); warps 0-7 consume: warp w
-// owns rows {w, w+8} of every 16-row tile, so each output is one warp's
-// fixed-order dot product and every epilogue is warp-local:
+// The last warp is the producer: its 32 lanes run the item iterator in
+// lockstep, lane 0 arms the stage's mbarrier and the lanes split a tile's row
+// copies (16 rows x 4 KB when rows are longer than the chunk) and activation
+// slices.  16 consumer warps: warps w and w + 8 own rows {w, w + 8} of every
+// 16-row tile, each over one half of the tile's K chunk (interleaved 16-byte
+// vectors); at the end of a row the second half's row sums join the first's
+// (fixed order, one named barrier), so each output is a fixed-order dot
+// product and every epilogue is warp-local to warp w < 8:
 //   STORE  : y = acc (+ residual)
 //   RELU   : y = max(acc, 0)                      (toy expert, toymoe.py:203)
 //   SWIGLU : tile rows [8 gate | 8 up] -> silu(g_w) * u_w   (extension)
@@ -29,13 +34,17 @@
 
 namespace mobile {
 
-constexpr int kSgConsumerWarps = 8;
+#ifndef MOBILE_SG_KSPLIT
+#define MOBILE_SG_KSPLIT 2  // consumer warps per row pair (each takes 1/KSPLIT of a tile's K chunk)
+#endif
+constexpr int kSgKSplit = MOBILE_SG_KSPLIT;
+constexpr int kSgConsumerWarps = 8 * kSgKSplit;
 constexpr int kSgThreads = (kSgConsumerWarps + 1) * 32;  // + 1 producer warp
 #ifndef MOBILE_SG_ROW_BYTES
 #define MOBILE_SG_ROW_BYTES 4096  // K chunk per tile row (bytes of weight)
 #endif
-#ifndef MOBILE_SG_ILP
-#define MOBILE_SG_ILP 0           // consumer inner loop: short product chains (see the consumer loop)
+#ifndef MOBILE_SG_WARP_ISSUE
+#define MOBILE_SG_WARP_ISSUE 1  // 1: the producer warp's 32 lanes issue a tile's row copies in parallel
 #endif
 #ifndef MOBILE_SG_STAGES1
 #define MOBILE_SG_STAGES1 3       // ring depth at batch 1
@@ -216,7 +225,8 @@ struct SgIter {
 };
 
 template <typename W, int TT>
-__device__ void sg_issue(const SgArgs& A, const SgIter<TT>& it, char* stage, uint64_t* bar) {
+__device__ void sg_issue(const SgArgs& A, const SgIter<TT>& it, char* stage, uint64_t* bar, int lane = 0,
+                         int nl = 1) {
   constexpr int KC = kSgTileRowBytes / sizeof(W);
   const SgGroup& G = A.g[it.g];
   const int s = it.slot;
@@ -226,15 +236,18 @@ __device__ void sg_issue(const SgArgs& A, const SgIter<TT>& it, char* stage, uin
   const uint32_t wbytes = (uint32_t)(it.rr * kn * sizeof(W));
   const int nt = min(TT, it.n - it.tc * TT);
   const uint32_t xbytes = (uint32_t)(kn * sizeof(float));
-  mbar_expect_tx(bar, wbytes + nt * xbytes);
+  if (lane == 0) mbar_expect_tx(bar, wbytes + nt * xbytes);
+  if (nl > 1) __syncwarp();
   if (kn == G.K) {  // whole rows: one contiguous copy
-    bulk_g2s(stage, rows, wbytes, bar);
+    if (lane == 0) bulk_g2s(stage, rows, wbytes, bar);
   } else {
     const uint32_t rb = (uint32_t)(kn * sizeof(W));
-    for (int r = 0; r < it.rr; ++r) bulk_g2s(stage + (size_t)r * rb, rows + ((size_t)r * G.K + k0) * sizeof(W), rb, bar);
+    for (int r = lane; r < it.rr; r += nl)
+      bulk_g2s(stage + (size_t)r * rb, rows + ((size_t)r * G.K + k0) * sizeof(W), rb, bar);
   }
-  for (int t = 0; t < nt; ++t)  // activation slices x[row, k0:k0+kn]
-    bulk_g2s(stage + kSgWBytes + (size_t)t * xbytes, G.x + (size_t)(it.pair[t] / G.x_div) * G.K + k0, xbytes, bar);
+  for (int t = nl > 1 ? lane - 16 : 0; t < nt; t += nl)  // activation slices x[row, k0:k0+kn]
+    if (t >= 0)
+      bulk_g2s(stage + kSgWBytes + (size_t)t * xbytes, G.x + (size_t)(it.pair[t] / G.x_div) * G.K + k0, xbytes, bar);
 }
 
 // L2 prefetch of an item's weight tile (no shared memory cost): the producer
@@ -274,8 +287,10 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
   __shared__ __align__(8) uint64_t full[kSgStages];
   __shared__ __align__(8) uint64_t empty[kSgStages];
   __shared__ float hred[kSgConsumerWarps][kSgMaxTok][3];
+  __shared__ float xred[2][8][2][kSgMaxTok];  // K-split partial row sums (double-buffered per epilogue)
   __shared__ bool is_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int w8 = warp & 7, kh = warp >> 3;  // consumer: row pair (w8, w8 + 8), K part kh
   constexpr int V = WVec<W>::N;
   constexpr int KC = kSgTileRowBytes / sizeof(W);
 
@@ -290,8 +305,11 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
 
   pdl_trigger();
   if (warp == kSgConsumerWarps) {
-    // ---------------- producer: one lane streams every item of this CTA
-    if (lane == 0) {
+    // ---------------- producer: one lane streams every item of this CTA (or
+    // the whole warp in lockstep, lanes splitting each tile's row copies)
+    constexpr int NL = MOBILE_SG_WARP_ISSUE ? 32 : 1;
+    const int pl = NL > 1 ? lane : 0;
+    if (NL > 1 || lane == 0) {
       // phase A (overlaps the previous kernel's tail): weight tiles of static
       // groups (dense / shared experts) for the first stages
       int npre = 0;
@@ -303,13 +321,14 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
           const int k0 = pre.kc * KC, kn = min(KC, G.K - k0);
           const char* rows = G.w_base + (long long)pre.slot * G.stride + (size_t)pre.rb * kSgTileRows * G.K * sizeof(W);
           const uint32_t wbytes = (uint32_t)(pre.rr * kn * sizeof(W));
-          mbar_expect_tx_only(&full[npre], wbytes);
+          if (pl == 0) mbar_expect_tx_only(&full[npre], wbytes);
+          if (NL > 1) __syncwarp();
           char* st = smem + (size_t)npre * kSgStageBytes;
           if (kn == G.K) {
-            bulk_g2s(st, rows, wbytes, &full[npre]);
+            if (pl == 0) bulk_g2s(st, rows, wbytes, &full[npre]);
           } else {
             const uint32_t rbytes = (uint32_t)(kn * sizeof(W));
-            for (int r = 0; r < pre.rr; ++r)
+            for (int r = pl; r < pre.rr; r += NL)
               bulk_g2s(st + (size_t)r * rbytes, rows + ((size_t)r * G.K + k0) * sizeof(W), rbytes, &full[npre]);
           }
           ++npre;
@@ -322,14 +341,14 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
       SgIter<TT> pf = prod;  // L2-prefetch cursor, kSgStages + kSgL2Ahead items ahead
       for (int j = 0; j < kSgStages && pf.valid; ++j) pf.next(A, KC);
       for (int j = 0; j < kSgL2Ahead && pf.valid; ++j) {
-        sg_prefetch<W, TT>(A, pf);
+        if (pl == 0) sg_prefetch<W, TT>(A, pf);
         pf.next(A, KC);
       }
       int stage = 0;
       uint32_t empty_phase = 0;
       for (int i = 0; prod.valid; ++i) {
         if (kSgL2Ahead > 0 && i >= kSgStages && pf.valid) {
-          sg_prefetch<W, TT>(A, pf);
+          if (pl == 0) sg_prefetch<W, TT>(A, pf);
           pf.next(A, KC);
         }
         if (i < npre) {  // weights already in flight: add the activation slices
@@ -337,8 +356,9 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
           const int k0 = prod.kc * KC, kn = min(KC, G.K - k0);
           const int nt = min(TT, prod.n - prod.tc * TT);
           const uint32_t xbytes = (uint32_t)(kn * sizeof(float));
-          mbar_expect_tx(&full[stage], nt * xbytes);
-          for (int t = 0; t < nt; ++t)
+          if (pl == 0) mbar_expect_tx(&full[stage], nt * xbytes);
+          if (NL > 1) __syncwarp();
+          for (int t = pl; t < nt; t += NL)
             bulk_g2s(smem + (size_t)stage * kSgStageBytes + kSgWBytes + (size_t)t * xbytes,
                      G.x + (size_t)(prod.pair[t] / G.x_div) * G.K + k0, xbytes, &full[stage]);
         } else {
@@ -347,7 +367,7 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
             empty_phase ^= 1u << stage;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           }
-          sg_issue<W, TT>(A, prod, smem + (size_t)stage * kSgStageBytes, &full[stage]);
+          sg_issue<W, TT>(A, prod, smem + (size_t)stage * kSgStageBytes, &full[stage], pl, NL);
         }
         prod.next(A, KC);
         stage = stage + 1 == kSgStages ? 0 : stage + 1;
@@ -361,7 +381,7 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
   SgIter<TT> cons;
   cons.start(A);
   uint32_t full_phase = 0;
-  int stage = 0;
+  int stage = 0, epi_par = 0;
   float acc[2][TT];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
@@ -377,7 +397,7 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
     const int k0 = cons.kc * KC;
     const int kn = min(KC, G.K - k0);
     const int nt = min(TT, cons.n - cons.tc * TT);
-    const bool has0 = warp < cons.rr, has1 = warp + 8 < cons.rr;
+    const bool has0 = w8 < cons.rr, has1 = w8 + 8 < cons.rr;
     int pair[TT];
 #pragma unroll
     for (int t = 0; t < TT; ++t) pair[t] = cons.pair[t];
@@ -385,12 +405,12 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
     full_phase ^= 1u << stage;
     if (has0) {
       const char* st = smem + (size_t)stage * kSgStageBytes;
-      const W* row0 = reinterpret_cast<const W*>(st) + (size_t)warp * kn;
+      const W* row0 = reinterpret_cast<const W*>(st) + (size_t)w8 * kn;
       const W* row1 = row0 + (size_t)8 * kn;
       const float* xs = reinterpret_cast<const float*>(st + kSgWBytes);
       const int nvec = kn / V;
 #pragma unroll 4
-      for (int vi = lane; vi < nvec; vi += 32) {
+      for (int vi = lane + 32 * kh; vi < nvec; vi += 32 * kSgKSplit) {
         float f0[V], f1[V];
         WVec<W>::widen(*reinterpret_cast<const uint4*>(row0 + vi * V), f0);
         if (has1) WVec<W>::widen(*reinterpret_cast<const uint4*>(row1 + vi * V), f1);
@@ -398,34 +418,6 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
         for (int t = 0; t < TT; ++t) {
           if (t < nt) {
             const float4* xp = reinterpret_cast<const float4*>(xs + (size_t)t * kn + vi * V);
-#if MOBILE_SG_ILP
-            // short independent chains per 4-element group, summed pairwise, one
-            // add into the running sum: the running-sum chain is one FADD per
-            // vector instead of V dependent FFMAs (the consumers are latency-
-            // bound at 2 warps per SMSP; fixed order, deterministic)
-            float p0[V / 4], p1[V / 4];
-#pragma unroll
-            for (int q = 0; q < V / 4; ++q) {
-              const float4 xq = xp[q];
-              p0[q] = f0[4 * q] * xq.x;
-              p0[q] = fmaf(f0[4 * q + 1], xq.y, p0[q]);
-              p0[q] = fmaf(f0[4 * q + 2], xq.z, p0[q]);
-              p0[q] = fmaf(f0[4 * q + 3], xq.w, p0[q]);
-              if (has1) {
-                p1[q] = f1[4 * q] * xq.x;
-                p1[q] = fmaf(f1[4 * q + 1], xq.y, p1[q]);
-                p1[q] = fmaf(f1[4 * q + 2], xq.z, p1[q]);
-                p1[q] = fmaf(f1[4 * q + 3], xq.w, p1[q]);
-              }
-            }
-#pragma unroll
-            for (int q = 1; q < V / 4; ++q) {
-              p0[0] += p0[q];
-              if (has1) p1[0] += p1[q];
-            }
-            acc[0][t] += p0[0];
-            if (has1) acc[1][t] += p1[0];
-#else
 #pragma unroll
             for (int q = 0; q < V / 4; ++q) {
               const float4 xq = xp[q];
@@ -440,7 +432,6 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
                 acc[1][t] = fmaf(f1[4 * q + 3], xq.w, acc[1][t]);
               }
             }
-#endif
           }
         }
       }
@@ -451,12 +442,34 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
 
     if ((cons.kc + 1) * KC >= G.K) {
       // ---------------- warp-local epilogue for (tile, token chunk)
-      if (has0) {
-        const int r0 = cons.rb * kSgTileRows + warp;  // output row of acc[0]
+      float s0v[TT], s1v[TT];
+#pragma unroll
+      for (int t = 0; t < TT; ++t) {
+        s0v[t] = has0 ? warp_sum(acc[0][t]) : 0.f;
+        s1v[t] = has1 ? warp_sum(acc[1][t]) : 0.f;
+      }
+      if constexpr (kSgKSplit > 1) {  // K part 1's row sums join part 0's (fixed order: part 0 + part 1)
+        if (kh == 1 && lane == 0)
+#pragma unroll
+          for (int t = 0; t < TT; ++t) {
+            xred[epi_par][w8][0][t] = s0v[t];
+            xred[epi_par][w8][1][t] = s1v[t];
+          }
+        asm volatile("bar.sync 2, %0;" ::"n"(kSgConsumerWarps * 32));
+        if (kh == 0)
+#pragma unroll
+          for (int t = 0; t < TT; ++t) {
+            s0v[t] += xred[epi_par][w8][0][t];
+            s1v[t] += xred[epi_par][w8][1][t];
+          }
+        epi_par ^= 1;
+      }
+      if (has0 && kh == 0) {
+        const int r0 = cons.rb * kSgTileRows + w8;  // output row of acc[0]
 #pragma unroll
         for (int t = 0; t < TT; ++t) {
-          const float s0 = warp_sum(acc[0][t]);
-          const float s1 = has1 ? warp_sum(acc[1][t]) : 0.f;
+          const float s0 = s0v[t];
+          const float s1 = s1v[t];
           if (t < nt) {
             if (G.epi == kEpiHead) {
               const float l0 = s0 * A.head.scale, l1 = s1 * A.head.scale;
@@ -468,7 +481,7 @@ __global__ void __launch_bounds__(kSgThreads, 1) stream_gemv_kernel(const __grid
               if (has1) online_add(hm[t], hs[t], ha[t], l1, r0 + 8);
             } else if (lane == 0) {
               if (G.epi == kEpiSwiglu) {  // row w = gate f, row w + 8 = up f
-                G.out[(size_t)pair[t] * G.out_dim + cons.rb * 8 + warp] = silu_f(s0) * s1;
+                G.out[(size_t)pair[t] * G.out_dim + cons.rb * 8 + w8] = silu_f(s0) * s1;
               } else {
                 const size_t o0 = (size_t)pair[t] * G.out_dim + r0;
                 float v0 = s0, v1 = s1;
