@@ -208,6 +208,9 @@ constexpr int kAttnThreads = 256;
 // softmax and in groups of 4, K rows double-buffered -- fewer dependent HBM
 // round trips per CTA.  Without PF (B*H >= SMs: many CTAs per SM hide the
 // latency) the kernel keeps its registers low for occupancy.
+#ifndef MOBILE_ATTN_L2PF
+#define MOBILE_ATTN_L2PF 0  // 1: L2 prefetch of the split's K / V rows before the PDL wait
+#endif
 template <int HD, bool PF>
 __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const float* __restrict__ qkv,
                                                                        float* __restrict__ kc, float* __restrict__ vc,
@@ -224,6 +227,29 @@ __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const flo
   __shared__ float red[NW];
   __shared__ int last_s;
   pdl_trigger();
+#if MOBILE_ATTN_L2PF
+  // before the wait on the previous kernel (the QKV projection): start this
+  // split's cached K / V rows toward L2.  A hint only -- the rows are read
+  // again after the wait, and L2 is the coherence point, so a prefetch from a
+  // stale position can cost bandwidth but never change a value.
+  if (threadIdx.x == 0) {
+    const int bh0 = blockIdx.x / nsplit, sp0 = blockIdx.x - bh0 * nsplit;
+    const int b0 = bh0 / H, p0 = *(volatile const int*)(pos + b0);
+    if (p0 > 0 && p0 < max_len) {
+      const int n0 = p0 + 1, ns0 = max(1, min(nsplit, n0 / 32));
+      if (sp0 < ns0) {
+        const int a0 = (int)((long long)n0 * sp0 / ns0), a1 = min((int)((long long)n0 * (sp0 + 1) / ns0), p0);
+        const int g0 = (bh0 % H) / (H / Hkv);
+        const size_t off = (((size_t)b0 * Hkv + g0) * max_len + a0) * HD;
+        const unsigned bytes = (unsigned)(a1 - a0) * HD * 4u;
+        if (a1 > a0) {
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kc + off), "r"(bytes) : "memory");
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vc + off), "r"(bytes) : "memory");
+        }
+      }
+    }
+  }
+#endif
   pdl_wait();
   const int bh = blockIdx.x / nsplit, sp = blockIdx.x - bh * nsplit;
   const int b = bh / H, hh = bh % H;

@@ -6,5 +6,5 @@ for lib in ${LIBS:-default sg3k4 sg2k5}; do
 done > gpurun_out/r2_ab_sg.txt
 cat gpurun_out/r2_ab_sg.txt
 for lib in ${TLIBS:-sg3k4 sg2k5}; do
-  MOBILE_LIB=paper_2510_12357_b200/variants/libmobile_$lib.so timeout 600 python -m pytest tests/test_kernels_gpu.py tests/test_runtime_gpu.py -q -x -k "gemv or head or step_engine or moe_layer" 2>&1 | tail -2
+  MOBILE_LIB=paper_2510_12357_b200/variants/libmobile_$lib.so timeout 600 python -m pytest tests/test_kernels_gpu.py tests/test_runtime_gpu.py -q -x -k "gemv or head or step_engine or moe_layer or attn" 2>&1 | tail -2
 done
