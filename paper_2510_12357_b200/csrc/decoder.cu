@@ -209,7 +209,7 @@ constexpr int kAttnThreads = 256;
 // round trips per CTA.  Without PF (B*H >= SMs: many CTAs per SM hide the
 // latency) the kernel keeps its registers low for occupancy.
 #ifndef MOBILE_ATTN_L2PF
-#define MOBILE_ATTN_L2PF 0  // 1: L2 prefetch of the split's K / V rows before the PDL wait
+#define MOBILE_ATTN_L2PF 1  // 1: L2 prefetch of the split's K / V rows before the PDL wait
 #endif
 template <int HD, bool PF>
 __global__ void __launch_bounds__(kAttnThreads) attn_decode_vec_kernel(const float* __restrict__ qkv,
