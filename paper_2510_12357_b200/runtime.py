@@ -31,7 +31,7 @@ import torch
 
 from . import _native as N
 from . import kernels as K
-from .model import DecodeSession, DeviceModel, pos_rows
+from .model import FFN_IMPL, TC_MIN_TOKENS, DecodeSession, DeviceModel, pos_rows
 from .policy import plan_from_targets
 
 KINDS = ("little", "big", "full")
@@ -54,8 +54,11 @@ class StepEngine:
         self.gemm_path = bool(gemm)
         # batched GEMM path: each layer's shared experts run on a side stream
         # concurrently with routing and the routed experts (C4 B = 8 / 64 / 256)
-        self.fork_shared = (self.gemm_path and dm.moe.S > 0 and dm.moe.tc_ok
-                            and os.environ.get("MOBILE_SHARED_FORK", "1") != "0")
+        # (only when the batch's experts run on the grouped GEMM: a GEMM path
+        # forced below TC_MIN_TOKENS streams its shared experts with the routed
+        # ones, and a fork there was never joined -- graph capture failed)
+        self.fork_shared = (self.gemm_path and dm.moe.S > 0 and dm.moe.tc_ok and batch >= TC_MIN_TOKENS
+                            and FFN_IMPL != "stream_only" and os.environ.get("MOBILE_SHARED_FORK", "1") != "0")
         self.side = torch.cuda.Stream(device=dm.device) if self.fork_shared else None
         # opt-in (MOBILE_ROUTER_PF=1): the router launch starts the selected
         # experts' whole gate-up weights toward L2.  Measured 2-8x SLOWER
