@@ -67,14 +67,14 @@ class StepEngine:
         # experts' HBM traffic and thrashes L2 for experts larger than it
         self.router_prefetch = (runtime is None and not self.gemm_path
                                 and os.environ.get("MOBILE_ROUTER_PF", "0") == "1")
-        # resident batches 1, 3 and 4: the per-op engine (graph-replayed,
-        # PDL-chained kernels; split-KV attention) beats the persistent pass
-        # (scripts/batch_paths.py, round 2, little pass: C2 1.04 vs 1.18 ms,
-        # C3 1.89 vs 2.07, C4 1.89 vs 2.07 at B = 1; C4 4.58 vs 5.67 / 4.71 GEMM
-        # at B = 3, 5.83 vs 6.16 / 5.91 at B = 4); the persistent pass stays the
-        # default for B = 2 (C4 2.55 vs 2.92 ms) and for offloaded experts
-        # (zero-sync)
-        if persistent is None and runtime is None and batch != 2 and not self.gemm_path:
+        # resident batches 1-4: the per-op engine (graph-replayed, PDL-chained
+        # kernels; split-KV attention; 16-warp streaming GEMV) beats or ties the
+        # persistent pass (scripts/batch_paths.py, round 2, little / full pass:
+        # B = 1 C2 1.01 / 1.20 vs 1.17 / 1.46 ms, C4 1.84 / 2.14 vs 2.06 / 2.46;
+        # B = 2 C2 1.47 / 1.99 vs 1.60 / 2.14, C4 2.74 / 3.67 vs 2.79 / 3.57;
+        # B = 3-4 also ahead of the GEMM path; profiles/r2_batch_paths_gemv16.txt).
+        # The persistent pass stays the engine of offloaded experts (zero-sync)
+        if persistent is None and runtime is None and not self.gemm_path:
             persistent = False
         if self.gemm_path:
             if not dm.moe.tc_ok:
