@@ -125,13 +125,21 @@ class ClockSampler:
                     N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
             mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
 
+            def sample():
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((float(sm), float(mx), [self.NAMES[i] for i, b in enumerate(bits) if rs & b]))
+
             def poll():
                 while True:
-                    sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
-                    rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
-                    self.rows.append((float(sm), float(mx), [self.NAMES[i] for i, b in enumerate(bits) if rs & b]))
-                    if self.stop.wait(0.02):
+                    sample()
+                    if self.stop.wait(0.01):
                         break
+            self.sample = sample
+            # the timed loop is Python calling into ctypes: a short GIL switch
+            # interval lets the polling thread run every ~10 ms
+            self.switch = sys.getswitchinterval()
+            sys.setswitchinterval(0.001)
             self.nvml = N
             self.t = threading.Thread(target=poll, daemon=True)
             self.t.start()
@@ -160,6 +168,11 @@ class ClockSampler:
         self.stop.set()
         if self.nvml is not None:
             self.t.join(timeout=1)
+            sys.setswitchinterval(self.switch)
+            try:
+                self.sample()  # the clock at the end of the timed region
+            except Exception:
+                pass
         if self.proc:
             self.proc.terminate()
             try:
